@@ -1,0 +1,174 @@
+/*
+ * dgx.h — C ABI of the B200-native batched grasp search (libdgx_cuda.so).
+ *
+ * Plain pointers and sizes only; no CUDA / C++ / torch types in signatures.
+ * Every entry point replaces one reference C++ interface of the hot path
+ * (/root/reference/proj/include/diffgrasp), batched over B candidates:
+ *
+ *   dgx_hand_upload            dg::HandModel (hand.hpp:53-102): descriptor of a
+ *                              loaded / assembled hand (samples in forward()
+ *                              order, hand.hpp:143-151)
+ *   dgx_object_upload          dg::GraspObject (losses.hpp:38-44): SDF backend
+ *                              + InertialData (rigid.hpp:8-13)
+ *   dgx_forward_batch          HandModel::forward(const HandConfig&) (hand.hpp:86)
+ *   dgx_loss_gradient_batch    dg::loss_gradient (losses.hpp:126-127, losses.cpp:20-66)
+ *   dgx_evaluate_losses_batch  dg::evaluate_losses (losses.hpp:119-121, losses.cpp:7-18)
+ *                              + SolveStats (sim.hpp:42-49) per perturbation
+ *   dgx_apply_gradient_step_batch  dg::apply_gradient_step (losses.hpp:136, losses.cpp:92-102)
+ *   dgx_optimize_batch         the synthesis loop the reference specifies but does
+ *                              not implement:
+ *                              linear dilation schedule + loss_gradient + Adam +
+ *                              apply_gradient_step, fused in one launch
+ *
+ * Layouts (row-major, double unless noted):
+ *   q      [B, 7+J]  base position (3) | base quaternion w,x,y,z (4) | joints (J)
+ *                    (dg::HandConfig, hand.hpp:15-19)
+ *   grads  [B, 3, 6+J]  d_stable | d_qrange | d_qlimit, each in the reference's
+ *                    gradient layout [pos 3 | orientation tangent 3 | joints J]
+ *                    (dg::LossGradient, losses.hpp:104-116)
+ *   losses [B, 3]    stable, qrange, qlimit (dg::LossBreakdown, losses.hpp:95-102)
+ *
+ * Errors: functions return DGX_OK or an error code; dgx_last_error() gives the
+ * thread-local message. Per-candidate failures (the reference throws
+ * std::runtime_error for that candidate, losses.cpp:15-16, tape.cpp:35-38) are
+ * reported in status[b] and do not affect other candidates.
+ * Calls are synchronous on the context's stream unless DGX_ASYNC is given.
+ */
+#ifndef DGX_H_
+#define DGX_H_
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define DGX_ABI_VERSION 1
+
+typedef struct dgx_ctx dgx_ctx;
+typedef struct dgx_hand dgx_hand;
+typedef struct dgx_object dgx_object;
+
+/* return / per-candidate status codes */
+enum {
+  DGX_OK = 0,
+  DGX_E_NONFINITE_LOSS = 1,  /* "loss evaluation produced a non-finite value" (losses.cpp:15-16) */
+  DGX_E_NONFINITE_GRAD = 2,  /* "tape: non-finite adjoint" (tape.cpp:35-38) */
+  DGX_E_CORR_OVERFLOW = 3,   /* more active corrections than the context's log capacity */
+  DGX_E_SLOT_OVERFLOW = 4,   /* more than 256 distinct contacts in one perturbation sim */
+  DGX_E_REPLAY = 5,          /* internal: adjoint replay disagreed with the forward */
+  DGX_E_INVALID = 100,       /* invalid argument (std::invalid_argument / runtime_error) */
+  DGX_E_CUDA = 101,
+  DGX_E_UNSUPPORTED = 102
+};
+
+/* flags */
+#define DGX_DEVICE_PTRS 1u  /* array arguments are device pointers on the context's device */
+#define DGX_ASYNC 2u        /* do not synchronize the stream before returning (device ptrs only) */
+
+typedef struct {
+  int32_t num_links, num_joints, num_samples;
+  const int32_t* topo;               /* [L] BFS order, parent before child (hand.hpp:97) */
+  const int32_t* link_parent_joint;  /* [L] -1 for the base link (hand.hpp:47) */
+  const int32_t* joint_parent;       /* [J] (hand.hpp:31) */
+  const int32_t* joint_child;        /* [J] (hand.hpp:32) */
+  const double* axis;                /* [J,3] unit, child origin frame (hand.hpp:33) */
+  const double* origin_R;            /* [J,9] row-major (hand.hpp:34) */
+  const double* origin_t;            /* [J,3] (hand.hpp:35) */
+  const double* lower;               /* [J] (hand.hpp:36) */
+  const double* upper;               /* [J] (hand.hpp:37) */
+  const double* samples;             /* [N,3] link-frame samples in forward() order */
+  const int32_t* sample_link;        /* [N] (hand.hpp:76) */
+} dgx_hand_desc;
+
+enum { DGX_SDF_SPHERE = 1, DGX_SDF_BOX = 2, DGX_SDF_GRID = 4 };
+
+typedef struct {
+  int32_t kind;
+  double center[3];        /* sphere / box */
+  double radius;           /* sphere */
+  double half_extents[3];  /* box */
+  int32_t dims[3];         /* grid nx, ny, nz (x fastest) */
+  double origin[3];        /* grid node (0,0,0) */
+  double spacing;          /* grid node spacing h */
+  double inv_spacing;      /* 1/h as used by the query (pass exactly what the oracle uses) */
+  const float* values;     /* grid [nz][ny][nx]; host memory (copied) */
+  double mass;             /* InertialData (rigid.hpp:8-13) */
+  double com[3];
+  double inertia_body_inv[9];
+} dgx_object_desc;
+
+typedef struct {
+  double dt;               /* SimParams::dt (sim.hpp:34) */
+  double mu;               /* SimParams::mu (sim.hpp:35) */
+  int32_t gs_iters;        /* SimParams::gs_iters (sim.hpp:36) */
+  int32_t steps;           /* StabilityProtocol::steps; only 1 is supported */
+  double dilation_radius;  /* SimParams::dilation_radius (sim.hpp:38) */
+  double alpha_leak;       /* LeakPolicy::alpha_leak (sim.hpp:23) */
+  int32_t num_velocities;  /* StabilityProtocol::velocities.size() (M <= 8) */
+  int32_t pad;
+  double velocities[8][3];
+  double w_stable, w_qrange, w_qlimit;  /* LossWeights (losses.hpp:31-35) */
+} dgx_params;
+
+typedef struct {
+  int32_t iters;           /* K: schedule length; r_k = r0 (1 - k/(K-1)) */
+  int32_t k_begin, k_end;  /* iterations [k_begin, k_end) run by this call */
+  int32_t record;          /* nonzero: write per-iterate losses + weighted grad to traj */
+  double r0, lr, beta1, beta2, eps;
+} dgx_opt;
+
+const char* dgx_last_error(void);
+int dgx_abi_version(void);
+
+int dgx_ctx_create(int device, dgx_ctx** out);
+int dgx_ctx_destroy(dgx_ctx* ctx);
+/* use an external cudaStream_t (NULL = the context's own stream) */
+int dgx_ctx_set_stream(dgx_ctx* ctx, void* cuda_stream);
+/* capacity of the per-perturbation active-correction log (default 1024) */
+int dgx_ctx_set_correction_capacity(dgx_ctx* ctx, int32_t cap);
+/* number of kernels this context has launched */
+int64_t dgx_ctx_launch_count(const dgx_ctx* ctx);
+
+int dgx_hand_upload(dgx_ctx* ctx, const dgx_hand_desc* desc, dgx_hand** out);
+int dgx_hand_free(dgx_hand* hand);
+int dgx_object_upload(dgx_ctx* ctx, const dgx_object_desc* desc, dgx_object** out);
+int dgx_object_free(dgx_object* obj);
+
+/* points [B, N, 3] = HandModel::forward(q_b) */
+int dgx_forward_batch(dgx_ctx* ctx, const dgx_hand* hand, int32_t B, const double* q, double* points,
+                      uint32_t flags);
+
+/* losses [B,3], grads [B,3,6+J] as dg::loss_gradient */
+int dgx_loss_gradient_batch(dgx_ctx* ctx, const dgx_hand* hand, const dgx_object* obj, int32_t B,
+                            const double* q, const dgx_params* params, double* losses, double* grads,
+                            int32_t* status, uint32_t flags);
+
+/* losses [B,3] as dg::evaluate_losses; stats [B,M,5] (active_contacts,
+   corrections, singular_skipped, max_penetration, max_friction_ratio) with
+   measure_residual; stats may be NULL */
+int dgx_evaluate_losses_batch(dgx_ctx* ctx, const dgx_hand* hand, const dgx_object* obj, int32_t B,
+                              const double* q, const dgx_params* params, double* losses, double* stats,
+                              int32_t* status, uint32_t flags);
+
+/* q_out [B,7+J] = apply_gradient_step(q_b, g_b, lr), g [B,6+J] */
+int dgx_apply_gradient_step_batch(dgx_ctx* ctx, const dgx_hand* hand, int32_t B, const double* q,
+                                  const double* g, double lr, double* q_out, uint32_t flags);
+
+/* Fused synthesis loop: q [B,7+J], adam_m / adam_v [B,6+J] updated in place;
+   traj [B, k_end-k_begin, 3+6+J] (losses, weighted gradient) when opt->record. */
+int dgx_optimize_batch(dgx_ctx* ctx, const dgx_hand* hand, const dgx_object* obj, int32_t B, double* q,
+                       double* adam_m, double* adam_v, const dgx_params* params, const dgx_opt* opt,
+                       double* traj, int32_t* status, uint32_t flags);
+
+/* Parity / debug: per-perturbation residuals [B,M], gradients [B,M,6+J] and
+   optionally d residual_m / d points [B,M,N,3] (pass NULL to skip). */
+int dgx_debug_sims(dgx_ctx* ctx, const dgx_hand* hand, const dgx_object* obj, int32_t B, const double* q,
+                   const dgx_params* params, double* sim_res, double* sim_grads, double* point_grads,
+                   int32_t* status, uint32_t flags);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* DGX_H_ */

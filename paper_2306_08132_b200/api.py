@@ -1,0 +1,268 @@
+"""Python mirror of the reference's diffgrasp API for the hot path, over the
+C-ABI (include/dgx.h). Names and argument meaning follow
+/root/reference/proj/include/diffgrasp:
+
+  SimParams / LeakPolicy       sim.hpp:22-40
+  StabilityProtocol.standard   losses.hpp:21-27
+  LossWeights                  losses.hpp:31-35
+  loss_gradient                losses.hpp:126-127   (batched: q is [B, 7+J])
+  evaluate_losses              losses.hpp:119-121   (+ SolveStats per perturbation)
+  apply_gradient_step          losses.hpp:136
+  HandModel.forward            hand.hpp:86
+
+Errors raise like the reference: invalid arguments -> ValueError
+(std::invalid_argument), per-candidate numeric failures are returned in
+``status`` and raised by ``check_status`` as RuntimeError with the
+reference's message. All compute runs in libdgx_cuda.so; there is no CPU
+path.
+"""
+from __future__ import annotations
+
+import ctypes as C
+from dataclasses import dataclass, field
+
+import numpy as np
+
+from . import capi
+from .model import HandDesc, ObjectDesc
+
+
+@dataclass
+class SimParams:
+    dt: float = 0.001
+    mu: float = 1.0
+    gs_iters: int = 8
+    dilation_radius: float = 0.0
+    alpha_leak: float = 0.1  # LeakPolicy::alpha_leak
+
+
+@dataclass
+class StabilityProtocol:
+    velocities: list = field(default_factory=list)
+    steps: int = 1
+
+    @staticmethod
+    def standard(speed: float = 0.5, steps: int = 1) -> "StabilityProtocol":
+        s = speed
+        return StabilityProtocol([(s, 0, 0), (-s, 0, 0), (0, s, 0), (0, -s, 0), (0, 0, s), (0, 0, -s), (0, 0, 0)],
+                                 steps)
+
+    @property
+    def m(self) -> int:
+        return len(self.velocities)
+
+
+@dataclass
+class LossWeights:
+    stable: float = 1.0
+    qrange: float = 0.01
+    qlimit: float = 1.0
+
+
+@dataclass
+class OptConfig:
+    """SURVEY App. C driver: linear dilation r0 -> 0, Adam, tangent-space step."""
+    iterations: int = 200
+    dilation_start_radius: float = 0.02
+    learning_rate: float = 1e-3
+    beta1: float = 0.9
+    beta2: float = 0.999
+    eps: float = 1e-8
+
+
+def params_c(params: SimParams, protocol: StabilityProtocol, weights: LossWeights | None = None) -> capi.ParamsC:
+    if params.dilation_radius < 0.0:
+        raise ValueError("dilation radius must be >= 0")
+    if not 1 <= protocol.m <= 8:
+        raise ValueError("protocol must have 1..8 velocities")
+    w = weights or LossWeights()
+    p = capi.ParamsC()
+    p.dt, p.mu, p.gs_iters, p.steps = params.dt, params.mu, params.gs_iters, protocol.steps
+    p.dilation_radius, p.alpha_leak = params.dilation_radius, params.alpha_leak
+    p.num_velocities = protocol.m
+    for m, v in enumerate(protocol.velocities):
+        for c in range(3):
+            p.velocities[m][c] = float(v[c])
+    p.w_stable, p.w_qrange, p.w_qlimit = w.stable, w.qrange, w.qlimit
+    return p
+
+
+class Context:
+    """One CUDA device + stream (dgx_ctx)."""
+
+    def __init__(self, device: int = 0, correction_capacity: int | None = None):
+        self.L = capi.load()
+        h = C.c_void_p()
+        capi.check(self.L.dgx_ctx_create(device, C.byref(h)))
+        self.h = h
+        self.device = device
+        if correction_capacity:
+            capi.check(self.L.dgx_ctx_set_correction_capacity(self.h, correction_capacity))
+
+    def set_stream(self, stream_ptr: int | None) -> None:
+        capi.check(self.L.dgx_ctx_set_stream(self.h, stream_ptr))
+
+    @property
+    def launches(self) -> int:
+        return int(self.L.dgx_ctx_launch_count(self.h))
+
+    def close(self) -> None:
+        if getattr(self, "h", None):
+            self.L.dgx_ctx_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+class Hand:
+    """A HandDesc resident on the device (dgx_hand)."""
+
+    def __init__(self, ctx: Context, desc: HandDesc):
+        self.ctx, self.desc = ctx, desc
+        d, keep = capi.hand_desc_c(desc)
+        h = C.c_void_p()
+        capi.check(ctx.L.dgx_hand_upload(ctx.h, C.byref(d), C.byref(h)))
+        self.h = h
+        self.J, self.N = desc.num_joints, desc.num_samples
+
+    def __del__(self):
+        try:
+            if self.h:
+                self.ctx.L.dgx_hand_free(self.h)
+                self.h = None
+        except Exception:
+            pass
+
+
+class GraspObject:
+    """An ObjectDesc resident on the device (dgx_object)."""
+
+    def __init__(self, ctx: Context, desc: ObjectDesc):
+        self.ctx, self.desc = ctx, desc
+        d, keep = capi.object_desc_c(desc)
+        h = C.c_void_p()
+        capi.check(ctx.L.dgx_object_upload(ctx.h, C.byref(d), C.byref(h)))
+        self.h = h
+
+    def __del__(self):
+        try:
+            if self.h:
+                self.ctx.L.dgx_object_free(self.h)
+                self.h = None
+        except Exception:
+            pass
+
+
+def _flags(*arrays) -> int:
+    dev = [not isinstance(a, np.ndarray) for a in arrays if a is not None]
+    if any(dev) and not all(dev):
+        raise ValueError("mix of host (numpy) and device (torch) arrays")
+    return capi.DGX_DEVICE_PTRS if dev and dev[0] else 0
+
+
+def _f64(a, shape):
+    a = np.ascontiguousarray(a, np.float64)
+    if a.shape != shape:
+        a = a.reshape(shape)
+    return a
+
+
+def check_status(status) -> None:
+    st = np.asarray(status)
+    bad = np.nonzero(st)[0]
+    if bad.size:
+        code = int(st[bad[0]])
+        raise RuntimeError(f"candidate {int(bad[0])}: {capi.STATUS_NAMES.get(code, code)}")
+
+
+def forward(ctx: Context, hand: Hand, q) -> np.ndarray:
+    q = _f64(q, (-1, 7 + hand.J))
+    out = np.zeros((q.shape[0], hand.N, 3))
+    capi.check(ctx.L.dgx_forward_batch(ctx.h, hand.h, q.shape[0], capi.ptr(q), capi.ptr(out), 0))
+    return out
+
+
+def loss_gradient(ctx: Context, obj: GraspObject, hand: Hand, q, protocol: StabilityProtocol, params: SimParams):
+    """Batched dg::loss_gradient → (losses [B,3], grads [B,3,6+J], status [B])."""
+    q = _f64(q, (-1, 7 + hand.J))
+    B = q.shape[0]
+    losses = np.zeros((B, 3))
+    grads = np.zeros((B, 3, 6 + hand.J))
+    status = np.zeros(B, np.int32)
+    p = params_c(params, protocol)
+    capi.check(ctx.L.dgx_loss_gradient_batch(ctx.h, hand.h, obj.h, B, capi.ptr(q), C.byref(p), capi.ptr(losses),
+                                             capi.ptr(grads), capi.ptr(status), 0))
+    return losses, grads, status
+
+
+def evaluate_losses(ctx: Context, obj: GraspObject, hand: Hand, q, protocol: StabilityProtocol, params: SimParams):
+    """Batched dg::evaluate_losses → (losses [B,3], stats [B,M,5], status [B])."""
+    q = _f64(q, (-1, 7 + hand.J))
+    B = q.shape[0]
+    losses = np.zeros((B, 3))
+    stats = np.zeros((B, protocol.m, 5))
+    status = np.zeros(B, np.int32)
+    p = params_c(params, protocol)
+    capi.check(ctx.L.dgx_evaluate_losses_batch(ctx.h, hand.h, obj.h, B, capi.ptr(q), C.byref(p), capi.ptr(losses),
+                                               capi.ptr(stats), capi.ptr(status), 0))
+    return losses, stats, status
+
+
+def apply_gradient_step(ctx: Context, hand: Hand, q, g, lr: float) -> np.ndarray:
+    q = _f64(q, (-1, 7 + hand.J))
+    g = _f64(g, (q.shape[0], 6 + hand.J))
+    out = np.zeros_like(q)
+    capi.check(ctx.L.dgx_apply_gradient_step_batch(ctx.h, hand.h, q.shape[0], capi.ptr(q), capi.ptr(g), lr,
+                                                   capi.ptr(out), 0))
+    return out
+
+
+def debug_sims(ctx: Context, obj: GraspObject, hand: Hand, q, protocol: StabilityProtocol, params: SimParams,
+               point_grads: bool = False):
+    """Per-perturbation residuals [B,M], gradients [B,M,6+J] (and d/dp [B,M,N,3])."""
+    q = _f64(q, (-1, 7 + hand.J))
+    B, M = q.shape[0], protocol.m
+    res = np.zeros((B, M))
+    g = np.zeros((B, M, 6 + hand.J))
+    gp = np.zeros((B, M, hand.N, 3)) if point_grads else None
+    status = np.zeros(B, np.int32)
+    p = params_c(params, protocol)
+    capi.check(ctx.L.dgx_debug_sims(ctx.h, hand.h, obj.h, B, capi.ptr(q), C.byref(p), capi.ptr(res), capi.ptr(g),
+                                    capi.ptr(gp), capi.ptr(status), 0))
+    return res, g, gp, status
+
+
+def optimize(ctx: Context, obj: GraspObject, hand: Hand, q, protocol: StabilityProtocol, params: SimParams,
+             weights: LossWeights, opt: OptConfig, k_begin: int = 0, k_end: int | None = None, adam_m=None,
+             adam_v=None, record: bool = False, flags: int | None = None):
+    """Fused synthesis loop (dgx_optimize_batch). numpy arrays: copied in/out
+    (host path, synchronous); torch CUDA tensors: updated in place on device."""
+    k_end = opt.iterations if k_end is None else k_end
+    D = 6 + hand.J
+    host = isinstance(q, np.ndarray) or not hasattr(q, "data_ptr")
+    if host:
+        q = np.array(q, np.float64, copy=True, order="C").reshape(-1, 7 + hand.J)
+        B = q.shape[0]
+        adam_m = np.zeros((B, D)) if adam_m is None else np.array(adam_m, np.float64, copy=True, order="C")
+        adam_v = np.zeros((B, D)) if adam_v is None else np.array(adam_v, np.float64, copy=True, order="C")
+        status = np.zeros(B, np.int32)
+        traj = np.zeros((B, k_end - k_begin, 3 + D)) if record else None
+    else:
+        import torch
+        B = q.shape[0]
+        dev = q.device
+        adam_m = torch.zeros((B, D), dtype=torch.float64, device=dev) if adam_m is None else adam_m
+        adam_v = torch.zeros((B, D), dtype=torch.float64, device=dev) if adam_v is None else adam_v
+        status = torch.zeros(B, dtype=torch.int32, device=dev)
+        traj = torch.zeros((B, k_end - k_begin, 3 + D), dtype=torch.float64, device=dev) if record else None
+    p = params_c(params, protocol, weights)
+    o = capi.OptC(opt.iterations, k_begin, k_end, int(record), opt.dilation_start_radius, opt.learning_rate,
+                  opt.beta1, opt.beta2, opt.eps)
+    fl = _flags(q, adam_m, adam_v, status, traj) if flags is None else flags
+    capi.check(ctx.L.dgx_optimize_batch(ctx.h, hand.h, obj.h, B, capi.ptr(q), capi.ptr(adam_m), capi.ptr(adam_v),
+                                        C.byref(p), C.byref(o), capi.ptr(traj), capi.ptr(status), fl))
+    return dict(q=q, m=adam_m, v=adam_v, status=status, traj=traj)

@@ -1,0 +1,475 @@
+// dgx_capi.cu — implementation of include/dgx.h over the sm_100a kernels.
+#include <cuda_runtime.h>
+
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "../../include/dgx.h"
+#include "dgx_kernel.cuh"
+
+using namespace dgx;
+
+namespace {
+
+thread_local std::string g_err;
+
+struct DgxError : std::runtime_error {
+  int code;
+  DgxError(int c, const std::string& m) : std::runtime_error(m), code(c) {}
+};
+
+void cuda_check(cudaError_t e, const char* what) {
+  if (e != cudaSuccess) throw DgxError(DGX_E_CUDA, std::string(what) + ": " + cudaGetErrorString(e));
+}
+
+template <class F>
+int guarded(F&& f) {
+  try {
+    f();
+    return DGX_OK;
+  } catch (const DgxError& e) {
+    g_err = e.what();
+    return e.code;
+  } catch (const std::exception& e) {
+    g_err = e.what();
+    return DGX_E_INVALID;
+  }
+}
+
+struct DevBuf {
+  void* p = nullptr;
+  size_t n = 0;
+  void ensure(size_t bytes) {
+    if (bytes <= n) return;
+    if (p) cudaFree(p);
+    p = nullptr;
+    n = 0;
+    cuda_check(cudaMalloc(&p, bytes), "cudaMalloc");
+    n = bytes;
+  }
+  void release() {
+    if (p) cudaFree(p);
+    p = nullptr;
+    n = 0;
+  }
+};
+
+}  // namespace
+
+struct dgx_ctx {
+  int device = 0;
+  int num_sms = 0;
+  cudaStream_t own = nullptr;
+  cudaStream_t stream = nullptr;
+  int cap_corr = 1024;
+  int64_t launches = 0;
+  DevBuf corr, slots, io;
+};
+
+struct dgx_hand {
+  dgx_ctx* ctx;
+  int L, J, N;
+  DevBuf mem;
+  KHand k;
+  std::vector<double> lower, upper;
+};
+
+struct dgx_object {
+  dgx_ctx* ctx;
+  int kind;
+  SphereSdf sphere{};
+  BoxSdf box{};
+  GridSdf grid{};
+  DevBuf vals;
+  KObj k;
+};
+
+namespace {
+
+void set_device(dgx_ctx* c) { cuda_check(cudaSetDevice(c->device), "cudaSetDevice"); }
+
+KSim make_sim(const dgx_params* p, bool eval) {
+  if (!p) throw DgxError(DGX_E_INVALID, "params is NULL");
+  if (p->steps != 1)
+    throw DgxError(DGX_E_UNSUPPORTED, "StabilityProtocol::steps != 1 is not supported by the fused kernel");
+  if (p->num_velocities < 1 || p->num_velocities > kMaxSims)
+    throw DgxError(DGX_E_INVALID, "protocol must have 1..8 velocities");
+  if (p->gs_iters < 0) throw DgxError(DGX_E_INVALID, "gs_iters must be >= 0");
+  if (p->dilation_radius < 0.0) throw std::invalid_argument("dilation radius must be >= 0");
+  if (!(p->dt > 0.0)) throw DgxError(DGX_E_INVALID, "dt must be > 0");
+  KSim s{};
+  s.dt = p->dt;
+  s.mu = p->mu;
+  s.alpha = p->alpha_leak;
+  s.radius = p->dilation_radius;
+  s.gs = p->gs_iters;
+  s.M = p->num_velocities;
+  s.measure_residual = eval ? 1 : 0;
+  for (int m = 0; m < s.M; ++m)
+    for (int c = 0; c < 3; ++c) s.vel[m][c] = p->velocities[m][c];
+  s.w_stable = p->w_stable;
+  s.w_qrange = p->w_qrange;
+  s.w_qlimit = p->w_qlimit;
+  return s;
+}
+
+// grid of persistent CTAs and the scratch it needs
+int prepare(dgx_ctx* c, const dgx_hand* h, const dgx_object* o, int M, int B, KBuf& buf, int& smem) {
+  smem = SmemLayout(h->N, h->L, M).total;
+  if (smem > 227 * 1024)
+    throw DgxError(DGX_E_UNSUPPORTED, "hand too large for one CTA's shared memory (N=" + std::to_string(h->N) + ")");
+  int per_sm = 0;
+  cuda_check(fused_occupancy(o->kind, M, smem, &per_sm), "occupancy");
+  if (per_sm < 1) throw DgxError(DGX_E_UNSUPPORTED, "fused kernel cannot be resident (registers/smem)");
+  int grid = c->num_sms * per_sm;
+  if (grid > B) grid = B;
+  if (grid < 1) grid = 1;
+  const size_t nws = static_cast<size_t>(grid) * M;
+  c->corr.ensure(nws * c->cap_corr * sizeof(CorrRec));
+  c->slots.ensure(nws * kSlotCap * (sizeof(SlotRec) + sizeof(int)));
+  buf.corr = static_cast<CorrRec*>(c->corr.p);
+  buf.slots = static_cast<SlotRec*>(c->slots.p);
+  buf.cap_corr = c->cap_corr;
+  buf.B = B;
+  return grid;
+}
+
+// host <-> device staging for non-device-pointer calls
+struct Staging {
+  dgx_ctx* c;
+  bool dev;
+  std::vector<std::pair<void*, std::pair<const void*, size_t>>> back;  // host dst, dev src, bytes
+  size_t off = 0;
+  explicit Staging(dgx_ctx* ctx, bool device_ptrs, size_t total) : c(ctx), dev(device_ptrs) {
+    if (!dev) c->io.ensure(total + 256 * 16);
+  }
+  template <class T>
+  T* in(const T* host, size_t count) {
+    if (dev || !host) return const_cast<T*>(host);
+    T* d = reinterpret_cast<T*>(static_cast<char*>(c->io.p) + off);
+    off += (count * sizeof(T) + 255) & ~size_t(255);
+    cuda_check(cudaMemcpyAsync(d, host, count * sizeof(T), cudaMemcpyHostToDevice, c->stream), "H2D");
+    return d;
+  }
+  template <class T>
+  T* out(T* host, size_t count, bool copy_in = false) {
+    if (dev || !host) return host;
+    T* d = reinterpret_cast<T*>(static_cast<char*>(c->io.p) + off);
+    off += (count * sizeof(T) + 255) & ~size_t(255);
+    if (copy_in) cuda_check(cudaMemcpyAsync(d, host, count * sizeof(T), cudaMemcpyHostToDevice, c->stream), "H2D");
+    back.push_back({host, {d, count * sizeof(T)}});
+    return d;
+  }
+  void finish(uint32_t flags) {
+    for (auto& b : back)
+      cuda_check(cudaMemcpyAsync(b.first, b.second.first, b.second.second, cudaMemcpyDeviceToHost, c->stream), "D2H");
+    if (!dev || !(flags & DGX_ASYNC)) cuda_check(cudaStreamSynchronize(c->stream), "sync");
+  }
+};
+
+size_t bytes_round(size_t n) { return (n + 255) & ~size_t(255); }
+
+}  // namespace
+
+extern "C" {
+
+const char* dgx_last_error(void) { return g_err.c_str(); }
+int dgx_abi_version(void) { return DGX_ABI_VERSION; }
+
+int dgx_ctx_create(int device, dgx_ctx** out) {
+  return guarded([&] {
+    if (!out) throw DgxError(DGX_E_INVALID, "out is NULL");
+    auto* c = new dgx_ctx();
+    c->device = device;
+    try {
+      set_device(c);
+      cudaDeviceProp prop;
+      cuda_check(cudaGetDeviceProperties(&prop, device), "cudaGetDeviceProperties");
+      if (prop.major < 10) throw DgxError(DGX_E_UNSUPPORTED, std::string("sm_100a device required, got ") + prop.name);
+      c->num_sms = prop.multiProcessorCount;
+      cuda_check(cudaStreamCreateWithFlags(&c->own, cudaStreamNonBlocking), "cudaStreamCreate");
+      c->stream = c->own;
+    } catch (...) {
+      delete c;
+      throw;
+    }
+    *out = c;
+  });
+}
+
+int dgx_ctx_destroy(dgx_ctx* c) {
+  return guarded([&] {
+    if (!c) return;
+    cudaSetDevice(c->device);
+    c->corr.release();
+    c->slots.release();
+    c->io.release();
+    if (c->own) cudaStreamDestroy(c->own);
+    delete c;
+  });
+}
+
+int dgx_ctx_set_stream(dgx_ctx* c, void* s) {
+  return guarded([&] { c->stream = s ? static_cast<cudaStream_t>(s) : c->own; });
+}
+
+int dgx_ctx_set_correction_capacity(dgx_ctx* c, int32_t cap) {
+  return guarded([&] {
+    if (cap < 1) throw DgxError(DGX_E_INVALID, "capacity must be >= 1");
+    c->cap_corr = cap;
+  });
+}
+
+int64_t dgx_ctx_launch_count(const dgx_ctx* c) { return c ? c->launches : 0; }
+
+int dgx_hand_upload(dgx_ctx* c, const dgx_hand_desc* d, dgx_hand** out) {
+  return guarded([&] {
+    if (!c || !d || !out) throw DgxError(DGX_E_INVALID, "NULL argument");
+    const int L = d->num_links, J = d->num_joints, N = d->num_samples;
+    if (L < 1 || J < 0 || N < 1) throw DgxError(DGX_E_INVALID, "hand: empty descriptor");
+    if (J + 6 > kMaxDim) throw DgxError(DGX_E_UNSUPPORTED, "hand: more than 26 joints");
+    if (L != J + 1) throw DgxError(DGX_E_INVALID, "hand: expected one parent joint per non-base link");
+    // validation mirrors hand.cpp:149-210
+    std::vector<int> seen(L, 0);
+    for (int k = 0; k < L; ++k) {
+      int li = d->topo[k];
+      if (li < 0 || li >= L || seen[li]) throw DgxError(DGX_E_INVALID, "hand: topo is not a permutation");
+      seen[li] = 1;
+      int pj = d->link_parent_joint[li];
+      if (k == 0 && pj >= 0) throw DgxError(DGX_E_INVALID, "hand: topo[0] must be the base link");
+      if (k > 0) {
+        if (pj < 0 || pj >= J) throw DgxError(DGX_E_INVALID, "hand: multiple base links");
+        if (d->joint_child[pj] != li) throw DgxError(DGX_E_INVALID, "hand: joint child mismatch");
+        int par = d->joint_parent[pj];
+        bool before = false;
+        for (int t = 0; t < k; ++t) before |= d->topo[t] == par;
+        if (!before) throw DgxError(DGX_E_INVALID, "hand: topo order must list parents before children");
+      }
+    }
+    for (int j = 0; j < J; ++j)
+      if (!(d->lower[j] < d->upper[j])) throw DgxError(DGX_E_INVALID, "hand: joint has lower >= upper limit");
+    for (int i = 0; i < N; ++i)
+      if (d->sample_link[i] < 0 || d->sample_link[i] >= L) throw DgxError(DGX_E_INVALID, "hand: bad sample_link");
+    auto* h = new dgx_hand();
+    h->ctx = c;
+    h->L = L; h->J = J; h->N = N;
+    h->lower.assign(d->lower, d->lower + J);
+    h->upper.assign(d->upper, d->upper + J);
+    size_t ints = 2 * bytes_round(4 * L) + 2 * bytes_round(4 * std::max(J, 1)) + bytes_round(4 * N);
+    size_t dbls = 2 * bytes_round(8 * 3 * std::max(J, 1)) + bytes_round(8 * 9 * std::max(J, 1)) +
+                  2 * bytes_round(8 * std::max(J, 1)) + bytes_round(8 * 3 * N);
+    try {
+      set_device(c);
+      h->mem.ensure(ints + dbls);
+      char* base = static_cast<char*>(h->mem.p);
+      size_t off = 0;
+      auto put = [&](const void* src, size_t bytes) {
+        void* dst = base + off;
+        if (bytes) cuda_check(cudaMemcpy(dst, src, bytes, cudaMemcpyHostToDevice), "hand upload");
+        off += bytes_round(std::max<size_t>(bytes, 1));
+        return dst;
+      };
+      KHand& k = h->k;
+      k.L = L; k.J = J; k.N = N;
+      k.topo = static_cast<const int*>(put(d->topo, 4 * L));
+      k.link_parent_joint = static_cast<const int*>(put(d->link_parent_joint, 4 * L));
+      k.joint_parent = static_cast<const int*>(put(d->joint_parent, 4 * J));
+      k.joint_child = static_cast<const int*>(put(d->joint_child, 4 * J));
+      k.sample_link = static_cast<const int*>(put(d->sample_link, 4 * N));
+      k.axis = static_cast<const double*>(put(d->axis, 8 * 3 * J));
+      k.origin_t = static_cast<const double*>(put(d->origin_t, 8 * 3 * J));
+      k.origin_R = static_cast<const double*>(put(d->origin_R, 8 * 9 * J));
+      k.lower = static_cast<const double*>(put(d->lower, 8 * J));
+      k.upper = static_cast<const double*>(put(d->upper, 8 * J));
+      k.samples = static_cast<const double*>(put(d->samples, 8 * 3 * N));
+    } catch (...) {
+      h->mem.release();
+      delete h;
+      throw;
+    }
+    *out = h;
+  });
+}
+
+int dgx_hand_free(dgx_hand* h) {
+  return guarded([&] {
+    if (!h) return;
+    cudaSetDevice(h->ctx->device);
+    h->mem.release();
+    delete h;
+  });
+}
+
+int dgx_object_upload(dgx_ctx* c, const dgx_object_desc* d, dgx_object** out) {
+  return guarded([&] {
+    if (!c || !d || !out) throw DgxError(DGX_E_INVALID, "NULL argument");
+    if (!(d->mass > 0.0)) throw DgxError(DGX_E_INVALID, "object: mass must be > 0");
+    auto* o = new dgx_object();
+    o->ctx = c;
+    o->kind = d->kind;
+    try {
+      set_device(c);
+      if (d->kind == DGX_SDF_SPHERE) {
+        if (!(d->radius > 0.0)) throw DgxError(DGX_E_INVALID, "sphere: radius must be > 0");
+        o->sphere = SphereSdf{V3{d->center[0], d->center[1], d->center[2]}, d->radius};
+      } else if (d->kind == DGX_SDF_BOX) {
+        o->box = BoxSdf{V3{d->center[0], d->center[1], d->center[2]},
+                        V3{d->half_extents[0], d->half_extents[1], d->half_extents[2]}};
+      } else if (d->kind == DGX_SDF_GRID) {
+        if (d->dims[0] < 2 || d->dims[1] < 2 || d->dims[2] < 2 || !d->values)
+          throw DgxError(DGX_E_INVALID, "grid: dims must be >= 2 and values non-NULL");
+        size_t n = static_cast<size_t>(d->dims[0]) * d->dims[1] * d->dims[2];
+        o->vals.ensure(n * sizeof(float));
+        cuda_check(cudaMemcpy(o->vals.p, d->values, n * sizeof(float), cudaMemcpyHostToDevice), "grid upload");
+        o->grid = GridSdf{d->dims[0], d->dims[1], d->dims[2], V3{d->origin[0], d->origin[1], d->origin[2]},
+                          d->spacing, d->inv_spacing, static_cast<const float*>(o->vals.p)};
+      } else {
+        throw DgxError(DGX_E_UNSUPPORTED, "object: unknown SDF kind " + std::to_string(d->kind));
+      }
+      o->k.mass = d->mass;
+      o->k.com = V3{d->com[0], d->com[1], d->com[2]};
+      for (int t = 0; t < 9; ++t) o->k.inertia_body_inv.m[t] = d->inertia_body_inv[t];
+    } catch (...) {
+      o->vals.release();
+      delete o;
+      throw;
+    }
+    *out = o;
+  });
+}
+
+int dgx_object_free(dgx_object* o) {
+  return guarded([&] {
+    if (!o) return;
+    cudaSetDevice(o->ctx->device);
+    o->vals.release();
+    delete o;
+  });
+}
+
+int dgx_forward_batch(dgx_ctx* c, const dgx_hand* h, int32_t B, const double* q, double* points, uint32_t flags) {
+  return guarded([&] {
+    if (B < 0) throw DgxError(DGX_E_INVALID, "B < 0");
+    if (B == 0) return;
+    set_device(c);
+    const bool dev = flags & DGX_DEVICE_PTRS;
+    Staging s(c, dev, bytes_round(8ull * B * (7 + h->J)) + bytes_round(24ull * B * h->N));
+    const double* dq = s.in(q, static_cast<size_t>(B) * (7 + h->J));
+    double* dp = s.out(points, static_cast<size_t>(B) * h->N * 3);
+    int grid = std::min(B, c->num_sms * 4);
+    cuda_check(launch_forward(h->k, dq, dp, B, grid, c->stream), "forward_kernel");
+    ++c->launches;
+    s.finish(flags);
+  });
+}
+
+static void run_fused(dgx_ctx* c, const dgx_hand* h, const dgx_object* o, int32_t B, const double* q,
+                      double* qio, double* am, double* av, const KSim& S, const KOpt& P, int mode, double* losses,
+                      double* grads, double* stats, double* sim_res, double* sim_grads, double* point_grads,
+                      double* traj, int32_t* status, uint32_t flags) {
+  if (!c || !h || !o) throw DgxError(DGX_E_INVALID, "NULL handle");
+  if (B < 0) throw DgxError(DGX_E_INVALID, "B < 0");
+  if (B == 0) return;
+  set_device(c);
+  const bool dev = flags & DGX_DEVICE_PTRS;
+  const int M = S.M, D = 6 + h->J, Qd = 7 + h->J, N = h->N;
+  const int steps = mode == kModeOpt ? (P.k_end - P.k_begin) : 0;
+  size_t total = bytes_round(8ull * B * Qd) + 2 * bytes_round(8ull * B * D) + bytes_round(8ull * B * 3) +
+                 bytes_round(8ull * B * 3 * D) + bytes_round(8ull * B * M * 5) + bytes_round(8ull * B * M) +
+                 bytes_round(8ull * B * M * D) + (point_grads ? bytes_round(24ull * B * M * N) : 0) +
+                 (traj ? bytes_round(8ull * B * steps * (3 + D)) : 0) + bytes_round(4ull * B);
+  Staging s(c, dev, total);
+  KBuf buf{};
+  if (mode == kModeOpt) {
+    buf.q = s.out(qio, static_cast<size_t>(B) * Qd, true);
+    buf.adam_m = s.out(am, static_cast<size_t>(B) * D, true);
+    buf.adam_v = s.out(av, static_cast<size_t>(B) * D, true);
+  } else {
+    buf.q = const_cast<double*>(s.in(q, static_cast<size_t>(B) * Qd));
+  }
+  buf.losses = s.out(losses, static_cast<size_t>(B) * 3);
+  buf.grads = s.out(grads, static_cast<size_t>(B) * 3 * D);
+  buf.stats = s.out(stats, static_cast<size_t>(B) * M * 5);
+  buf.sim_res = s.out(sim_res, static_cast<size_t>(B) * M);
+  buf.sim_grads = s.out(sim_grads, static_cast<size_t>(B) * M * D);
+  buf.point_grads = s.out(point_grads, static_cast<size_t>(B) * M * N * 3);
+  buf.traj = s.out(traj, static_cast<size_t>(B) * steps * (3 + D));
+  if (!status) throw DgxError(DGX_E_INVALID, "status is NULL");
+  buf.status = s.out(status, static_cast<size_t>(B));
+  if (point_grads) cuda_check(cudaMemsetAsync(buf.point_grads, 0, 24ull * B * M * N, c->stream), "memset");
+  int smem = 0;
+  int grid = prepare(c, h, o, M, B, buf, smem);
+  cuda_check(launch_fused(h->k, o->k, o->kind, o->sphere, o->box, o->grid, S, P, buf, mode, grid, smem, c->stream),
+             "fused_kernel");
+  ++c->launches;
+  s.finish(flags);
+}
+
+int dgx_loss_gradient_batch(dgx_ctx* c, const dgx_hand* h, const dgx_object* o, int32_t B, const double* q,
+                            const dgx_params* p, double* losses, double* grads, int32_t* status, uint32_t flags) {
+  return guarded([&] {
+    KSim S = make_sim(p, false);
+    KOpt P{};
+    run_fused(c, h, o, B, q, nullptr, nullptr, nullptr, S, P, kModeGrad, losses, grads, nullptr, nullptr, nullptr,
+              nullptr, nullptr, status, flags);
+  });
+}
+
+int dgx_evaluate_losses_batch(dgx_ctx* c, const dgx_hand* h, const dgx_object* o, int32_t B, const double* q,
+                              const dgx_params* p, double* losses, double* stats, int32_t* status, uint32_t flags) {
+  return guarded([&] {
+    KSim S = make_sim(p, true);
+    KOpt P{};
+    run_fused(c, h, o, B, q, nullptr, nullptr, nullptr, S, P, kModeEval, losses, nullptr, stats, nullptr, nullptr,
+              nullptr, nullptr, status, flags);
+  });
+}
+
+int dgx_debug_sims(dgx_ctx* c, const dgx_hand* h, const dgx_object* o, int32_t B, const double* q,
+                   const dgx_params* p, double* sim_res, double* sim_grads, double* point_grads, int32_t* status,
+                   uint32_t flags) {
+  return guarded([&] {
+    KSim S = make_sim(p, false);
+    KOpt P{};
+    run_fused(c, h, o, B, q, nullptr, nullptr, nullptr, S, P, kModeGrad, nullptr, nullptr, nullptr, sim_res,
+              sim_grads, point_grads, nullptr, status, flags);
+  });
+}
+
+int dgx_optimize_batch(dgx_ctx* c, const dgx_hand* h, const dgx_object* o, int32_t B, double* q, double* am,
+                       double* av, const dgx_params* p, const dgx_opt* opt, double* traj, int32_t* status,
+                       uint32_t flags) {
+  return guarded([&] {
+    if (!opt) throw DgxError(DGX_E_INVALID, "opt is NULL");
+    if (opt->iters < 1 || opt->k_begin < 0 || opt->k_end < opt->k_begin || opt->k_end > opt->iters)
+      throw DgxError(DGX_E_INVALID, "opt: need 0 <= k_begin <= k_end <= iters, iters >= 1");
+    if (!(opt->lr > 0.0)) throw DgxError(DGX_E_INVALID, "opt: learning rate must be > 0");
+    KSim S = make_sim(p, false);
+    KOpt P{opt->iters, opt->k_begin, opt->k_end, opt->record, opt->r0, opt->lr, opt->beta1, opt->beta2, opt->eps};
+    run_fused(c, h, o, B, nullptr, q, am, av, S, P, kModeOpt, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr,
+              opt->record ? traj : nullptr, status, flags);
+  });
+}
+
+int dgx_apply_gradient_step_batch(dgx_ctx* c, const dgx_hand* h, int32_t B, const double* q, const double* g,
+                                  double lr, double* q_out, uint32_t flags) {
+  return guarded([&] {
+    if (B <= 0) return;
+    set_device(c);
+    const bool dev = flags & DGX_DEVICE_PTRS;
+    const int Qd = 7 + h->J, D = 6 + h->J;
+    Staging s(c, dev, 2 * bytes_round(8ull * B * Qd) + bytes_round(8ull * B * D));
+    const double* dq = s.in(q, static_cast<size_t>(B) * Qd);
+    const double* dg = s.in(g, static_cast<size_t>(B) * D);
+    double* dout = s.out(q_out, static_cast<size_t>(B) * Qd);
+    cuda_check(launch_step(h->J, dq, dg, lr, dout, B, c->stream), "step_kernel");
+    ++c->launches;
+    s.finish(flags);
+  });
+}
+
+}  // extern "C"

@@ -1,0 +1,987 @@
+// dgx_kernels.cu — the fused batched grasp-search kernel for sm_100a.
+//
+// One CTA per grasp candidate (persistent grid-stride), one warp per
+// perturbation simulation (M = 7, losses.hpp:21-27). Per candidate-iteration:
+//
+//   1. FK (HandModel::forward<Rec>, hand.hpp:116-152; record_pose_vars,
+//      hand.cpp:246-257) -> world points in shared memory (SoA, FP64).
+//   2. Per warp: predict (sim.hpp:74-83), then the Gauss-Seidel contact solve
+//      (ContactSolver::solve, sim.hpp:138-210) with SPECULATIVE lanes: 32
+//      consecutive points are evaluated against the current state, the first
+//      active lane (ballot) is applied serially, evaluation restarts right after
+//      it. Inactive points never change forward values (the zero-depth axpy,
+//      sim.hpp:105-125), so this reproduces the sequential sweep exactly.
+//      Friction (sim.hpp:247-274) in point order, finalize (sim.hpp:276-287),
+//      residual |xdot| + |thetadot| (losses.hpp:47-57).
+//   3. Per warp: hand-written adjoint of the recorded path (the reference tape,
+//      tape.cpp:27-114): residual -> finalize -> friction (reverse) -> sweeps in
+//      reverse. Only active corrections are logged; inactive runs between them
+//      are recomputed and their leak channel (sim.hpp:105-125, gate backward
+//      -alpha, tape.hpp:179-185) is a 3-vector affine recurrence on adj_x.
+//      Point adjoints are folded straight into per-link force/torque sums.
+//   4. Warp 0: FK adjoint (per-joint a_j . (T_sub - o_j x F_sub)), qrange /
+//      qlimit (losses.hpp:70-93), the losses.cpp:20-66 reductions, and for
+//      the optimizer the shared App. C driver (Adam + apply_gradient_step,
+//      losses.cpp:92-102).
+//
+// Built with --fmad=false: every forward value is the same IEEE op sequence
+// as the reference, so activations / corrections are bit-exact. Adjoint code
+// uses explicit fma().
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+#include "dgx_adjoint.cuh"
+#include "dgx_kernel.cuh"
+
+namespace dgx {
+
+constexpr unsigned kFull = 0xffffffffu;
+
+__device__ __forceinline__ double shfl(double v, int l) { return __shfl_sync(kFull, v, l); }
+__device__ __forceinline__ V3 shfl(V3 v, int l) { return V3{shfl(v.x, l), shfl(v.y, l), shfl(v.z, l)}; }
+__device__ __forceinline__ double warp_sum(double v) {
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(kFull, v, o);
+  return v;
+}
+__device__ __forceinline__ double warp_max(double v) {
+  for (int o = 16; o > 0; o >>= 1) {
+    double w = __shfl_xor_sync(kFull, v, o);
+    v = v < w ? w : v;
+  }
+  return v;
+}
+
+struct SimEnv {
+  int lane, N, gs;
+  const double *px, *py, *pz;
+  const int* sample_link;
+  unsigned* bitmap;
+  int* slot_point;
+  double* stage;
+  double* ft;             // [L*6] this warp's link force / torque accumulators
+  CorrRec* corr;
+  SlotRec* slots;
+  int* fric_order;
+  int cap_corr;
+  double inv_mass, radius, alpha, mu, dt;
+  V3 com;
+  M3 Ibody_inv;           // InertialData::inertia_body_inv (rigid.hpp:12)
+  M3 Iw;                  // world inverse inertia frozen at the predicted pose
+  double* point_grads;    // debug, may be null
+};
+
+struct PointEval {
+  V3 p, rel, rl;
+  SdfQuery q;
+  double rho_d;
+  bool fb;
+};
+
+// rel = p - x; r_local = R^T rel + com (sim.hpp:160-161); dilated SDF value in
+// recorded (sdf.cpp:140-164) or forward-only (sdf.cpp:126-138) semantics.
+template <class Sdf>
+__device__ __forceinline__ void eval_point(const Sdf& sdf, const SimEnv& e, int i, V3 x, const M3& R,
+                                           bool record, PointEval& pe) {
+  pe.p = V3{e.px[i], e.py[i], e.pz[i]};
+  pe.rel = pe.p - x;
+  pe.rl = tmul(R, pe.rel) + e.com;
+  pe.q = sdf.query(pe.rl);
+  pe.fb = fabs(pe.q.rho) < kSurfaceEps;
+  if (record && pe.fb) {
+    V3 dx = pe.rl - pe.q.proxy;
+    double proj = dx.x * pe.q.grad.x + dx.y * pe.q.grad.y + dx.z * pe.q.grad.z;
+    pe.rho_d = static_cast<double>(pe.q.sign) * proj - e.radius;
+  } else {
+    pe.rho_d = pe.q.rho - e.radius;
+  }
+}
+
+// per-lane link accumulator for d/dp, flushed to the warp's shared array
+struct FtAcc {
+  int link = -1;
+  V3 F{0.0, 0.0, 0.0}, T{0.0, 0.0, 0.0};
+  __device__ __forceinline__ void flush(double* ft) {
+    if (link >= 0) {
+      double* d = ft + 6 * link;
+      atomicAdd(d + 0, F.x); atomicAdd(d + 1, F.y); atomicAdd(d + 2, F.z);
+      atomicAdd(d + 3, T.x); atomicAdd(d + 4, T.y); atomicAdd(d + 5, T.z);
+    }
+    link = -1;
+    F = V3{0.0, 0.0, 0.0};
+    T = V3{0.0, 0.0, 0.0};
+  }
+  __device__ __forceinline__ void add(double* ft, int l, V3 ap, V3 p) {
+    if (l != link) {
+      flush(ft);
+      link = l;
+    }
+    F = F + ap;
+    T = T + cross(p, ap);
+  }
+};
+
+__device__ __forceinline__ void add_point_grad(const SimEnv& e, int i, V3 ap) {
+  if (e.point_grads) {
+    atomicAdd(e.point_grads + 3 * i, ap.x);
+    atomicAdd(e.point_grads + 3 * i + 1, ap.y);
+    atomicAdd(e.point_grads + 3 * i + 2, ap.z);
+  }
+}
+
+struct SimStats {
+  int active = 0, corrections = 0, singular = 0;
+  double max_pen = 0.0, max_fric = 0.0;
+};
+
+// warp-parallel lookup of the slot owning point i (slot_point in shared mem)
+__device__ __forceinline__ int find_slot(const SimEnv& e, int nslot, int i) {
+  for (int base = 0; base < nslot; base += 32) {
+    int s = base + e.lane;
+    unsigned hit = __ballot_sync(kFull, s < nslot && e.slot_point[s] == i);
+    if (hit) return base + __ffs(hit) - 1;
+  }
+  return -1;
+}
+
+// ContactSolver::apply_friction (sim.hpp:247-274) on values; returns whether
+// the state changed. Friction-ratio stat as sim.hpp:266-272.
+__device__ __forceinline__ bool friction_fwd(const SimEnv& e, V3 prev_x, Q4 prev_q, V3& x, Q4& q, V3 rb, V3 n,
+                                             double lambda_n, SimStats& st) {
+  V3 before = prev_x + rotate(prev_q, rb);
+  V3 arm = rotate(q, rb);
+  V3 after = x + arm;
+  V3 u = after - before;
+  V3 u_t = u - n * dot(u, n);
+  double ut = norm(u_t);
+  if (ut < 1e-12) return false;
+  V3 t = u_t / ut;
+  V3 at = cross(arm, t);
+  V3 iwat = mul(e.Iw, at);
+  double w_t = e.inv_mass + dot(at, iwat);
+  if (w_t < 1e-12) return false;
+  double a1 = ut / w_t, a2 = e.mu * lambda_n;
+  double lam_t = a1 <= a2 ? a1 : a2;
+  x = x - t * (e.inv_mass * lam_t);
+  q = qnormalized(qmul(quat_exp(iwat * (-lam_t)), q));
+  ++st.corrections;
+  double denom = e.mu * lambda_n;
+  if (denom > 0.0) {
+    double r = lam_t / denom;
+    st.max_fric = st.max_fric < r ? r : st.max_fric;
+  }
+  return true;
+}
+
+// Reverse of friction_fwd for one applied slot; aX/aQ: adjoints of the state
+// after it (in) and before it (out). Accumulates the slot's a_lam / a_n.
+__device__ __forceinline__ void friction_adj(const SimEnv& e, V3 prev_x, Q4 prev_q, const SlotRec& s, V3& aX, Q4& aQ,
+                                             double& a_lam_slot, V3& a_n_slot) {
+  V3 rb{s.rb[0], s.rb[1], s.rb[2]};
+  V3 n{s.n[0], s.n[1], s.n[2]};
+  V3 fx{s.fx[0], s.fx[1], s.fx[2]};
+  Q4 fq{s.fq[0], s.fq[1], s.fq[2], s.fq[3]};
+  V3 before = prev_x + rotate(prev_q, rb);
+  V3 arm = rotate(fq, rb);
+  V3 u = (fx + arm) - before;
+  double d = dot(u, n);
+  V3 u_t = u - n * d;
+  double ut = norm(u_t);
+  V3 t = u_t / ut;
+  V3 at = cross(arm, t);
+  V3 iwat = mul(e.Iw, at);
+  double w_t = e.inv_mass + dot(at, iwat);
+  double a1 = ut / w_t, a2 = e.mu * s.lambda_n;
+  bool first = a1 <= a2;
+  double lam_t = first ? a1 : a2;
+  V3 om = iwat * (-lam_t);
+  Q4 E = quat_exp(om);
+  Q4 P = qmul(E, fq);
+  // x_out = fx - t (m^-1 lam_t)
+  V3 a_t = aX * (-e.inv_mass * lam_t);
+  double a_lamt = -e.inv_mass * fdot(t, aX);
+  // q_out = normalized(E (x) fq)
+  Q4 a_P = qnormalize_adj(P, aQ);
+  Q4 a_E = qmul_adj_a(a_P, fq);
+  Q4 aQ_in = qmul_adj_b(a_P, E);
+  V3 a_om = quat_exp_adj(om, a_E);
+  a_lamt -= fdot(iwat, a_om);
+  V3 a_iwat = a_om * (-lam_t);
+  double a_a1 = first ? a_lamt : 0.0;
+  double a_a2 = first ? 0.0 : a_lamt;
+  a_lam_slot = fma(e.mu, a_a2, a_lam_slot);
+  double a_ut = a_a1 / w_t;
+  double a_wt = -a_a1 * a1 / w_t;
+  V3 a_at = iwat * a_wt;
+  a_iwat = fma3(a_wt, at, a_iwat);
+  a_at = a_at + ftmul(e.Iw, a_iwat);
+  V3 a_arm = cross(t, a_at);
+  a_t = a_t + cross(a_at, arm);
+  V3 a_utv = a_t / ut;
+  a_ut -= fdot(a_t, t) / ut;
+  a_utv = fma3(a_ut / ut, u_t, a_utv);
+  V3 a_u = a_utv;
+  V3 a_n = a_utv * (-d);
+  double a_d = -fdot(n, a_utv);
+  a_u = fma3(a_d, n, a_u);
+  a_n = fma3(a_d, u, a_n);
+  a_n_slot = a_n_slot + a_n;
+  aX = aX + a_u;
+  a_arm = a_arm + a_u;
+  Q4 r = rotate_adj_q(fq, rb, a_arm);
+  aQ = qadd(aQ_in, r);
+}
+
+// Warp-wide all-reduce of a per-lane 3x3 accumulator.
+__device__ __forceinline__ M3 warp_sum(const M3& A) {
+  M3 r;
+  for (int k = 0; k < 9; ++k) r.m[k] = warp_sum(A.m[k]);
+  return r;
+}
+
+// One perturbation simulation (losses.hpp:47-57 with T = 1), forward and,
+// when `record`, its adjoint. Returns the residual; status via `status`.
+template <class Sdf>
+__device__ double run_sim(const Sdf& sdf, SimEnv& e, V3 v_m, bool record, bool measure_residual, SimStats& st,
+                          int& status, FtAcc& acc) {
+  const int lane = e.lane, N = e.N;
+  // canonical_state (rigid.hpp:29-33) with xdot = v_m; predict (sim.hpp:74-83)
+  const V3 prev_x = e.com;
+  const Q4 prev_q{1.0, 0.0, 0.0, 0.0};
+  const V3 prev_thd{0.0, 0.0, 0.0};
+  const V3 pred_xdot = v_m + V3{0.0 * e.dt, 0.0 * e.dt, 0.0 * e.dt};
+  const V3 pred_x = prev_x + pred_xdot * e.dt;
+  const Q4 pred_q = qnormalized(qmul(quat_exp(prev_thd * e.dt), prev_q));
+  {  // world_inertia_inv at the predicted orientation (sim.hpp:96-100, 142)
+    const M3 Rp = rotation_matrix(pred_q);
+    e.Iw = mul(mul(Rp, e.Ibody_inv), transposed(Rp));
+  }
+  V3 x = pred_x;
+  Q4 q = pred_q;
+  M3 R = rotation_matrix(q);
+  bool touched = false;
+  const int nwords = (N + 31) / 32;
+  for (int w = lane; w < nwords; w += 32) e.bitmap[w] = 0u;
+  __syncwarp();
+
+  // ---- Gauss-Seidel sweeps (sim.hpp:157-186) -------------------------------
+  int ncorr = 0, nslot = 0;
+  int pos = 0, sweep = 0;
+  while (sweep < e.gs) {
+    const int i = pos + lane;
+    PointEval pe;
+    bool act = false;
+    if (i < N) {
+      eval_point(sdf, e, i, x, R, record, pe);
+      act = record ? (pe.rho_d < 0.0) : !(pe.rho_d >= 0.0);
+    }
+    const unsigned mask = __ballot_sync(kFull, act);
+    if (mask == 0u) {
+      pos += 32;
+      if (pos >= N) { pos = 0; ++sweep; }
+      continue;
+    }
+    const int j = __ffs(mask) - 1;
+    const int ij = pos + j;
+    const V3 rel = shfl(pe.rel, j);
+    const V3 g = shfl(pe.q.grad, j);
+    const V3 pj = shfl(pe.p, j);
+    const double C = -shfl(pe.rho_d, j);
+    // apply_contact (sim.hpp:215-245)
+    const V3 n_w = mul(R, g);
+    const V3 a = cross(rel, n_w);
+    const V3 iwa = mul(e.Iw, a);
+    const double w = e.inv_mass + dot(a, iwa);
+    if (w < 1e-12) {
+      ++st.singular;
+    } else {
+      const double lam = C / w;
+      x = x - n_w * (e.inv_mass * lam);
+      q = qnormalized(qmul(quat_exp(iwa * (-lam)), q));
+      R = rotation_matrix(q);
+      touched = true;
+      const unsigned bit = 1u << (ij & 31);
+      const bool was = (e.bitmap[ij >> 5] & bit) != 0u;
+      int slot;
+      double lambda_n;
+      if (!was) {
+        slot = nslot;
+        if (slot >= kSlotCap) { status = kSlotOverflow; return 0.0; }
+        ++nslot;
+        lambda_n = 0.0 + lam;
+        if (lane == 0) {
+          e.bitmap[ij >> 5] |= bit;
+          e.slot_point[slot] = ij;
+          SlotRec& s = e.slots[slot];
+          V3 rb = tmul(R, pj - x);
+          s.rb[0] = rb.x; s.rb[1] = rb.y; s.rb[2] = rb.z;
+          s.a_lam = 0.0;
+          s.a_n[0] = s.a_n[1] = s.a_n[2] = 0.0;
+          s.point = ij;
+          s.fric = 0;
+        }
+      } else {
+        slot = find_slot(e, nslot, ij);
+        lambda_n = e.slots[slot].lambda_n + lam;
+      }
+      if (ncorr >= e.cap_corr) { status = kCorrOverflow; return 0.0; }
+      if (lane == 0) {
+        SlotRec& s = e.slots[slot];
+        s.lambda_n = lambda_n;
+        s.n[0] = n_w.x; s.n[1] = n_w.y; s.n[2] = n_w.z;
+        s.last_corr = ncorr;
+        CorrRec& c = e.corr[ncorr];
+        c.x[0] = x.x; c.x[1] = x.y; c.x[2] = x.z;
+        c.q[0] = q.w; c.q[1] = q.x; c.q[2] = q.y; c.q[3] = q.z;
+        c.lam = lam;
+        c.f = sweep * N + ij;
+        c.slot = slot;
+      }
+      ++ncorr;
+      ++st.corrections;
+      if (lambda_n == lam) ++st.active;
+      __syncwarp();
+    }
+    pos = ij + 1;
+    if (pos >= N) { pos = 0; ++sweep; }
+  }
+
+  // ---- friction (sim.hpp:188-196), active slots in point order -------------
+  int nfric = 0;
+  if (e.mu > 0.0) {
+    for (int wd = 0; wd < nwords; ++wd) {
+      unsigned bits = e.bitmap[wd];
+      while (bits) {
+        const int b = __ffs(bits) - 1;
+        bits &= bits - 1u;
+        const int pt = wd * 32 + b;
+        const int slot = find_slot(e, nslot, pt);
+        const SlotRec& s = e.slots[slot];
+        const double lambda_n = s.lambda_n;
+        if (lambda_n <= 0.0) continue;
+        const V3 x_in = x;
+        const Q4 q_in = q;
+        const bool applied =
+            friction_fwd(e, prev_x, prev_q, x, q, V3{s.rb[0], s.rb[1], s.rb[2]}, V3{s.n[0], s.n[1], s.n[2]},
+                         lambda_n, st);
+        if (applied) {
+          touched = true;
+          if (lane == 0) {
+            SlotRec& sw = e.slots[slot];
+            sw.fx[0] = x_in.x; sw.fx[1] = x_in.y; sw.fx[2] = x_in.z;
+            sw.fq[0] = q_in.w; sw.fq[1] = q_in.x; sw.fq[2] = q_in.y; sw.fq[3] = q_in.z;
+            sw.fric = 1;
+            e.fric_order[nfric] = slot;
+          }
+          ++nfric;
+        }
+        __syncwarp();
+      }
+    }
+  }
+
+  // ---- finalize_velocities (sim.hpp:276-287) and residual ------------------
+  V3 xdot, thd;
+  Q4 qd{0.0, 0.0, 0.0, 0.0};
+  const double inv_dt = 1.0 / e.dt;
+  if (!touched) {
+    xdot = pred_xdot;
+    thd = prev_thd;
+  } else {
+    xdot = (x - prev_x) * inv_dt;
+    qd = qmul(q, qconj(prev_q));
+    thd = quat_log(qd) * inv_dt;
+  }
+  const double n1 = norm(xdot), n2 = norm(thd);
+  const double residual = n1 + n2;
+
+  if (measure_residual) {  // sim.hpp:200-208
+    M3 Rf = rotation_matrix(q);
+    double mp = 0.0;
+    for (int i = lane; i < N; i += 32) {
+      V3 p{e.px[i], e.py[i], e.pz[i]};
+      V3 rl = tmul(Rf, p - x) + e.com;
+      SdfQuery qq = sdf.query(rl);
+      double rho = qq.rho - e.radius;
+      if (rho < 0.0) mp = mp < -rho ? -rho : mp;
+    }
+    st.max_pen = warp_max(mp);
+  }
+  if (!record || !touched) return residual;  // untouched: constant loss, zero gradient
+
+  // ---- adjoint: residual -> finalize ---------------------------------------
+  const V3 a_xdot = n1 > 0.0 ? xdot / n1 : V3{0.0, 0.0, 0.0};
+  const V3 a_thd = n2 > 0.0 ? thd / n2 : V3{0.0, 0.0, 0.0};
+  Q4 aQ = qmul_adj_a(quat_log_adj(qd, a_thd * inv_dt), qconj(prev_q));
+  V3 aX = a_xdot * inv_dt;
+
+  // ---- friction, reverse --------------------------------------------------
+  for (int k = nfric - 1; k >= 0; --k) {
+    const int slot = e.fric_order[k];
+    SlotRec s = e.slots[slot];
+    double a_lam = s.a_lam;
+    V3 a_n{s.a_n[0], s.a_n[1], s.a_n[2]};
+    friction_adj(e, prev_x, prev_q, s, aX, aQ, a_lam, a_n);
+    __syncwarp();
+    if (lane == 0) {
+      SlotRec& sw = e.slots[slot];
+      sw.a_lam = a_lam;
+      sw.a_n[0] = a_n.x; sw.a_n[1] = a_n.y; sw.a_n[2] = a_n.z;
+    }
+    __syncwarp();
+  }
+
+  // ---- sweeps, reverse ----------------------------------------------------
+  M3 aR;  // per-lane partial adjoint of the current R node
+  for (int k = 0; k < 9; ++k) aR.m[k] = 0.0;
+  int hi = e.gs * N;
+  double* stg = e.stage;
+  for (int k = ncorr - 1;; --k) {
+    // state of the run after correction k (predicted state for k < 0)
+    V3 xk = pred_x;
+    Q4 qk = pred_q;
+    if (k >= 0) {
+      const CorrRec& c = e.corr[k];
+      xk = V3{c.x[0], c.x[1], c.x[2]};
+      qk = Q4{c.q[0], c.q[1], c.q[2], c.q[3]};
+    }
+    const M3 Rk = rotation_matrix(qk);
+    const int lo = k >= 0 ? e.corr[k].f + 1 : 0;
+    {
+      // H . k == ([0,k] (x) q_k) . aQ (the leak's theta axpy coefficient, sim.hpp:118-124)
+      const V3 H{-qk.x * aQ.w + qk.w * aQ.x - qk.z * aQ.y + qk.y * aQ.z,
+                 -qk.y * aQ.w + qk.z * aQ.x + qk.w * aQ.y - qk.x * aQ.z,
+                 -qk.z * aQ.w - qk.y * aQ.x + qk.x * aQ.y + qk.w * aQ.z};
+      const V3 G = ftmul(e.Iw, H);
+      for (int top = hi; top > lo; top -= 32) {
+        const int f = top - 1 - lane;
+        PointEval pe;
+        V3 nw{0.0, 0.0, 0.0};
+        double c1 = 0.0, c0 = 0.0;
+        int i = 0;
+        bool contrib = false;
+        if (f >= lo) {
+          i = f % N;
+          eval_point(sdf, e, i, xk, Rk, true, pe);
+          if (pe.rho_d >= 0.0) {
+            nw = mul(Rk, pe.q.grad);
+            const V3 a = cross(pe.rel, nw);
+            const V3 Ia = mul(e.Iw, a);
+            const double w = e.inv_mass + dot(a, Ia);
+            if (w >= 1e-12) {
+              const double lpc = 1.0 / w;
+              const double kxs = e.inv_mass * lpc;
+              const double ee = -0.5 * lpc * fdot(a, G);
+              const double sg = pe.fb ? static_cast<double>(pe.q.sign) : 1.0;
+              c1 = e.alpha * kxs * sg;
+              c0 = -e.alpha * ee * sg;
+              contrib = true;
+            }
+          }
+        }
+        const unsigned cm = __ballot_sync(kFull, contrib);
+        if (cm == 0u) continue;
+        stg[lane] = nw.x;
+        stg[32 + lane] = nw.y;
+        stg[64 + lane] = nw.z;
+        stg[96 + lane] = c1;
+        stg[128 + lane] = c0;
+        __syncwarp();
+        double my_s = 0.0;
+        unsigned bits = cm;
+        while (bits) {
+          const int l = __ffs(bits) - 1;
+          bits &= bits - 1u;
+          const double nx = stg[l], ny = stg[32 + l], nz = stg[64 + l];
+          const double s = fma(stg[96 + l], fma(nz, aX.z, fma(ny, aX.y, nx * aX.x)), stg[128 + l]);
+          if (lane == l) my_s = s;
+          aX.x = fma(-s, nx, aX.x);
+          aX.y = fma(-s, ny, aX.y);
+          aX.z = fma(-s, nz, aX.z);
+        }
+        __syncwarp();
+        if (contrib) {
+          const V3 a_rl = pe.q.grad * my_s;
+          const V3 a_rel = nw * my_s;
+          outer_acc(aR, pe.rel, a_rl);
+          acc.add(e.ft, e.sample_link[i], a_rel, pe.p);
+          add_point_grad(e, i, a_rel);
+        }
+      }
+    }
+    if (k < 0) break;
+
+    // ---- active correction k (sim.hpp:215-245), reverse ----
+    const M3 aRk = warp_sum(aR);
+    aQ = qadd(aQ, rotmat_adj(qk, aRk));
+    for (int t = 0; t < 9; ++t) aR.m[t] = 0.0;
+    const CorrRec c = e.corr[k];
+    const int i = c.f % N;
+    V3 xb = pred_x;
+    Q4 qb = pred_q;
+    if (k >= 1) {
+      const CorrRec& cp = e.corr[k - 1];
+      xb = V3{cp.x[0], cp.x[1], cp.x[2]};
+      qb = Q4{cp.q[0], cp.q[1], cp.q[2], cp.q[3]};
+    }
+    const M3 Rb = rotation_matrix(qb);
+    PointEval pe;
+    eval_point(sdf, e, i, xb, Rb, true, pe);
+    const double C = -pe.rho_d;
+    const V3 g = pe.q.grad;
+    const V3 n_w = mul(Rb, g);
+    const V3 a = cross(pe.rel, n_w);
+    const V3 iwa = mul(e.Iw, a);
+    const double w = e.inv_mass + dot(a, iwa);
+    const double lam = C / w;
+    if (lam != c.lam) status = kReplayMismatch;
+    const V3 om = iwa * (-lam);
+    const Q4 E = quat_exp(om);
+    const Q4 P = qmul(E, qb);
+    const SlotRec& s = e.slots[c.slot];
+    double a_lam = s.a_lam;
+    V3 a_nw = s.last_corr == k ? V3{s.a_n[0], s.a_n[1], s.a_n[2]} : V3{0.0, 0.0, 0.0};
+    const Q4 a_P = qnormalize_adj(P, aQ);
+    const Q4 a_E = qmul_adj_a(a_P, qb);
+    const Q4 aQb = qmul_adj_b(a_P, E);
+    const V3 a_om = quat_exp_adj(om, a_E);
+    a_lam -= fdot(iwa, a_om);
+    V3 a_iwa = a_om * (-lam);
+    a_lam -= e.inv_mass * fdot(n_w, aX);
+    a_nw = fma3(-e.inv_mass * lam, aX, a_nw);
+    const double a_C = a_lam / w;
+    const double a_w = -a_lam * lam / w;
+    V3 a_a = iwa * a_w;
+    a_iwa = fma3(a_w, a, a_iwa);
+    a_a = a_a + ftmul(e.Iw, a_iwa);
+    V3 a_rel = cross(n_w, a_a);
+    a_nw = a_nw + cross(a_a, pe.rel);
+    const V3 a_g = ftmul(Rb, a_nw);
+    if (lane == 0) outer_acc(aR, a_nw, g);
+    const double a_rho = -a_C;  // gate active: dC/drho = -1
+    V3 a_rl;
+    if (pe.fb) {
+      a_rl = g * (static_cast<double>(pe.q.sign) * a_rho);
+    } else {
+      const V3 dx = pe.rl - pe.q.proxy;
+      const double dist = norm(dx);
+      const double inv = static_cast<double>(pe.q.sign) / dist;
+      double a_dist = static_cast<double>(pe.q.sign) * a_rho;
+      a_dist -= fdot(a_g, dx) * inv / dist;
+      a_rl = fma3(a_dist / dist, dx, a_g * inv);
+    }
+    a_rel = a_rel + fmul(Rb, a_rl);
+    if (lane == 0) {
+      outer_acc(aR, pe.rel, a_rl);
+      acc.add(e.ft, e.sample_link[i], a_rel, pe.p);
+      add_point_grad(e, i, a_rel);
+    }
+    aX = aX - a_rel;
+    aQ = aQb;
+    hi = c.f;
+  }
+  return residual;
+}
+
+// HandModel::forward (hand.hpp:116-152) link transforms, lane 0 serial over
+// the BFS order. base_q is the recorded orientation quat_exp(0) (x) q0
+// (hand.cpp:250-253) on the recorded path, q0 itself on the forward path.
+__device__ void link_transforms(const KHand& H, const double* qv, bool record, double* link) {
+  Q4 q0{qv[3], qv[4], qv[5], qv[6]};
+  Q4 base_q = record ? qmul(quat_exp(V3{0.0, 0.0, 0.0}), q0) : q0;
+  for (int k = 0; k < H.L; ++k) {
+    const int li = H.topo[k];
+    double* Rl = link + 12 * li;
+    const int pj = H.link_parent_joint[li];
+    M3 R;
+    V3 t;
+    if (pj < 0) {
+      R = rotation_matrix(base_q);
+      t = V3{qv[0], qv[1], qv[2]};
+    } else {
+      const double angle = qv[7 + pj];
+      const V3 ax{H.axis[3 * pj], H.axis[3 * pj + 1], H.axis[3 * pj + 2]};
+      const V3 rotvec{ax.x * angle, ax.y * angle, ax.z * angle};
+      const M3 Rj = rotation_matrix(quat_exp(rotvec));
+      M3 Ro;
+      for (int m = 0; m < 9; ++m) Ro.m[m] = H.origin_R[9 * pj + m];
+      const V3 to{H.origin_t[3 * pj], H.origin_t[3 * pj + 1], H.origin_t[3 * pj + 2]};
+      const double* Pp = link + 12 * H.joint_parent[pj];
+      M3 Rp;
+      for (int m = 0; m < 9; ++m) Rp.m[m] = Pp[m];
+      const V3 tp{Pp[9], Pp[10], Pp[11]};
+      R = mul(mul(Rp, Ro), Rj);
+      t = mul(Rp, to) + tp;
+    }
+    for (int m = 0; m < 9; ++m) Rl[m] = R.m[m];
+    Rl[9] = t.x; Rl[10] = t.y; Rl[11] = t.z;
+  }
+}
+
+// FK adjoint: link force/torque sums -> gradient [pos | tangent | joints]
+// (hand.cpp:246-257 layout). ft is consumed (subtree sums in place).
+__device__ void fk_adjoint(const KHand& H, const double* qv, const double* link, double* ft, double* g) {
+  for (int k = H.L - 1; k >= 1; --k) {
+    const int li = H.topo[k];
+    const int par = H.joint_parent[H.link_parent_joint[li]];
+    for (int c = 0; c < 6; ++c) ft[6 * par + c] += ft[6 * li + c];
+  }
+  const int base = H.topo[0];
+  const V3 F{ft[6 * base], ft[6 * base + 1], ft[6 * base + 2]};
+  const V3 T{ft[6 * base + 3], ft[6 * base + 4], ft[6 * base + 5]};
+  const V3 pos{qv[0], qv[1], qv[2]};
+  const V3 tau = T - cross(pos, F);
+  g[0] = F.x; g[1] = F.y; g[2] = F.z;
+  g[3] = tau.x; g[4] = tau.y; g[5] = tau.z;
+  for (int j = 0; j < H.J; ++j) {
+    const int c = H.joint_child[j], p = H.joint_parent[j];
+    M3 Rp, Ro;
+    for (int m = 0; m < 9; ++m) { Rp.m[m] = link[12 * p + m]; Ro.m[m] = H.origin_R[9 * j + m]; }
+    const V3 aw = mul(Rp, mul(Ro, V3{H.axis[3 * j], H.axis[3 * j + 1], H.axis[3 * j + 2]}));
+    const V3 tc{link[12 * c + 9], link[12 * c + 10], link[12 * c + 11]};
+    const V3 Fc{ft[6 * c], ft[6 * c + 1], ft[6 * c + 2]};
+    const V3 Tc{ft[6 * c + 3], ft[6 * c + 4], ft[6 * c + 5]};
+    g[6 + j] = dot(aw, Tc - cross(tc, Fc));
+  }
+}
+
+template <class Sdf>
+__global__ void __launch_bounds__(256) fused_kernel(KHand H, KObj O, Sdf sdf, KSim S, KOpt P, KBuf buf, int mode) {
+  extern __shared__ __align__(16) unsigned char smem[];
+  const SmemLayout lay(H.N, H.L, S.M);
+  double* px = reinterpret_cast<double*>(smem + lay.off_px);
+  double* py = reinterpret_cast<double*>(smem + lay.off_py);
+  double* pz = reinterpret_cast<double*>(smem + lay.off_pz);
+  double* link = reinterpret_cast<double*>(smem + lay.off_link);
+  double* ft_all = reinterpret_cast<double*>(smem + lay.off_ft);
+  unsigned* bitmap_all = reinterpret_cast<unsigned*>(smem + lay.off_bitmap);
+  int* slotpt_all = reinterpret_cast<int*>(smem + lay.off_slotpt);
+  double* stage_all = reinterpret_cast<double*>(smem + lay.off_stage);
+  double* misc = reinterpret_cast<double*>(smem + lay.off_misc);
+  double* sq = misc;               // [40] configuration
+  double* sg = misc + 40;          // [3*32] d_stable, d_qrange, d_qlimit
+  double* sres = misc + 136;       // [8] residuals
+  int* sflag = reinterpret_cast<int*>(misc + 144);  // [16] per-warp status
+
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int M = S.M, N = H.N, L = H.L, J = H.J, D = 6 + J, Qd = 7 + J;
+  const bool record = mode != kModeEval;
+  const int nwords = (N + 31) / 32;
+
+  SimEnv e;
+  e.lane = lane;
+  e.N = N;
+  e.gs = S.gs;
+  e.px = px; e.py = py; e.pz = pz;
+  e.sample_link = H.sample_link;
+  e.bitmap = bitmap_all + warp * nwords;
+  e.slot_point = slotpt_all + warp * kSlotCap;
+  e.stage = stage_all + warp * 160;
+  e.ft = ft_all + warp * 6 * L;
+  const size_t wslot = static_cast<size_t>(blockIdx.x) * M + (warp < M ? warp : 0);
+  e.corr = buf.corr + wslot * buf.cap_corr;
+  e.slots = buf.slots + wslot * kSlotCap;
+  e.fric_order = reinterpret_cast<int*>(buf.slots + static_cast<size_t>(gridDim.x) * M * kSlotCap) + wslot * kSlotCap;
+  e.cap_corr = buf.cap_corr;
+  e.inv_mass = 1.0 / O.mass;
+  e.com = O.com;
+  e.Ibody_inv = O.inertia_body_inv;
+  e.alpha = S.alpha;
+  e.mu = S.mu;
+  e.dt = S.dt;
+  e.point_grads = nullptr;
+
+  const int k0 = mode == kModeOpt ? P.k_begin : 0;
+  const int k1 = mode == kModeOpt ? P.k_end : 1;
+
+  for (int b = blockIdx.x; b < buf.B; b += gridDim.x) {
+    // Adam state in registers of lanes < D of warp 0
+    double am = 0.0, av = 0.0;
+    double b1t = 1.0, b2t = 1.0;
+    if (tid < Qd) sq[tid] = buf.q[static_cast<size_t>(b) * Qd + tid];
+    if (mode == kModeOpt) {
+      if (tid < D) {
+        am = buf.adam_m[static_cast<size_t>(b) * D + tid];
+        av = buf.adam_v[static_cast<size_t>(b) * D + tid];
+      }
+      for (int k = 0; k < P.k_begin; ++k) { b1t = b1t * P.beta1; b2t = b2t * P.beta2; }
+    }
+    int cand_status = kOk;
+    __syncthreads();
+
+    for (int k = k0; k < k1; ++k) {
+      double radius = S.radius;
+      if (mode == kModeOpt)
+        radius = P.iters > 1 ? P.r0 * (1.0 - static_cast<double>(k) / static_cast<double>(P.iters - 1)) : 0.0;
+      // 1. FK
+      if (tid == 0) link_transforms(H, sq, record, link);
+      for (int t = tid; t < 6 * L * M; t += blockDim.x) ft_all[t] = 0.0;
+      if (tid < 16) sflag[tid] = kOk;
+      __syncthreads();
+      for (int i = tid; i < N; i += blockDim.x) {
+        const int li = H.sample_link[i];
+        const double* Rl = link + 12 * li;
+        M3 R;
+        for (int m = 0; m < 9; ++m) R.m[m] = Rl[m];
+        const V3 s{H.samples[3 * i], H.samples[3 * i + 1], H.samples[3 * i + 2]};
+        const V3 p = mul(R, s) + V3{Rl[9], Rl[10], Rl[11]};
+        px[i] = p.x; py[i] = p.y; pz[i] = p.z;
+      }
+      __syncthreads();
+
+      // 2-3. perturbation sims, one per warp
+      if (warp < M) {
+        e.radius = radius;
+        e.point_grads = buf.point_grads ? buf.point_grads + (static_cast<size_t>(b) * M + warp) * N * 3 : nullptr;
+        SimStats st;
+        int status = kOk;
+        FtAcc acc;
+        const V3 vm{S.vel[warp][0], S.vel[warp][1], S.vel[warp][2]};
+        const bool meas = mode == kModeEval && S.measure_residual;
+        const double res = run_sim(sdf, e, vm, record, meas, st, status, acc);
+        acc.flush(e.ft);
+        __syncwarp();
+        if (lane == 0) {
+          sres[warp] = res;
+          sflag[warp] = status;
+          if (buf.sim_res) buf.sim_res[static_cast<size_t>(b) * M + warp] = res;
+          if (buf.stats && mode == kModeEval) {
+            double* so = buf.stats + (static_cast<size_t>(b) * M + warp) * 5;
+            so[0] = st.active; so[1] = st.corrections; so[2] = st.singular; so[3] = st.max_pen; so[4] = st.max_fric;
+          }
+        }
+        if (buf.sim_grads && record) {  // debug: per-perturbation gradient via the FK adjoint
+          __syncwarp();
+          if (lane == 0) {
+            double gtmp[kMaxDim];
+            double* ftw = e.stage;  // reuse the stage buffer (>= 6L doubles for L <= 26)
+            for (int t = 0; t < 6 * L; ++t) ftw[t] = e.ft[t];
+            fk_adjoint(H, sq, link, ftw, gtmp);
+            double* o = buf.sim_grads + (static_cast<size_t>(b) * M + warp) * D;
+            for (int t = 0; t < D; ++t) o[t] = gtmp[t];
+          }
+        }
+      }
+      __syncthreads();
+
+      // 4. losses, gradient, optimizer (warp 0)
+      if (warp == 0) {
+        for (int m = 0; m < M; ++m)
+          if (sflag[m] != kOk) cand_status = sflag[m];
+        // stability loss: losses.cpp:43-45 (record) / losses.hpp:60-67 (eval)
+        double stable = 0.0;
+        for (int m = 0; m < M; ++m) stable = stable + sres[m];
+        if (record) stable = stable * (1.0 / static_cast<double>(M));
+        else stable = stable / static_cast<double>(M);
+        // qrange / qlimit (losses.hpp:70-93)
+        double qr = 0.0, ql = 0.0;
+        for (int j = 0; j < J; ++j) {
+          const double d = sq[7 + j] - 0.5 * (H.lower[j] + H.upper[j]);
+          qr = qr + d * d;
+        }
+        qr = sqrt(qr);
+        for (int j = 0; j < J; ++j) {
+          const double a = sq[7 + j] - H.upper[j];
+          ql = ql + (a >= 0.0 ? a : 0.0);
+          const double c = H.lower[j] - sq[7 + j];
+          ql = ql + (c >= 0.0 ? c : 0.0);
+        }
+        if (record) {
+          if (lane == 0) {
+            for (int t = 0; t < 6 * L; ++t) {
+              double s = 0.0;
+              for (int m = 0; m < M; ++m) s += ft_all[m * 6 * L + t];
+              stage_all[t] = s;
+            }
+            fk_adjoint(H, sq, link, stage_all, sg);
+          }
+          __syncwarp();
+          if (lane < D) {
+            const double inv_m = 1.0 / static_cast<double>(M);
+            double ds = sg[lane] * inv_m;
+            double dr = 0.0, dl = 0.0;
+            if (lane >= 6) {
+              const int j = lane - 6;
+              const double d = sq[7 + j] - 0.5 * (H.lower[j] + H.upper[j]);
+              dr = qr > 0.0 ? 2.0 * ((0.5 / qr) * d) : 0.0;
+              dl = (sq[7 + j] - H.upper[j] >= 0.0 ? 1.0 : 0.0) + (H.lower[j] - sq[7 + j] >= 0.0 ? -1.0 : 0.0);
+            }
+            sg[lane] = ds;
+            sg[32 + lane] = dr;
+            sg[64 + lane] = dl;
+          }
+          __syncwarp();
+        }
+        const bool finite_loss = isfinite(stable) && isfinite(qr) && isfinite(ql);
+        if (!finite_loss && cand_status == kOk) cand_status = kNonFiniteLoss;
+        if (mode == kModeGrad || mode == kModeEval) {
+          if (lane == 0 && buf.losses) {
+            double* lo = buf.losses + static_cast<size_t>(b) * 3;
+            lo[0] = stable; lo[1] = qr; lo[2] = ql;
+          }
+          if (mode == kModeGrad && lane < D && buf.grads) {
+            double* go = buf.grads + static_cast<size_t>(b) * 3 * D;
+            go[lane] = sg[lane];
+            go[D + lane] = sg[32 + lane];
+            go[2 * D + lane] = sg[64 + lane];
+            if (!isfinite(sg[lane]) && cand_status == kOk) cand_status = kNonFiniteGrad;
+          }
+        } else {
+          // App. C: weighted gradient, Adam, apply_gradient_step
+          double gw = 0.0;
+          if (lane < D) gw = S.w_stable * sg[lane] + S.w_qrange * sg[32 + lane] + S.w_qlimit * sg[64 + lane];
+          const bool bad = __any_sync(kFull, lane < D && !isfinite(gw));
+          if (bad && cand_status == kOk) cand_status = kNonFiniteGrad;
+          if (buf.traj) {
+            double* tr = buf.traj + (static_cast<size_t>(b) * (P.k_end - P.k_begin) + (k - P.k_begin)) * (3 + D);
+            if (lane == 0) { tr[0] = stable; tr[1] = qr; tr[2] = ql; }
+            if (lane < D) tr[3 + lane] = gw;
+          }
+          b1t = b1t * P.beta1;
+          b2t = b2t * P.beta2;
+          double dir = 0.0;
+          if (lane < D) {
+            const double c1 = 1.0 - P.beta1, c2 = 1.0 - P.beta2;
+            am = P.beta1 * am + c1 * gw;
+            av = P.beta2 * av + c2 * (gw * gw);
+            const double mhat = am / (1.0 - b1t);
+            const double vhat = av / (1.0 - b2t);
+            dir = mhat / (sqrt(vhat) + P.eps);
+          }
+          __syncwarp();
+          if (lane < D) sg[lane] = dir;  // sg now holds the step direction
+          __syncwarp();
+          if (lane == 0 && cand_status == kOk) {
+            // apply_gradient_step (losses.cpp:92-102)
+            const double lr = P.lr;
+            sq[0] = sq[0] - lr * sg[0];
+            sq[1] = sq[1] - lr * sg[1];
+            sq[2] = sq[2] - lr * sg[2];
+            const V3 tangent{-lr * sg[3], -lr * sg[4], -lr * sg[5]};
+            const Q4 qn = qnormalized(qmul(quat_exp(tangent), Q4{sq[3], sq[4], sq[5], sq[6]}));
+            sq[3] = qn.w; sq[4] = qn.x; sq[5] = qn.y; sq[6] = qn.z;
+            for (int j = 0; j < J; ++j) sq[7 + j] = sq[7 + j] - lr * sg[6 + j];
+          }
+        }
+        if (lane == 0) sflag[15] = cand_status;
+      }
+      __syncthreads();
+      cand_status = sflag[15];
+      if (cand_status != kOk) break;
+    }
+    // write back
+    if (mode == kModeOpt) {
+      if (tid < Qd) buf.q[static_cast<size_t>(b) * Qd + tid] = sq[tid];
+      if (tid < D) {
+        buf.adam_m[static_cast<size_t>(b) * D + tid] = am;
+        buf.adam_v[static_cast<size_t>(b) * D + tid] = av;
+      }
+    }
+    if (tid == 0) buf.status[b] = cand_status;
+    __syncthreads();
+  }
+}
+
+}  // namespace dgx
+
+// ---------------------------------------------------------------------------
+// FK-only and apply_gradient_step kernels (HandModel::forward, hand.hpp:86;
+// apply_gradient_step, losses.cpp:92-102)
+// ---------------------------------------------------------------------------
+namespace dgx {
+
+__global__ void __launch_bounds__(256) forward_kernel(KHand H, const double* q, double* out, int B) {
+  extern __shared__ __align__(16) unsigned char smem[];
+  double* link = reinterpret_cast<double*>(smem);
+  double* sq = link + 12 * H.L;
+  const int Qd = 7 + H.J;
+  for (int b = blockIdx.x; b < B; b += gridDim.x) {
+    if (threadIdx.x < Qd) sq[threadIdx.x] = q[static_cast<size_t>(b) * Qd + threadIdx.x];
+    __syncthreads();
+    if (threadIdx.x == 0) link_transforms(H, sq, false, link);
+    __syncthreads();
+    for (int i = threadIdx.x; i < H.N; i += blockDim.x) {
+      const double* Rl = link + 12 * H.sample_link[i];
+      M3 R;
+      for (int m = 0; m < 9; ++m) R.m[m] = Rl[m];
+      const V3 p = mul(R, V3{H.samples[3 * i], H.samples[3 * i + 1], H.samples[3 * i + 2]}) + V3{Rl[9], Rl[10], Rl[11]};
+      double* o = out + (static_cast<size_t>(b) * H.N + i) * 3;
+      o[0] = p.x; o[1] = p.y; o[2] = p.z;
+    }
+    __syncthreads();
+  }
+}
+
+__global__ void step_kernel(int J, const double* q, const double* g, double lr, double* out, int B) {
+  const int b = blockIdx.x * blockDim.x + threadIdx.x;
+  if (b >= B) return;
+  const int Qd = 7 + J, D = 6 + J;
+  const double* qi = q + static_cast<size_t>(b) * Qd;
+  const double* gi = g + static_cast<size_t>(b) * D;
+  double* o = out + static_cast<size_t>(b) * Qd;
+  o[0] = qi[0] - lr * gi[0];
+  o[1] = qi[1] - lr * gi[1];
+  o[2] = qi[2] - lr * gi[2];
+  const V3 tangent{-lr * gi[3], -lr * gi[4], -lr * gi[5]};
+  const Q4 qn = qnormalized(qmul(quat_exp(tangent), Q4{qi[3], qi[4], qi[5], qi[6]}));
+  o[3] = qn.w; o[4] = qn.x; o[5] = qn.y; o[6] = qn.z;
+  for (int j = 0; j < J; ++j) o[7 + j] = qi[7 + j] - lr * gi[6 + j];
+}
+
+template <class Sdf>
+static cudaError_t launch_fused_t(const KHand& H, const KObj& O, const Sdf& sdf, const KSim& S, const KOpt& P,
+                                  const KBuf& buf, int mode, int grid, int smem, cudaStream_t st) {
+  static bool configured = false;
+  if (!configured) {
+    cudaError_t e = cudaFuncSetAttribute(fused_kernel<Sdf>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+    if (e != cudaSuccess) return e;
+    configured = true;
+  }
+  fused_kernel<Sdf><<<grid, 32 * S.M, smem, st>>>(H, O, sdf, S, P, buf, mode);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_fused(const KHand& H, const KObj& O, int kind, const SphereSdf& sph, const BoxSdf& box,
+                         const GridSdf& grd, const KSim& S, const KOpt& P, const KBuf& buf, int mode, int grid,
+                         int smem, cudaStream_t st) {
+  switch (kind) {
+    case kSdfSphere: return launch_fused_t(H, O, sph, S, P, buf, mode, grid, smem, st);
+    case kSdfBox: return launch_fused_t(H, O, box, S, P, buf, mode, grid, smem, st);
+    case kSdfGrid: return launch_fused_t(H, O, grd, S, P, buf, mode, grid, smem, st);
+    default: return cudaErrorInvalidValue;
+  }
+}
+
+cudaError_t fused_occupancy(int kind, int M, int smem, int* blocks_per_sm) {
+  cudaError_t e;
+  switch (kind) {
+    case kSdfSphere:
+      cudaFuncSetAttribute(fused_kernel<SphereSdf>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+      e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(blocks_per_sm, fused_kernel<SphereSdf>, 32 * M, smem);
+      break;
+    case kSdfBox:
+      cudaFuncSetAttribute(fused_kernel<BoxSdf>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+      e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(blocks_per_sm, fused_kernel<BoxSdf>, 32 * M, smem);
+      break;
+    case kSdfGrid:
+      cudaFuncSetAttribute(fused_kernel<GridSdf>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+      e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(blocks_per_sm, fused_kernel<GridSdf>, 32 * M, smem);
+      break;
+    default:
+      return cudaErrorInvalidValue;
+  }
+  return e;
+}
+
+cudaError_t launch_forward(const KHand& H, const double* q, double* out, int B, int grid, cudaStream_t st) {
+  const int smem = 8 * (12 * H.L + 7 + H.J + 8);
+  forward_kernel<<<grid, 256, smem, st>>>(H, q, out, B);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_step(int J, const double* q, const double* g, double lr, double* out, int B, cudaStream_t st) {
+  step_kernel<<<(B + 127) / 128, 128, 0, st>>>(J, q, g, lr, out, B);
+  return cudaGetLastError();
+}
+
+}  // namespace dgx

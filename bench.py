@@ -1,0 +1,326 @@
+#!/usr/bin/env python
+"""bench.py — batched gradient-based grasp search (Fast-Grasp'D hot path) on B200.
+
+Metric (BASELINE.json): candidate-iterations/s (and grasps/s) at N GPUs.
+Workload (BASELINE config 2, the largest single-GPU config the metric names):
+  Allegro-style 4-finger hand (allegro16: J=16, N=2001 samples from the
+  reference's sampler) grasping a 40 mm box and a cylinder (r 17.5 mm,
+  h 70 mm), each an analytic SDF baked on a 64^3 FP32 grid over bounds +
+  30 mm; 1024 candidates per GPU (512 per object), approach-sampled; the
+  500-iteration optimizer schedule (dilation 0.02 -> 0, Adam lr 1e-3).
+A step = one optimizer iteration of the whole batch: loss_gradient (7
+perturbation sims x 8 Gauss-Seidel sweeps over every hand point, with the
+adjoint) + Adam + apply_gradient_step for every candidate, i.e. 1024
+candidate-iterations per GPU per step, two fused launches (one per object).
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl dgx|reference]
+
+For N>1 run under torchrun: candidates are sharded across ranks (weak
+scaling: 1024 per GPU), no collective in the timed loop; timing is the max
+over ranks of the CUDA-event time. `--impl reference` times the reference's
+own CPU implementation (oracle/_ref/libdgref.so: the unmodified reference
+compiled from /root/reference with the grid SDF behind its contract) on the
+host cores, rank 0 only.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+ITERS = 500
+CAND_PER_GPU = 1024
+RES = 64
+HAND = "allegro16"
+# algorithmic FLOP per point-sweep: 160 backend-independent
+# (50 forward + 110 adjoint) + 2 x F_sdf with F_sdf(grid trilinear + gradient + proxy) = 70
+FLOP_PER_POINT_SWEEP = 160 + 2 * 70
+M_SIMS, GS = 7, 8
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="dgx", choices=["dgx", "reference"])
+    ap.add_argument("--candidates", type=int, default=CAND_PER_GPU)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    return ap.parse_args()
+
+
+def workload(rank: int, cand: int):
+    from paper_2306_08132_b200 import init, model
+    hand = model.HandDesc.asset(HAND)
+    objs = [model.box_grid(res=RES), model.cylinder_grid(res=RES)]
+    per = cand // len(objs)
+    qs = [init.approach_init(o, hand, per, seed=17 + oi, first=rank * per) for oi, o in enumerate(objs)]
+    return hand, objs, qs
+
+
+def config_dict(cand: int, n_gpus: int) -> dict:
+    return {
+        "workload": f"config2: {HAND} (J=16, N=2001) on box 40mm + cylinder r17.5/h70mm SDF grids {RES}^3, "
+                    f"{cand} candidates/GPU ({cand // 2}/object), {ITERS}-iteration schedule; step = 1 iteration",
+        "hand": HAND, "candidates_per_gpu": cand, "objects": ["box40_grid64", "cylinder_grid64"],
+        "sdf": f"fp32 trilinear grid {RES}^3, fp64 arithmetic", "iterations_schedule": ITERS,
+        "perturbations": M_SIMS, "gs_iters": GS, "l2": "flushed between timed steps (256 MiB write)",
+        "parallelism": f"candidates sharded over {n_gpus} GPU(s), no inner-loop collective",
+    }
+
+
+# ---------------------------------------------------------------------------
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+
+    Q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index, self.rows, self.proc = index, [], None
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}",
+                                          "--format=csv,noheader,nounits", "-lms", "200"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except OSError:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.rows.append([c.strip() for c in line.split(",")])
+
+    def __exit__(self, *a):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except subprocess.TimeoutExpired:
+                self.proc.kill()
+
+    def summary(self) -> dict:
+        sm = [float(r[0]) for r in self.rows if len(r) >= 7 and r[0].replace(".", "").isdigit()]
+        mx = [float(r[1]) for r in self.rows if len(r) >= 7 and r[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in self.rows if len(r) >= 7 for i in range(4)
+                          if r[3 + i].lower() == "active"})
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(sm)}
+
+
+def traffic_from_profiles():
+    p = os.path.join(ROOT, "profiles", "roofline_traffic.json")
+    if os.path.exists(p):
+        with open(p) as f:
+            return json.load(f).get("dram_bytes_per_launch")
+    return None
+
+
+# ---------------------------------------------------------------------------
+def cpu_reference_sample(hand_name, objs, qs, k, n_per_obj, threads, variant="glibc"):
+    """Reference CPU path (oracle/_ref) on a bounded sample: n_per_obj candidates
+    per object, one optimizer iteration at schedule index k. Returns
+    (candidate-iterations, seconds)."""
+    from oracle import ref
+    rh = {"allegro16": lambda: ref.RefHand.load_xml(os.path.join(ROOT, "assets", "hands", "allegro16",
+                                                                 "allegro16.xml"), 2000, 12345, variant=variant)}[
+        hand_name]()
+    done, secs = 0, 0.0
+    for o, q in zip(objs, qs):
+        ro = ref.RefObject.from_desc(o, variant=variant)
+        sub = q[:n_per_obj]
+        t0 = time.perf_counter()
+        out = ref.optimize(ro, rh, sub, ref.default_params(), iters=ITERS, k_begin=k, k_end=k + 1, threads=threads)
+        secs += time.perf_counter() - t0
+        done += sub.shape[0]
+        assert not np.any(out["status"]), "reference optimizer failed"
+    return done, secs
+
+
+def run_reference(args, rank):
+    if rank != 0:
+        return
+    threads = os.cpu_count() or 1
+    hand, objs, qs = workload(0, args.candidates)
+    n_per = max(1, min(qs[0].shape[0], 2 * threads))
+    for w in range(args.warmup):
+        cpu_reference_sample(HAND, objs, qs, w, n_per, threads)
+    done = secs = 0
+    for s in range(args.steps):
+        d, t = cpu_reference_sample(HAND, objs, qs, args.warmup + s, n_per, threads)
+        done += d
+        secs += t
+    v = done / secs
+    sample = f"{n_per} candidates x 2 objects x 1 iteration per step, {threads} threads"
+    print(json.dumps({
+        "metric": "candidate-iterations/sec", "value": v, "unit": "candidate-iterations/s", "n_gpus": args.gpus,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * secs / args.steps,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": config_dict(args.candidates, args.gpus), "impl": "reference",
+        "grasps_per_sec": v / ITERS,
+        "cpu_baseline": {"value": v, "unit": "candidate-iterations/s", "cores": threads, "kind": "reference",
+                         "sample": sample},
+        "e2e": {"value": v, "unit": "candidate-iterations/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }), flush=True)
+
+
+# ---------------------------------------------------------------------------
+def run_dgx(args, rank, world, local_rank):
+    import torch
+    import torch.distributed as dist
+    from paper_2306_08132_b200 import api, capi
+
+    torch.cuda.set_device(local_rank)
+    dev = torch.device("cuda", local_rank)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+    hand_d, objs_d, qs = workload(rank, args.candidates)
+    ctx = api.Context(local_rank)
+    stream = torch.cuda.Stream(dev)  # a real stream: the kernels and the timing events share it
+    torch.cuda.set_stream(stream)
+    ctx.set_stream(stream.cuda_stream)
+    hand = api.Hand(ctx, hand_d)
+    objs = [api.GraspObject(ctx, o) for o in objs_d]
+    proto, params, weights = api.StabilityProtocol.standard(), api.SimParams(), api.LossWeights()
+    opt = api.OptConfig(iterations=ITERS)
+    D = 6 + hand_d.num_joints
+    st = [dict(q=torch.tensor(q, device=dev), m=torch.zeros(q.shape[0], D, dtype=torch.float64, device=dev),
+               v=torch.zeros(q.shape[0], D, dtype=torch.float64, device=dev),
+               status=torch.zeros(q.shape[0], dtype=torch.int32, device=dev)) for q in qs]
+    flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)
+    flags = capi.DGX_DEVICE_PTRS | capi.DGX_ASYNC
+
+    def step(k, evs=None):
+        for oi, o in enumerate(objs):
+            s = st[oi]
+            if evs is not None:
+                evs[oi][0].record(stream)
+            out = api.optimize(ctx, o, hand, s["q"], proto, params, weights, opt, k_begin=k, k_end=k + 1,
+                               adam_m=s["m"], adam_v=s["v"], flags=flags, status=s["status"])
+            if evs is not None:
+                evs[oi][1].record(stream)
+
+    for w in range(args.warmup):
+        step(w)
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    launches0 = ctx.launches
+    launch_ms = []
+    with ClockSampler(local_rank) as clk:
+        for s in range(args.steps):
+            flush.zero_()  # L2 flush, outside the timed events
+            evs = [[torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)] for _ in objs]
+            step(args.warmup + s, evs)
+            torch.cuda.synchronize()
+            launch_ms += [e0.elapsed_time(e1) for e0, e1 in evs]
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    launches = ctx.launches - launches0
+    total_ms = sum(launch_ms)
+    status_bad = int(sum(int(torch.count_nonzero(s["status"])) for s in st))
+    t = torch.tensor([total_ms], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    max_ms = float(t.item())
+    cand_total = args.candidates * world
+    value = cand_total * args.steps / (max_ms * 1e-3)
+
+    # ---- end to end through the public host API (pinned-free numpy path) ----
+    host = [dict(q=st[i]["q"].cpu().numpy(), m=st[i]["m"].cpu().numpy(), v=st[i]["v"].cpu().numpy())
+            for i in range(len(objs))]
+    ctx.set_stream(None)
+    k0 = args.warmup + args.steps
+    h2d = d2h = 0
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    t0 = time.perf_counter()
+    for s in range(args.steps):
+        for oi, o in enumerate(objs):
+            h = host[oi]
+            out = api.optimize(ctx, o, hand, h["q"], proto, params, weights, opt, k_begin=k0 + s, k_end=k0 + s + 1,
+                               adam_m=h["m"], adam_v=h["v"], record=True)
+            h.update(q=out["q"], m=out["m"], v=out["v"])
+            nb = h["q"].nbytes + h["m"].nbytes + h["v"].nbytes
+            h2d += nb
+            d2h += nb + out["traj"].nbytes + out["status"].nbytes
+    e2e_s = time.perf_counter() - t0
+    t = torch.tensor([e2e_s], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    e2e_value = cand_total * args.steps / float(t.item())
+
+    if rank == 0:
+        L = capi.load()
+        import ctypes as C
+        pk, pms = C.c_double(), C.c_double()
+        capi.check(L.dgx_fp64_peak(local_rank, C.byref(pk), C.byref(pms)))
+        n_pts = hand_d.num_samples
+        flop_cand_iter = M_SIMS * GS * n_pts * FLOP_PER_POINT_SWEEP
+        per_launch_cand = args.candidates // len(objs)
+        avg_launch_s = statistics.mean(launch_ms) * 1e-3
+        achieved = flop_cand_iter * per_launch_cand / avg_launch_s / 1e12
+        traffic = traffic_from_profiles()
+        result = {
+            "metric": "candidate-iterations/sec", "value": value, "unit": "candidate-iterations/s",
+            "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": max_ms / args.steps,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic (approach-sampled configurations, analytic SDFs baked to grids)",
+            "config": config_dict(args.candidates, world),
+            "grasps_per_sec": value / ITERS,
+            "e2e": {"value": e2e_value, "unit": "candidate-iterations/s",
+                    "h2d_bytes_per_step": h2d // args.steps, "d2h_bytes_per_step": d2h // args.steps},
+            "gpu_launches": launches,
+            "roofline": {"bound": "fp64", "achieved": achieved, "peak": pk.value, "unit": "TFLOP/s",
+                         "frac": achieved / pk.value, "traffic": traffic,
+                         "peak_source": "measured DFMA microbenchmark (dgx_fp64_peak, csrc/dgx_peak.cu)",
+                         "flop_per_candidate_iteration": flop_cand_iter,
+                         "avg_launch_ms": statistics.mean(launch_ms)},
+            "clocks": clk.summary(),
+            "failed_candidates": status_bad,
+        }
+        if world == 1 and not args.no_cpu_baseline:
+            threads = os.cpu_count() or 1
+            hand_r, objs_r, qs_r = workload(0, args.candidates)
+            n_per = max(1, min(qs_r[0].shape[0], 2 * threads))
+            d, secs = cpu_reference_sample(HAND, objs_r, qs_r, 0, n_per, threads)
+            result["cpu_baseline"] = {"value": d / secs, "unit": "candidate-iterations/s", "cores": threads,
+                                      "kind": "reference",
+                                      "sample": f"{n_per} candidates x 2 objects x 1 iteration (k=0), "
+                                                f"{threads} std::threads, oracle/_ref/libdgref.so"}
+        print(json.dumps(result), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+def main():
+    args = parse()
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    if args.impl == "reference":
+        run_reference(args, rank)
+    else:
+        run_dgx(args, rank, world, local_rank)
+
+
+if __name__ == "__main__":
+    main()

@@ -167,6 +167,10 @@ int dgx_debug_sims(dgx_ctx* ctx, const dgx_hand* hand, const dgx_object* obj, in
                    const dgx_params* params, double* sim_res, double* sim_grads, double* point_grads,
                    int32_t* status, uint32_t flags);
 
+/* Utility: measured FP64 FMA throughput of the device (TFLOP/s), the
+   roofline denominator for the fused kernel. */
+int dgx_fp64_peak(int device, double* tflops, double* ms);
+
 #ifdef __cplusplus
 }
 #endif

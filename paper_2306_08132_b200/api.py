@@ -100,7 +100,9 @@ class Context:
             capi.check(self.L.dgx_ctx_set_correction_capacity(self.h, correction_capacity))
 
     def set_stream(self, stream_ptr: int | None) -> None:
-        capi.check(self.L.dgx_ctx_set_stream(self.h, stream_ptr))
+        """Launch on an external cudaStream_t; None/0 selects the context's own
+        stream (the legacy default stream cannot be selected)."""
+        capi.check(self.L.dgx_ctx_set_stream(self.h, stream_ptr or None))
 
     @property
     def launches(self) -> int:
@@ -238,7 +240,7 @@ def debug_sims(ctx: Context, obj: GraspObject, hand: Hand, q, protocol: Stabilit
 
 def optimize(ctx: Context, obj: GraspObject, hand: Hand, q, protocol: StabilityProtocol, params: SimParams,
              weights: LossWeights, opt: OptConfig, k_begin: int = 0, k_end: int | None = None, adam_m=None,
-             adam_v=None, record: bool = False, flags: int | None = None):
+             adam_v=None, record: bool = False, flags: int | None = None, status=None):
     """Fused synthesis loop (dgx_optimize_batch). numpy arrays: copied in/out
     (host path, synchronous); torch CUDA tensors: updated in place on device."""
     k_end = opt.iterations if k_end is None else k_end
@@ -257,7 +259,7 @@ def optimize(ctx: Context, obj: GraspObject, hand: Hand, q, protocol: StabilityP
         dev = q.device
         adam_m = torch.zeros((B, D), dtype=torch.float64, device=dev) if adam_m is None else adam_m
         adam_v = torch.zeros((B, D), dtype=torch.float64, device=dev) if adam_v is None else adam_v
-        status = torch.zeros(B, dtype=torch.int32, device=dev)
+        status = torch.zeros(B, dtype=torch.int32, device=dev) if status is None else status
         traj = torch.zeros((B, k_end - k_begin, 3 + D), dtype=torch.float64, device=dev) if record else None
     p = params_c(params, protocol, weights)
     o = capi.OptC(opt.iterations, k_begin, k_end, int(record), opt.dilation_start_radius, opt.learning_rate,

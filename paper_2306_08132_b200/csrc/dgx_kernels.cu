@@ -630,11 +630,22 @@ __device__ void fk_adjoint(const KHand& H, const double* qv, const double* link,
   const V3 F{ft[6 * base], ft[6 * base + 1], ft[6 * base + 2]};
   const V3 T{ft[6 * base + 3], ft[6 * base + 4], ft[6 * base + 5]};
   const V3 pos{qv[0], qv[1], qv[2]};
-  const V3 tau = T - cross(pos, F);
+  // the tape never propagates a zero adjoint (tape.cpp:33): a subtree without
+  // adjoint contributes exactly 0 even where pose values are non-finite
+  auto zero6 = [&](int l) {
+    for (int c = 0; c < 6; ++c)
+      if (ft[6 * l + c] != 0.0) return false;
+    return true;
+  };
+  const V3 tau = (F.x == 0.0 && F.y == 0.0 && F.z == 0.0) ? T : T - cross(pos, F);
   g[0] = F.x; g[1] = F.y; g[2] = F.z;
   g[3] = tau.x; g[4] = tau.y; g[5] = tau.z;
   for (int j = 0; j < H.J; ++j) {
     const int c = H.joint_child[j], p = H.joint_parent[j];
+    if (zero6(c)) {
+      g[6 + j] = 0.0;
+      continue;
+    }
     M3 Rp, Ro;
     for (int m = 0; m < 9; ++m) { Rp.m[m] = link[12 * p + m]; Ro.m[m] = H.origin_R[9 * j + m]; }
     const V3 aw = mul(Rp, mul(Ro, V3{H.axis[3 * j], H.axis[3 * j + 1], H.axis[3 * j + 2]}));

@@ -1,0 +1,103 @@
+"""Approach-sampling initialization (defaults) —
+specified by the reference but not implemented there.
+
+Per candidate (deterministic per (seed, index), counter-based Philox):
+  * a random direction d from the object's centre of mass; the surface point
+    p_s is where the ray leaves the zero level set (analytic for primitives,
+    bisection on the trilinear grid for grids) and n is the outward normal;
+  * palm position p_s + standoff * n, standoff = 1.2 x bounding radius;
+  * palm approach axis (+z, assets.cpp:211) anti-parallel to n, roll about it
+    uniform in [0, 2 pi);
+  * joints at mid-range (hand.cpp:212-216).
+
+This is host-side setup producing the optimizer's INPUT q; the same array is
+fed to the GPU and to the oracle.
+"""
+from __future__ import annotations
+
+import numpy as np
+
+from .model import HandDesc, ObjectDesc
+
+
+def _grid_phi(o: ObjectDesc, p: np.ndarray) -> np.ndarray:
+    """Trilinear value (same node layout as csrc/dgx_geom.h GridSdf), inside the box."""
+    u = (p - o.origin) * o.inv_spacing
+    n = np.array(o.dims)
+    u = np.clip(u, 0.0, n - 1.0)
+    i = np.minimum(u.astype(np.int64), n - 2)
+    t = u - i
+    v = o.values
+    def at(di, dj, dk):
+        return v[i[..., 2] + dk, i[..., 1] + dj, i[..., 0] + di].astype(np.float64)
+    tx, ty, tz = t[..., 0], t[..., 1], t[..., 2]
+    c00 = at(0, 0, 0) + (at(1, 0, 0) - at(0, 0, 0)) * tx
+    c10 = at(0, 1, 0) + (at(1, 1, 0) - at(0, 1, 0)) * tx
+    c01 = at(0, 0, 1) + (at(1, 0, 1) - at(0, 0, 1)) * tx
+    c11 = at(0, 1, 1) + (at(1, 1, 1) - at(0, 1, 1)) * tx
+    c0 = c00 + (c10 - c00) * ty
+    c1 = c01 + (c11 - c01) * ty
+    return c0 + (c1 - c0) * tz
+
+
+def surface_point(o: ObjectDesc, d: np.ndarray) -> tuple[np.ndarray, np.ndarray]:
+    """(p_s, outward unit normal) along the ray com + t d."""
+    if o.kind == "sphere":
+        return o.center + o.radius * d, d.copy()
+    if o.kind == "box":
+        with np.errstate(divide="ignore"):
+            ts = np.where(np.abs(d) > 0, o.half_extents / np.abs(d), np.inf)
+        k = int(np.argmin(ts))
+        n = np.zeros(3)
+        n[k] = np.sign(d[k])
+        return o.center + ts[k] * d, n
+    lo, hi = 0.0, float(np.max(o.spacing * (np.array(o.dims) - 1)))
+    for _ in range(60):  # bisection on phi(com + t d) = 0
+        mid = 0.5 * (lo + hi)
+        if _grid_phi(o, o.com + mid * d) < 0.0:
+            lo = mid
+        else:
+            hi = mid
+    p = o.com + 0.5 * (lo + hi) * d
+    h = 0.5 * o.spacing
+    g = np.array([(_grid_phi(o, p + h * e) - _grid_phi(o, p - h * e)) for e in np.eye(3)])
+    n = g / np.linalg.norm(g) if np.linalg.norm(g) > 0 else d.copy()
+    return p, n
+
+
+def _quat_from_matrix(R: np.ndarray) -> np.ndarray:
+    w = np.sqrt(max(0.0, 1.0 + R[0, 0] + R[1, 1] + R[2, 2])) / 2.0
+    x = np.sqrt(max(0.0, 1.0 + R[0, 0] - R[1, 1] - R[2, 2])) / 2.0
+    y = np.sqrt(max(0.0, 1.0 - R[0, 0] + R[1, 1] - R[2, 2])) / 2.0
+    z = np.sqrt(max(0.0, 1.0 - R[0, 0] - R[1, 1] + R[2, 2])) / 2.0
+    x = np.copysign(x, R[2, 1] - R[1, 2])
+    y = np.copysign(y, R[0, 2] - R[2, 0])
+    z = np.copysign(z, R[1, 0] - R[0, 1])
+    q = np.array([w, x, y, z])
+    return q / np.linalg.norm(q)
+
+
+def approach_init(obj: ObjectDesc, hand: HandDesc, B: int, seed: int = 0, standoff_scale: float = 1.2,
+                  first: int = 0) -> np.ndarray:
+    """[B, 7+J] initial configurations for candidates first..first+B-1."""
+    out = np.zeros((B, 7 + hand.num_joints))
+    standoff = standoff_scale * obj.bounding_radius()
+    mid = hand.mid_range()
+    for b in range(B):
+        rng = np.random.Generator(np.random.Philox(key=seed, counter=first + b))
+        d = rng.normal(size=3)
+        d /= np.linalg.norm(d)
+        roll = rng.uniform(0.0, 2.0 * np.pi)
+        p_s, n = surface_point(obj, d)
+        z = -n
+        a = np.array([1.0, 0.0, 0.0]) if abs(z[0]) < 0.9 else np.array([0.0, 1.0, 0.0])
+        x = a - np.dot(a, z) * z
+        x /= np.linalg.norm(x)
+        y = np.cross(z, x)
+        c, s = np.cos(roll), np.sin(roll)
+        xr, yr = c * x + s * y, -s * x + c * y
+        R = np.stack([xr, yr, z], axis=1)  # columns: palm x, y, z in world
+        out[b, :3] = p_s + standoff * n
+        out[b, 3:7] = _quat_from_matrix(R)
+        out[b, 7:] = mid
+    return out

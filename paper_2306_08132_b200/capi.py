@@ -11,7 +11,7 @@ import os
 import numpy as np
 
 PKG_DIR = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(PKG_DIR, "libdgx_cuda.so")
+LIB_PATH = os.environ.get("DGX_LIBRARY") or os.path.join(PKG_DIR, "libdgx_cuda.so")
 
 _dp = C.POINTER(C.c_double)
 _ip = C.POINTER(C.c_int32)

@@ -9,6 +9,7 @@ namespace dgx {
 constexpr int kMaxSims = 8;        // protocol velocities per candidate (standard: 7)
 constexpr int kMaxDim = 32;        // 6 + J gradient coordinates (J <= 26)
 constexpr int kSlotCap = 256;      // distinct active contacts per perturbation sim
+constexpr int kStageDoubles = 640; // per-warp staging (adjoint segment: 4 slots x 5 x 32 lanes)
 
 enum Mode : int { kModeGrad = 0, kModeEval = 1, kModeOpt = 2 };
 
@@ -110,7 +111,7 @@ struct SmemLayout {
     off_ft = o; o = align(o + 8 * 6 * L * M);
     off_bitmap = o; o = align(o + 4 * ((N + 31) / 32) * M);
     off_slotpt = o; o = align(o + 4 * kSlotCap * M);
-    off_stage = o; o = align(o + 8 * 5 * 32 * M);
+    off_stage = o; o = align(o + 8 * kStageDoubles * M);
     off_misc = o; o = align(o + 8 * (64 + 4 * kMaxDim + 2 * kMaxSims));
     total = o;
   }

@@ -33,6 +33,7 @@
 
 #include "dgx_adjoint.cuh"
 #include "dgx_kernel.cuh"
+#include "dgx_sdf_fast.cuh"
 
 namespace dgx {
 
@@ -97,29 +98,57 @@ __device__ __forceinline__ void eval_point(const Sdf& sdf, const SimEnv& e, int 
   }
 }
 
-// per-lane link accumulator for d/dp, flushed to the warp's shared array
+// Per-lane accumulator of d/dp folded into per-link force / torque sums
+// (F_l = sum adj_p, T_l = sum p x adj_p). A lane crossing a link boundary
+// mid-walk spills its partial with a (rare) shared atomic; the common path is
+// the warp-cooperative flush below (no atomics).
 struct FtAcc {
   int link = -1;
   V3 F{0.0, 0.0, 0.0}, T{0.0, 0.0, 0.0};
-  __device__ __forceinline__ void flush(double* ft) {
-    if (link >= 0) {
-      double* d = ft + 6 * link;
-      atomicAdd(d + 0, F.x); atomicAdd(d + 1, F.y); atomicAdd(d + 2, F.z);
-      atomicAdd(d + 3, T.x); atomicAdd(d + 4, T.y); atomicAdd(d + 5, T.z);
-    }
+  __device__ __forceinline__ void reset() {
     link = -1;
     F = V3{0.0, 0.0, 0.0};
     T = V3{0.0, 0.0, 0.0};
   }
+  __device__ __forceinline__ void spill(double* ft) {
+    double* d = ft + 6 * link;
+    atomicAdd(d + 0, F.x); atomicAdd(d + 1, F.y); atomicAdd(d + 2, F.z);
+    atomicAdd(d + 3, T.x); atomicAdd(d + 4, T.y); atomicAdd(d + 5, T.z);
+    reset();
+  }
   __device__ __forceinline__ void add(double* ft, int l, V3 ap, V3 p) {
     if (l != link) {
-      flush(ft);
+      if (link >= 0) spill(ft);
       link = l;
     }
     F = F + ap;
     T = T + cross(p, ap);
   }
 };
+
+// Warp-cooperative flush: lanes holding the same link are summed with a
+// butterfly and written by one leader lane; every lane's accumulator resets.
+__device__ __forceinline__ void ft_flush_warp(FtAcc& acc, double* ft, int lane) {
+  unsigned pending = __ballot_sync(0xffffffffu, acc.link >= 0);
+  while (pending) {
+    const int leader = __ffs(pending) - 1;
+    const int key = __shfl_sync(0xffffffffu, acc.link, leader);
+    const bool mine = acc.link == key;
+    pending &= ~__ballot_sync(0xffffffffu, mine);
+    double v[6] = {mine ? acc.F.x : 0.0, mine ? acc.F.y : 0.0, mine ? acc.F.z : 0.0,
+                   mine ? acc.T.x : 0.0, mine ? acc.T.y : 0.0, mine ? acc.T.z : 0.0};
+#pragma unroll
+    for (int k = 0; k < 6; ++k)
+      for (int o = 16; o > 0; o >>= 1) v[k] += __shfl_xor_sync(0xffffffffu, v[k], o);
+    if (lane == leader) {
+      double* d = ft + 6 * key;
+#pragma unroll
+      for (int k = 0; k < 6; ++k) d[k] += v[k];
+    }
+  }
+  __syncwarp();
+  acc.reset();
+}
 
 __device__ __forceinline__ void add_point_grad(const SimEnv& e, int i, V3 ap) {
   if (e.point_grads) {
@@ -239,6 +268,174 @@ __device__ __forceinline__ M3 warp_sum(const M3& A) {
   return r;
 }
 
+// 1/w to full double accuracy: MUFU reciprocal seed + two Newton steps
+// (adjoint-only; the forward keeps IEEE division)
+__device__ __forceinline__ double rcp_fast(double w) {
+  double r;
+  asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(w));
+  double e = fma(-w, r, 1.0);
+  r = fma(r, e, r);
+  e = fma(-w, r, 1.0);
+  return fma(r, e, r);
+}
+
+// Geometry of one inactive point-sweep for the leak adjoint (sim.hpp:105-125
+// recorded with C = gate(rho_d) = 0): unit SDF gradient g (local frame),
+// n = R g (world), the arm rel = p - x. contrib == false for points that were
+// active in the forward (a singular-skipped correction: no axpy recorded).
+struct LeakGeo {
+  V3 p, rel, g, n;
+  double sg;     // sign factor of the interpolated-normal fallback (sdf.cpp:150-155)
+  bool contrib;
+};
+
+template <class Sdf>
+__device__ __forceinline__ void leak_geo(const Sdf& sdf, const SimEnv& e, int i, V3 xk, const M3& Rk, LeakGeo& L) {
+  L.p = V3{e.px[i], e.py[i], e.pz[i]};
+  L.rel = L.p - xk;
+  const V3 rl = ftmul(Rk, L.rel) + e.com;
+  FastEval fe = classify(sdf, rl, e.radius);
+  L.sg = 1.0;
+  L.contrib = false;
+  if (fe.cls == 0) {  // near the decision boundary: the exact (bit-exact) query decides
+    PointEval pe;
+    eval_point(sdf, e, i, xk, Rk, true, pe);
+    if (pe.rho_d < 0.0) return;
+    fe.g = pe.q.grad;
+    L.sg = pe.fb ? static_cast<double>(pe.q.sign) : 1.0;
+  } else if (fe.cls < 0) {
+    return;
+  }
+  L.g = fe.g;
+  L.n = fmul(Rk, fe.g);
+  L.contrib = true;
+}
+
+// Leak recurrence coefficients: adj_x_before = adj_x_after - s n with
+// s = c1 (n . adj_x_after) + c0 (kx = -(m^-1/w) n, g_q = 1/2 [0,k_w] (x) q,
+// gate backward -alpha; sim.hpp:107-124, tape.cpp:103-107).
+__device__ __forceinline__ bool leak_coef(const SimEnv& e, const LeakGeo& L, V3 G, double& c1, double& c0) {
+  const V3 a = cross(L.rel, L.n);
+  const V3 Ia = fmul(e.Iw, a);
+  const double w = e.inv_mass + fdot(a, Ia);
+  if (w < 1e-12) return false;
+  const double lpc = rcp_fast(w);
+  c1 = e.alpha * e.inv_mass * lpc * L.sg;
+  c0 = 0.5 * e.alpha * lpc * fdot(a, G) * L.sg;
+  return true;
+}
+
+constexpr int kSeg = 4;  // points per lane segment in the adjoint (block = 128 point-sweeps)
+// per (segment slot, lane): c1, c0, g.x, g.y, g.z staged in shared memory by pass 1
+__device__ __forceinline__ int stg_idx(int k, int c, int lane) { return (k * 5 + c) * 32 + lane; }
+
+// Adjoint of one inactive run [lo, hi) of flattened (sweep*N + point)
+// positions with frozen state (xk, qk): lane l walks positions
+// [top-(l+1)S, top-lS) downward. Pass 1 composes each lane's affine map on
+// adj_x, a 5-level Kogge-Stone scan hands every lane its incoming adj_x,
+// pass 3 re-walks with it and emits the point / R adjoints.
+template <class Sdf>
+__device__ void process_run(const Sdf& sdf, SimEnv& e, int lo, int hi, V3 xk, Q4 qk, const M3& Rk, Q4 aQ, V3& aX,
+                            M3& aR, FtAcc& acc) {
+  const int lane = e.lane, N = e.N;
+  double* stg = e.stage;
+  // H . k == ([0,k] (x) q_k) . aQ ; G = Iw^T H  (theta-axpy coefficient)
+  const V3 H{-qk.x * aQ.w + qk.w * aQ.x - qk.z * aQ.y + qk.y * aQ.z,
+             -qk.y * aQ.w + qk.z * aQ.x + qk.w * aQ.y - qk.x * aQ.z,
+             -qk.z * aQ.w - qk.y * aQ.x + qk.x * aQ.y + qk.w * aQ.z};
+  const V3 G = ftmul(e.Iw, H);
+  V3 X = aX;
+  for (int top = hi; top > lo; top -= 32 * kSeg) {
+    const int shi = top - lane * kSeg;
+    const int slo = max(top - (lane + 1) * kSeg, lo);
+    const int cnt = shi - slo;
+    // ---- pass 1: coefficients and this lane's composed map a -> M a + b
+    M3 Mm;
+    Mm.m[0] = 1.0; Mm.m[1] = 0.0; Mm.m[2] = 0.0;
+    Mm.m[3] = 0.0; Mm.m[4] = 1.0; Mm.m[5] = 0.0;
+    Mm.m[6] = 0.0; Mm.m[7] = 0.0; Mm.m[8] = 1.0;
+    V3 bm{0.0, 0.0, 0.0};
+    int i = cnt > 0 ? (shi - 1) % N : 0;
+    for (int k = 0; k < cnt; ++k) {
+      LeakGeo L;
+      leak_geo(sdf, e, i, xk, Rk, L);
+      double c1 = 0.0, c0 = 0.0;
+      if (L.contrib && leak_coef(e, L, G, c1, c0)) {
+        const V3 n = L.n;
+        const V3 v{fma(n.z, Mm.m[6], fma(n.y, Mm.m[3], n.x * Mm.m[0])),
+                   fma(n.z, Mm.m[7], fma(n.y, Mm.m[4], n.x * Mm.m[1])),
+                   fma(n.z, Mm.m[8], fma(n.y, Mm.m[5], n.x * Mm.m[2]))};
+        const V3 cn = n * (-c1);
+        outer_acc(Mm, cn, v);
+        const double t = fdot(n, bm);
+        bm = fma3(-fma(c1, t, c0), n, bm);
+      } else {
+        c1 = 0.0;
+        c0 = 0.0;
+      }
+      stg[stg_idx(k, 0, lane)] = c1;
+      stg[stg_idx(k, 1, lane)] = c0;
+      stg[stg_idx(k, 2, lane)] = L.g.x;
+      stg[stg_idx(k, 3, lane)] = L.g.y;
+      stg[stg_idx(k, 4, lane)] = L.g.z;
+      if (--i < 0) i = N - 1;
+    }
+    // ---- pass 2: inclusive scan of maps across lanes (lane 0 applies first)
+    M3 Mi = Mm;
+    V3 bi = bm;
+#pragma unroll
+    for (int d = 1; d < 32; d <<= 1) {
+      M3 Mu;
+#pragma unroll
+      for (int t = 0; t < 9; ++t) Mu.m[t] = __shfl_up_sync(kFull, Mi.m[t], d);
+      const V3 bu{__shfl_up_sync(kFull, bi.x, d), __shfl_up_sync(kFull, bi.y, d), __shfl_up_sync(kFull, bi.z, d)};
+      if (lane >= d) {
+        bi = fmul(Mi, bu) + bi;
+        M3 P;
+#pragma unroll
+        for (int r = 0; r < 3; ++r)
+#pragma unroll
+          for (int c = 0; c < 3; ++c)
+            P.m[3 * r + c] = fma(Mi.m[3 * r + 2], Mu.m[6 + c], fma(Mi.m[3 * r + 1], Mu.m[3 + c], Mi.m[3 * r] * Mu.m[c]));
+        Mi = P;
+      }
+    }
+    M3 Mp;
+#pragma unroll
+    for (int t = 0; t < 9; ++t) Mp.m[t] = __shfl_up_sync(kFull, Mi.m[t], 1);
+    const V3 bp{__shfl_up_sync(kFull, bi.x, 1), __shfl_up_sync(kFull, bi.y, 1), __shfl_up_sync(kFull, bi.z, 1)};
+    V3 a = lane == 0 ? X : fmul(Mp, X) + bp;
+    M3 Ml;
+#pragma unroll
+    for (int t = 0; t < 9; ++t) Ml.m[t] = __shfl_sync(kFull, Mi.m[t], 31);
+    const V3 bl{__shfl_sync(kFull, bi.x, 31), __shfl_sync(kFull, bi.y, 31), __shfl_sync(kFull, bi.z, 31)};
+    const V3 Xnext = fmul(Ml, X) + bl;
+    __syncwarp();
+    // ---- pass 3: re-walk with the incoming adjoint, emit contributions
+    i = cnt > 0 ? (shi - 1) % N : 0;
+    for (int k = 0; k < cnt; ++k) {
+      const double c1 = stg[stg_idx(k, 0, lane)], c0 = stg[stg_idx(k, 1, lane)];
+      if (c1 != 0.0 || c0 != 0.0) {
+        const V3 g{stg[stg_idx(k, 2, lane)], stg[stg_idx(k, 3, lane)], stg[stg_idx(k, 4, lane)]};
+        const V3 p{e.px[i], e.py[i], e.pz[i]};
+        const V3 rel = p - xk;
+        const V3 n = fmul(Rk, g);
+        const double s = fma(c1, fdot(n, a), c0);
+        a = fma3(-s, n, a);
+        const V3 a_rel = n * s;
+        outer_acc(aR, rel, g * s);
+        acc.add(e.ft, e.sample_link[i], a_rel, p);
+        add_point_grad(e, i, a_rel);
+      }
+      if (--i < 0) i = N - 1;
+    }
+    X = Xnext;
+    __syncwarp();
+    ft_flush_warp(acc, e.ft, lane);
+  }
+  aX = X;
+}
+
 // One perturbation simulation (losses.hpp:47-57 with T = 1), forward and,
 // when `record`, its adjoint. Returns the residual; status via `status`.
 template <class Sdf>
@@ -265,13 +462,28 @@ __device__ double run_sim(const Sdf& sdf, SimEnv& e, V3 v_m, bool record, bool m
   __syncwarp();
 
   // ---- Gauss-Seidel sweeps (sim.hpp:157-186) -------------------------------
+  // 32 consecutive points are classified against the current state; only
+  // candidates near / inside the dilated surface run the exact query; the
+  // first exact-active lane is applied and evaluation restarts after it.
   int ncorr = 0, nslot = 0;
   int pos = 0, sweep = 0;
   while (sweep < e.gs) {
     const int i = pos + lane;
+    int cls = 1;
+    if (i < N) {
+      const V3 p{e.px[i], e.py[i], e.pz[i]};
+      const V3 rl = ftmul(R, p - x) + e.com;
+      cls = classify(sdf, rl, e.radius).cls;
+    }
+    const unsigned cand = __ballot_sync(kFull, i < N && cls <= 0);
+    if (cand == 0u) {
+      pos += 32;
+      if (pos >= N) { pos = 0; ++sweep; }
+      continue;
+    }
     PointEval pe;
     bool act = false;
-    if (i < N) {
+    if (i < N && cls <= 0) {
       eval_point(sdf, e, i, x, R, record, pe);
       act = record ? (pe.rho_d < 0.0) : !(pe.rho_d >= 0.0);
     }
@@ -435,7 +647,6 @@ __device__ double run_sim(const Sdf& sdf, SimEnv& e, V3 v_m, bool record, bool m
   M3 aR;  // per-lane partial adjoint of the current R node
   for (int k = 0; k < 9; ++k) aR.m[k] = 0.0;
   int hi = e.gs * N;
-  double* stg = e.stage;
   for (int k = ncorr - 1;; --k) {
     // state of the run after correction k (predicted state for k < 0)
     V3 xk = pred_x;
@@ -447,68 +658,7 @@ __device__ double run_sim(const Sdf& sdf, SimEnv& e, V3 v_m, bool record, bool m
     }
     const M3 Rk = rotation_matrix(qk);
     const int lo = k >= 0 ? e.corr[k].f + 1 : 0;
-    {
-      // H . k == ([0,k] (x) q_k) . aQ (the leak's theta axpy coefficient, sim.hpp:118-124)
-      const V3 H{-qk.x * aQ.w + qk.w * aQ.x - qk.z * aQ.y + qk.y * aQ.z,
-                 -qk.y * aQ.w + qk.z * aQ.x + qk.w * aQ.y - qk.x * aQ.z,
-                 -qk.z * aQ.w - qk.y * aQ.x + qk.x * aQ.y + qk.w * aQ.z};
-      const V3 G = ftmul(e.Iw, H);
-      for (int top = hi; top > lo; top -= 32) {
-        const int f = top - 1 - lane;
-        PointEval pe;
-        V3 nw{0.0, 0.0, 0.0};
-        double c1 = 0.0, c0 = 0.0;
-        int i = 0;
-        bool contrib = false;
-        if (f >= lo) {
-          i = f % N;
-          eval_point(sdf, e, i, xk, Rk, true, pe);
-          if (pe.rho_d >= 0.0) {
-            nw = mul(Rk, pe.q.grad);
-            const V3 a = cross(pe.rel, nw);
-            const V3 Ia = mul(e.Iw, a);
-            const double w = e.inv_mass + dot(a, Ia);
-            if (w >= 1e-12) {
-              const double lpc = 1.0 / w;
-              const double kxs = e.inv_mass * lpc;
-              const double ee = -0.5 * lpc * fdot(a, G);
-              const double sg = pe.fb ? static_cast<double>(pe.q.sign) : 1.0;
-              c1 = e.alpha * kxs * sg;
-              c0 = -e.alpha * ee * sg;
-              contrib = true;
-            }
-          }
-        }
-        const unsigned cm = __ballot_sync(kFull, contrib);
-        if (cm == 0u) continue;
-        stg[lane] = nw.x;
-        stg[32 + lane] = nw.y;
-        stg[64 + lane] = nw.z;
-        stg[96 + lane] = c1;
-        stg[128 + lane] = c0;
-        __syncwarp();
-        double my_s = 0.0;
-        unsigned bits = cm;
-        while (bits) {
-          const int l = __ffs(bits) - 1;
-          bits &= bits - 1u;
-          const double nx = stg[l], ny = stg[32 + l], nz = stg[64 + l];
-          const double s = fma(stg[96 + l], fma(nz, aX.z, fma(ny, aX.y, nx * aX.x)), stg[128 + l]);
-          if (lane == l) my_s = s;
-          aX.x = fma(-s, nx, aX.x);
-          aX.y = fma(-s, ny, aX.y);
-          aX.z = fma(-s, nz, aX.z);
-        }
-        __syncwarp();
-        if (contrib) {
-          const V3 a_rl = pe.q.grad * my_s;
-          const V3 a_rel = nw * my_s;
-          outer_acc(aR, pe.rel, a_rl);
-          acc.add(e.ft, e.sample_link[i], a_rel, pe.p);
-          add_point_grad(e, i, a_rel);
-        }
-      }
-    }
+    process_run(sdf, e, lo, hi, xk, qk, Rk, aQ, aX, aR, acc);
     if (k < 0) break;
 
     // ---- active correction k (sim.hpp:215-245), reverse ----
@@ -573,9 +723,13 @@ __device__ double run_sim(const Sdf& sdf, SimEnv& e, V3 v_m, bool record, bool m
     a_rel = a_rel + fmul(Rb, a_rl);
     if (lane == 0) {
       outer_acc(aR, pe.rel, a_rl);
-      acc.add(e.ft, e.sample_link[i], a_rel, pe.p);
+      double* d = e.ft + 6 * e.sample_link[i];
+      const V3 tq = cross(pe.p, a_rel);
+      d[0] += a_rel.x; d[1] += a_rel.y; d[2] += a_rel.z;
+      d[3] += tq.x; d[4] += tq.y; d[5] += tq.z;
       add_point_grad(e, i, a_rel);
     }
+    __syncwarp();
     aX = aX - a_rel;
     aQ = aQb;
     hi = c.f;
@@ -657,7 +811,7 @@ __device__ void fk_adjoint(const KHand& H, const double* qv, const double* link,
 }
 
 template <class Sdf>
-__global__ void __launch_bounds__(256) fused_kernel(KHand H, KObj O, Sdf sdf, KSim S, KOpt P, KBuf buf, int mode) {
+__global__ void __launch_bounds__(224, 1) fused_kernel(KHand H, KObj O, Sdf sdf, KSim S, KOpt P, KBuf buf, int mode) {
   extern __shared__ __align__(16) unsigned char smem[];
   const SmemLayout lay(H.N, H.L, S.M);
   double* px = reinterpret_cast<double*>(smem + lay.off_px);
@@ -687,7 +841,7 @@ __global__ void __launch_bounds__(256) fused_kernel(KHand H, KObj O, Sdf sdf, KS
   e.sample_link = H.sample_link;
   e.bitmap = bitmap_all + warp * nwords;
   e.slot_point = slotpt_all + warp * kSlotCap;
-  e.stage = stage_all + warp * 160;
+  e.stage = stage_all + warp * kStageDoubles;
   e.ft = ft_all + warp * 6 * L;
   const size_t wslot = static_cast<size_t>(blockIdx.x) * M + (warp < M ? warp : 0);
   e.corr = buf.corr + wslot * buf.cap_corr;
@@ -750,7 +904,7 @@ __global__ void __launch_bounds__(256) fused_kernel(KHand H, KObj O, Sdf sdf, KS
         const V3 vm{S.vel[warp][0], S.vel[warp][1], S.vel[warp][2]};
         const bool meas = mode == kModeEval && S.measure_residual;
         const double res = run_sim(sdf, e, vm, record, meas, st, status, acc);
-        acc.flush(e.ft);
+        ft_flush_warp(acc, e.ft, lane);
         __syncwarp();
         if (lane == 0) {
           sres[warp] = res;

@@ -55,7 +55,7 @@ enum {
   DGX_E_NONFINITE_LOSS = 1,  /* "loss evaluation produced a non-finite value" (losses.cpp:15-16) */
   DGX_E_NONFINITE_GRAD = 2,  /* "tape: non-finite adjoint" (tape.cpp:35-38) */
   DGX_E_CORR_OVERFLOW = 3,   /* more active corrections than the context's log capacity */
-  DGX_E_SLOT_OVERFLOW = 4,   /* more than 256 distinct contacts in one perturbation sim */
+  DGX_E_SLOT_OVERFLOW = 4,   /* reserved (contact slots are sized N, as sim.hpp:155) */
   DGX_E_REPLAY = 5,          /* internal: adjoint replay disagreed with the forward */
   DGX_E_INVALID = 100,       /* invalid argument (std::invalid_argument / runtime_error) */
   DGX_E_CUDA = 101,

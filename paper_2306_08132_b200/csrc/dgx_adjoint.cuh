@@ -65,6 +65,8 @@ __device__ __forceinline__ Q4 rotmat_adj(Q4 q, const M3& A) {
   return r;
 }
 
+__device__ __forceinline__ V3 quat_exp_adj_trig(V3 w, Q4 g, double a, double s, double c);
+
 // E = quat_exp(w) (vec.hpp:155-168), both branches: adjoint w.r.t. w
 __device__ __forceinline__ V3 quat_exp_adj(V3 w, Q4 g) {
   double a2 = dot(w, w);
@@ -80,6 +82,18 @@ __device__ __forceinline__ V3 quat_exp_adj(V3 w, Q4 g) {
   double half = 0.5 * a;
   double s, c;
   sincos(half, &s, &c);
+  return quat_exp_adj_trig(w, g, a, s, c);
+}
+
+// trig branch of quat_exp_adj with sin / cos of the half angle supplied by
+// the forward (quat_exp_sin), so no trig is evaluated in the adjoint
+__device__ __forceinline__ V3 quat_exp_adj_sc(V3 w, Q4 g, double s, double c) {
+  double a2 = dot(w, w);
+  if (a2 < 1e-16) return quat_exp_adj(w, g);
+  return quat_exp_adj_trig(w, g, sqrt(a2), s, c);
+}
+
+__device__ __forceinline__ V3 quat_exp_adj_trig(V3 w, Q4 g, double a, double s, double c) {
   double k = s / a;
   V3 gv{g.x, g.y, g.z};
   double a_k = fdot(gv, w);

@@ -130,9 +130,12 @@ int prepare(dgx_ctx* c, const dgx_hand* h, const dgx_object* o, int M, int B, KB
   if (grid < 1) grid = 1;
   const size_t nws = static_cast<size_t>(grid) * M;
   c->corr.ensure(nws * c->cap_corr * sizeof(CorrRec));
-  c->slots.ensure(nws * kSlotCap * (sizeof(SlotRec) + sizeof(int)));
+  const size_t per = nws * static_cast<size_t>(h->N);
+  c->slots.ensure(per * (sizeof(SlotRec) + 2 * sizeof(int)));
   buf.corr = static_cast<CorrRec*>(c->corr.p);
   buf.slots = static_cast<SlotRec*>(c->slots.p);
+  buf.slot_of_point = reinterpret_cast<int*>(buf.slots + per);
+  buf.fric_order = buf.slot_of_point + per;
   buf.cap_corr = c->cap_corr;
   buf.B = B;
   return grid;
@@ -331,8 +334,14 @@ int dgx_object_upload(dgx_ctx* c, const dgx_object_desc* d, dgx_object** out) {
         throw DgxError(DGX_E_UNSUPPORTED, "object: unknown SDF kind " + std::to_string(d->kind));
       }
       o->k.mass = d->mass;
+      o->k.inv_mass = 1.0 / d->mass;
       o->k.com = V3{d->com[0], d->com[1], d->com[2]};
       for (int t = 0; t < 9; ++t) o->k.inertia_body_inv.m[t] = d->inertia_body_inv[t];
+      // predict() from the canonical state (thetadot = 0, sim.hpp:74-83) and
+      // world_inertia_inv (sim.hpp:96-100), same formulas as the kernel
+      const Q4 pred_q = qnormalized(qmul(quat_exp(V3{0.0, 0.0, 0.0}), Q4{1.0, 0.0, 0.0, 0.0}));
+      const M3 Rp = rotation_matrix(pred_q);
+      o->k.Iw = mul(mul(Rp, o->k.inertia_body_inv), transposed(Rp));
     } catch (...) {
       o->vals.release();
       delete o;

@@ -27,9 +27,11 @@
 
 #if defined(__CUDACC__)
 #define DGX_GHD __host__ __device__ __forceinline__
+#define DGX_GHD_OUTLINE __host__ __device__ __forceinline__
 #else
 #include <cmath>
 #define DGX_GHD inline
+#define DGX_GHD_OUTLINE inline
 #endif
 
 namespace dgx {
@@ -122,19 +124,28 @@ DGX_GHD V3 rotate(Q4 q, V3 v) {
   return (v + t * q.w) + cross(u, t);
 }
 
-DGX_GHD Q4 quat_exp(V3 rv) {
+// quat_exp that also reports sin(|rv|/2) (0 on the small-angle branch) for
+// the adjoint, which then needs no trig of its own
+DGX_GHD Q4 quat_exp_sin(V3 rv, double& sin_half) {
   double a2 = dot(rv, rv);
   if (a2 < 1e-16) {
+    sin_half = 0.0;
     double k = 0.5 - a2 * (1.0 / 48.0);
     return qnormalized(Q4{1.0 - a2 * 0.125, rv.x * k, rv.y * k, rv.z * k});
   }
   double a = dsqrt(a2);
   double half = 0.5 * a;
-  double k = dgx_sin(half) / a;
+  sin_half = dgx_sin(half);
+  double k = sin_half / a;
   return Q4{dgx_cos(half), rv.x * k, rv.y * k, rv.z * k};
 }
 
-DGX_GHD V3 quat_log(Q4 q) {
+DGX_GHD_OUTLINE Q4 quat_exp(V3 rv) {
+  double s;
+  return quat_exp_sin(rv, s);
+}
+
+DGX_GHD_OUTLINE V3 quat_log(Q4 q) {
   if (q.w < 0.0) q = Q4{-q.w, -q.x, -q.y, -q.z};
   double v2 = q.x * q.x + q.y * q.y + q.z * q.z;
   if (v2 < 1e-18) {

@@ -8,7 +8,6 @@ namespace dgx {
 
 constexpr int kMaxSims = 8;        // protocol velocities per candidate (standard: 7)
 constexpr int kMaxDim = 32;        // 6 + J gradient coordinates (J <= 26)
-constexpr int kSlotCap = 256;      // distinct active contacts per perturbation sim
 constexpr int kStageDoubles = 640; // per-warp staging (adjoint segment: 4 slots x 5 x 32 lanes)
 
 enum Mode : int { kModeGrad = 0, kModeEval = 1, kModeOpt = 2 };
@@ -27,8 +26,17 @@ struct CorrRec {
   double x[3];
   double q[4];
   double lam;
-  int f;      // flattened (sweep * N + point)
+  // recorded values of the correcting point (sdf.cpp:140-164, sim.hpp:160-161)
+  double g[3];      // grad_obj (recorded unit gradient)
+  double rel[3];    // p - x before the correction
+  double dx[3];     // r_local - proxy point
+  double rho_d;     // dilated distance (C = -rho_d)
+  double E[4];      // quat_exp(-lam * iwa)
+  double sin_half;  // sin(|lam * iwa| / 2), 0 on the small-angle branch
+  int f;            // flattened (sweep * N + point)
   int slot;
+  int sign;         // PhongQuery::sign
+  int fb;           // interpolated-normal fallback branch taken
 };
 
 // One contact slot (sim.hpp:149-155) plus its friction replay data and the
@@ -39,6 +47,8 @@ struct SlotRec {
   double rb[3];
   double fx[3];   // state before this slot's friction correction
   double fq[4];
+  double fE[4];   // friction's quat_exp(-lam_t * iwat) and its sin(half angle)
+  double fsin;
   double a_lam;
   double a_n[3];
   int point;
@@ -64,8 +74,10 @@ struct KHand {
 
 struct KObj {
   double mass;
+  double inv_mass;        // 1.0 / mass (sim.hpp:141)
   V3 com;
-  M3 inertia_body_inv;
+  M3 inertia_body_inv;    // InertialData::inertia_body_inv (rigid.hpp:12)
+  M3 Iw;                  // world_inertia_inv at the predicted pose (sim.hpp:96-100, 142)
 };
 
 struct KSim {
@@ -93,14 +105,16 @@ struct KBuf {
   double* traj;         // [B, k_end-k_begin, 3 + D] opt: losses + weighted grad per iterate
   int* status;          // [B]
   CorrRec* corr;        // [grid, M, cap_corr]
-  SlotRec* slots;       // [grid, M, kSlotCap]
+  SlotRec* slots;       // [grid, M, N]  contact slots (one per hand point at most)
+  int* slot_of_point;   // [grid, M, N]
+  int* fric_order;      // [grid, M, N]
   int cap_corr;
   int B;
 };
 
 // dynamic shared memory layout (bytes), identical on host and device
 struct SmemLayout {
-  int off_px, off_py, off_pz, off_link, off_ft, off_bitmap, off_slotpt, off_stage, off_misc, total;
+  int off_px, off_py, off_pz, off_link, off_ft, off_bitmap, off_stage, off_misc, total;
   __host__ __device__ static int align(int x) { return (x + 15) & ~15; }
   __host__ __device__ SmemLayout(int N, int L, int M) {
     int o = 0;
@@ -110,7 +124,6 @@ struct SmemLayout {
     off_link = o; o = align(o + 8 * 12 * L);
     off_ft = o; o = align(o + 8 * 6 * L * M);
     off_bitmap = o; o = align(o + 4 * ((N + 31) / 32) * M);
-    off_slotpt = o; o = align(o + 4 * kSlotCap * M);
     off_stage = o; o = align(o + 8 * kStageDoubles * M);
     off_misc = o; o = align(o + 8 * (64 + 4 * kMaxDim + 2 * kMaxSims));
     total = o;

@@ -39,6 +39,21 @@ namespace dgx {
 
 constexpr unsigned kFull = 0xffffffffu;
 
+// Optional region timers (profiling builds only: -DDGX_PROFILE_REGIONS).
+// Lane 0 of each warp accumulates clock64() cycles / event counts per region.
+#ifdef DGX_PROFILE_REGIONS
+__device__ unsigned long long g_prof[32];
+#define PROF_T(v) const long long v = clock64()
+#define PROF_ACC(r, v) \
+  if ((threadIdx.x & 31) == 0) atomicAdd(&g_prof[r], static_cast<unsigned long long>(clock64() - (v)))
+#define PROF_CNT(r, n) \
+  if ((threadIdx.x & 31) == 0) atomicAdd(&g_prof[r], static_cast<unsigned long long>(n))
+#else
+#define PROF_T(v)
+#define PROF_ACC(r, v)
+#define PROF_CNT(r, n)
+#endif
+
 __device__ __forceinline__ double shfl(double v, int l) { return __shfl_sync(kFull, v, l); }
 __device__ __forceinline__ V3 shfl(V3 v, int l) { return V3{shfl(v.x, l), shfl(v.y, l), shfl(v.z, l)}; }
 __device__ __forceinline__ double warp_sum(double v) {
@@ -58,17 +73,15 @@ struct SimEnv {
   const double *px, *py, *pz;
   const int* sample_link;
   unsigned* bitmap;
-  int* slot_point;
+  int* slot_of_point;     // [N] slot index, valid where the bitmap bit is set
   double* stage;
   double* ft;             // [L*6] this warp's link force / torque accumulators
   CorrRec* corr;
   SlotRec* slots;
   int* fric_order;
   int cap_corr;
-  double inv_mass, radius, alpha, mu, dt;
-  V3 com;
-  M3 Ibody_inv;           // InertialData::inertia_body_inv (rigid.hpp:12)
-  M3 Iw;                  // world inverse inertia frozen at the predicted pose
+  const KObj* O;          // mass / COM / world inverse inertia (kernel parameter space)
+  double radius, alpha, mu, dt;
   double* point_grads;    // debug, may be null
 };
 
@@ -86,7 +99,7 @@ __device__ __forceinline__ void eval_point(const Sdf& sdf, const SimEnv& e, int 
                                            bool record, PointEval& pe) {
   pe.p = V3{e.px[i], e.py[i], e.pz[i]};
   pe.rel = pe.p - x;
-  pe.rl = tmul(R, pe.rel) + e.com;
+  pe.rl = tmul(R, pe.rel) + e.O->com;
   pe.q = sdf.query(pe.rl);
   pe.fb = fabs(pe.q.rho) < kSurfaceEps;
   if (record && pe.fb) {
@@ -126,24 +139,52 @@ struct FtAcc {
   }
 };
 
-// Warp-cooperative flush: lanes holding the same link are summed with a
-// butterfly and written by one leader lane; every lane's accumulator resets.
+// Warp-cooperative flush of the per-lane link accumulators. Lanes walk
+// positions in descending order, so equal links normally occupy one
+// contiguous lane range: a single segmented inclusive scan then leaves each
+// segment's sum in its highest lane, which writes it (one writer per link, no
+// atomics). Non-contiguous key patterns (possible only for tiny hands) take
+// the keyed butterfly loop instead.
 __device__ __forceinline__ void ft_flush_warp(FtAcc& acc, double* ft, int lane) {
-  unsigned pending = __ballot_sync(0xffffffffu, acc.link >= 0);
-  while (pending) {
-    const int leader = __ffs(pending) - 1;
-    const int key = __shfl_sync(0xffffffffu, acc.link, leader);
-    const bool mine = acc.link == key;
-    pending &= ~__ballot_sync(0xffffffffu, mine);
-    double v[6] = {mine ? acc.F.x : 0.0, mine ? acc.F.y : 0.0, mine ? acc.F.z : 0.0,
-                   mine ? acc.T.x : 0.0, mine ? acc.T.y : 0.0, mine ? acc.T.z : 0.0};
+  const int key = acc.link;
+  const unsigned m = __match_any_sync(0xffffffffu, key);
+  const int lo = __ffs(m) - 1;
+  const unsigned run = m >> lo;
+  if (__all_sync(0xffffffffu, (run & (run + 1u)) == 0u)) {
+    double v[6] = {acc.F.x, acc.F.y, acc.F.z, acc.T.x, acc.T.y, acc.T.z};
 #pragma unroll
-    for (int k = 0; k < 6; ++k)
-      for (int o = 16; o > 0; o >>= 1) v[k] += __shfl_xor_sync(0xffffffffu, v[k], o);
-    if (lane == leader) {
+    for (int d = 1; d < 32; d <<= 1) {
+      double u[6];
+#pragma unroll
+      for (int k = 0; k < 6; ++k) u[k] = __shfl_up_sync(0xffffffffu, v[k], d);
+      if (lane - d >= lo) {
+#pragma unroll
+        for (int k = 0; k < 6; ++k) v[k] += u[k];
+      }
+    }
+    if (key >= 0 && lane == 31 - __clz(m)) {
       double* d = ft + 6 * key;
 #pragma unroll
       for (int k = 0; k < 6; ++k) d[k] += v[k];
+    }
+  } else {
+    unsigned pending = __ballot_sync(0xffffffffu, key >= 0);
+    while (pending) {
+      const int leader = __ffs(pending) - 1;
+      const int kk = __shfl_sync(0xffffffffu, key, leader);
+      const bool mine = key == kk;
+      pending &= ~__ballot_sync(0xffffffffu, mine);
+      double v[6] = {mine ? acc.F.x : 0.0, mine ? acc.F.y : 0.0, mine ? acc.F.z : 0.0,
+                     mine ? acc.T.x : 0.0, mine ? acc.T.y : 0.0, mine ? acc.T.z : 0.0};
+#pragma unroll
+      for (int k = 0; k < 6; ++k)
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) v[k] += __shfl_xor_sync(0xffffffffu, v[k], o);
+      if (lane == leader) {
+        double* d = ft + 6 * kk;
+#pragma unroll
+        for (int k = 0; k < 6; ++k) d[k] += v[k];
+      }
     }
   }
   __syncwarp();
@@ -163,20 +204,10 @@ struct SimStats {
   double max_pen = 0.0, max_fric = 0.0;
 };
 
-// warp-parallel lookup of the slot owning point i (slot_point in shared mem)
-__device__ __forceinline__ int find_slot(const SimEnv& e, int nslot, int i) {
-  for (int base = 0; base < nslot; base += 32) {
-    int s = base + e.lane;
-    unsigned hit = __ballot_sync(kFull, s < nslot && e.slot_point[s] == i);
-    if (hit) return base + __ffs(hit) - 1;
-  }
-  return -1;
-}
-
 // ContactSolver::apply_friction (sim.hpp:247-274) on values; returns whether
 // the state changed. Friction-ratio stat as sim.hpp:266-272.
 __device__ __forceinline__ bool friction_fwd(const SimEnv& e, V3 prev_x, Q4 prev_q, V3& x, Q4& q, V3 rb, V3 n,
-                                             double lambda_n, SimStats& st) {
+                                             double lambda_n, SimStats& st, Q4& E, double& sin_half) {
   V3 before = prev_x + rotate(prev_q, rb);
   V3 arm = rotate(q, rb);
   V3 after = x + arm;
@@ -186,13 +217,14 @@ __device__ __forceinline__ bool friction_fwd(const SimEnv& e, V3 prev_x, Q4 prev
   if (ut < 1e-12) return false;
   V3 t = u_t / ut;
   V3 at = cross(arm, t);
-  V3 iwat = mul(e.Iw, at);
-  double w_t = e.inv_mass + dot(at, iwat);
+  V3 iwat = mul(e.O->Iw, at);
+  double w_t = e.O->inv_mass + dot(at, iwat);
   if (w_t < 1e-12) return false;
   double a1 = ut / w_t, a2 = e.mu * lambda_n;
   double lam_t = a1 <= a2 ? a1 : a2;
-  x = x - t * (e.inv_mass * lam_t);
-  q = qnormalized(qmul(quat_exp(iwat * (-lam_t)), q));
+  x = x - t * (e.O->inv_mass * lam_t);
+  E = quat_exp_sin(iwat * (-lam_t), sin_half);
+  q = qnormalized(qmul(E, q));
   ++st.corrections;
   double denom = e.mu * lambda_n;
   if (denom > 0.0) {
@@ -218,22 +250,22 @@ __device__ __forceinline__ void friction_adj(const SimEnv& e, V3 prev_x, Q4 prev
   double ut = norm(u_t);
   V3 t = u_t / ut;
   V3 at = cross(arm, t);
-  V3 iwat = mul(e.Iw, at);
-  double w_t = e.inv_mass + dot(at, iwat);
+  V3 iwat = mul(e.O->Iw, at);
+  double w_t = e.O->inv_mass + dot(at, iwat);
   double a1 = ut / w_t, a2 = e.mu * s.lambda_n;
   bool first = a1 <= a2;
   double lam_t = first ? a1 : a2;
   V3 om = iwat * (-lam_t);
-  Q4 E = quat_exp(om);
+  const Q4 E{s.fE[0], s.fE[1], s.fE[2], s.fE[3]};  // logged by the forward
   Q4 P = qmul(E, fq);
   // x_out = fx - t (m^-1 lam_t)
-  V3 a_t = aX * (-e.inv_mass * lam_t);
-  double a_lamt = -e.inv_mass * fdot(t, aX);
+  V3 a_t = aX * (-e.O->inv_mass * lam_t);
+  double a_lamt = -e.O->inv_mass * fdot(t, aX);
   // q_out = normalized(E (x) fq)
   Q4 a_P = qnormalize_adj(P, aQ);
   Q4 a_E = qmul_adj_a(a_P, fq);
   Q4 aQ_in = qmul_adj_b(a_P, E);
-  V3 a_om = quat_exp_adj(om, a_E);
+  V3 a_om = quat_exp_adj_sc(om, a_E, s.fsin, E.w);
   a_lamt -= fdot(iwat, a_om);
   V3 a_iwat = a_om * (-lam_t);
   double a_a1 = first ? a_lamt : 0.0;
@@ -243,7 +275,7 @@ __device__ __forceinline__ void friction_adj(const SimEnv& e, V3 prev_x, Q4 prev
   double a_wt = -a_a1 * a1 / w_t;
   V3 a_at = iwat * a_wt;
   a_iwat = fma3(a_wt, at, a_iwat);
-  a_at = a_at + ftmul(e.Iw, a_iwat);
+  a_at = a_at + ftmul(e.O->Iw, a_iwat);
   V3 a_arm = cross(t, a_at);
   a_t = a_t + cross(a_at, arm);
   V3 a_utv = a_t / ut;
@@ -293,7 +325,7 @@ template <class Sdf>
 __device__ __forceinline__ void leak_geo(const Sdf& sdf, const SimEnv& e, int i, V3 xk, const M3& Rk, LeakGeo& L) {
   L.p = V3{e.px[i], e.py[i], e.pz[i]};
   L.rel = L.p - xk;
-  const V3 rl = ftmul(Rk, L.rel) + e.com;
+  const V3 rl = ftmul(Rk, L.rel) + e.O->com;
   FastEval fe = classify(sdf, rl, e.radius);
   L.sg = 1.0;
   L.contrib = false;
@@ -316,11 +348,11 @@ __device__ __forceinline__ void leak_geo(const Sdf& sdf, const SimEnv& e, int i,
 // gate backward -alpha; sim.hpp:107-124, tape.cpp:103-107).
 __device__ __forceinline__ bool leak_coef(const SimEnv& e, const LeakGeo& L, V3 G, double& c1, double& c0) {
   const V3 a = cross(L.rel, L.n);
-  const V3 Ia = fmul(e.Iw, a);
-  const double w = e.inv_mass + fdot(a, Ia);
+  const V3 Ia = fmul(e.O->Iw, a);
+  const double w = e.O->inv_mass + fdot(a, Ia);
   if (w < 1e-12) return false;
   const double lpc = rcp_fast(w);
-  c1 = e.alpha * e.inv_mass * lpc * L.sg;
+  c1 = e.alpha * e.O->inv_mass * lpc * L.sg;
   c0 = 0.5 * e.alpha * lpc * fdot(a, G) * L.sg;
   return true;
 }
@@ -343,43 +375,105 @@ __device__ void process_run(const Sdf& sdf, SimEnv& e, int lo, int hi, V3 xk, Q4
   const V3 H{-qk.x * aQ.w + qk.w * aQ.x - qk.z * aQ.y + qk.y * aQ.z,
              -qk.y * aQ.w + qk.z * aQ.x + qk.w * aQ.y - qk.x * aQ.z,
              -qk.z * aQ.w - qk.y * aQ.x + qk.x * aQ.y + qk.w * aQ.z};
-  const V3 G = ftmul(e.Iw, H);
+  const V3 G = ftmul(e.O->Iw, H);
   V3 X = aX;
   for (int top = hi; top > lo; top -= 32 * kSeg) {
     const int shi = top - lane * kSeg;
     const int slo = max(top - (lane + 1) * kSeg, lo);
     const int cnt = shi - slo;
-    // ---- pass 1: coefficients and this lane's composed map a -> M a + b
-    M3 Mm;
-    Mm.m[0] = 1.0; Mm.m[1] = 0.0; Mm.m[2] = 0.0;
-    Mm.m[3] = 0.0; Mm.m[4] = 1.0; Mm.m[5] = 0.0;
-    Mm.m[6] = 0.0; Mm.m[7] = 0.0; Mm.m[8] = 1.0;
-    V3 bm{0.0, 0.0, 0.0};
+    PROF_CNT(18, 1);
+    PROF_T(t1a);
+#ifdef DGX_P1A_PAIR
+    // ---- pass 1a: per point n = R g, c1, c0 -> shared staging (own lane).
+    // Two points per step: both classifications are straight-line code so the
+    // compiler overlaps their grid loads and FP64 chains; the exact query for
+    // undecided points follows (rare).
+    int i = cnt > 0 ? (shi - 1) % N : 0;
+    for (int k = 0; k < cnt; k += 2) {
+      const int i0 = i;
+      const int i1 = i0 > 0 ? i0 - 1 : N - 1;
+      LeakGeo L[2];
+      FastEval fe[2];
+      const int ii[2] = {i0, i1};
+#pragma unroll
+      for (int u = 0; u < 2; ++u) {
+        L[u].p = V3{e.px[ii[u]], e.py[ii[u]], e.pz[ii[u]]};
+        L[u].rel = L[u].p - xk;
+        fe[u] = classify(sdf, ftmul(Rk, L[u].rel) + e.O->com, e.radius);
+      }
+#pragma unroll
+      for (int u = 0; u < 2; ++u) {
+        L[u].sg = 1.0;
+        L[u].contrib = fe[u].cls > 0;
+        if (fe[u].cls == 0 && (u == 0 || k + 1 < cnt)) {  // decision boundary: exact (bit-exact) query
+          PointEval pe;
+          eval_point(sdf, e, ii[u], xk, Rk, true, pe);
+          if (!(pe.rho_d < 0.0)) {
+            fe[u].g = pe.q.grad;
+            L[u].sg = pe.fb ? static_cast<double>(pe.q.sign) : 1.0;
+            L[u].contrib = true;
+          }
+        }
+        L[u].g = fe[u].g;
+        L[u].n = fmul(Rk, fe[u].g);
+      }
+#pragma unroll
+      for (int u = 0; u < 2; ++u) {
+        if (u == 1 && k + 1 >= cnt) break;
+        double c1 = 0.0, c0 = 0.0;
+        if (!(L[u].contrib && leak_coef(e, L[u], G, c1, c0))) {
+          c1 = 0.0;
+          c0 = 0.0;
+        }
+        stg[stg_idx(k + u, 0, lane)] = c1;
+        stg[stg_idx(k + u, 1, lane)] = c0;
+        stg[stg_idx(k + u, 2, lane)] = L[u].n.x;
+        stg[stg_idx(k + u, 3, lane)] = L[u].n.y;
+        stg[stg_idx(k + u, 4, lane)] = L[u].n.z;
+      }
+      i = i1 > 0 ? i1 - 1 : N - 1;
+    }
+#else
+    // ---- pass 1a: per point n = R g, c1, c0 -> shared staging (own lane)
     int i = cnt > 0 ? (shi - 1) % N : 0;
     for (int k = 0; k < cnt; ++k) {
       LeakGeo L;
       leak_geo(sdf, e, i, xk, Rk, L);
       double c1 = 0.0, c0 = 0.0;
-      if (L.contrib && leak_coef(e, L, G, c1, c0)) {
-        const V3 n = L.n;
-        const V3 v{fma(n.z, Mm.m[6], fma(n.y, Mm.m[3], n.x * Mm.m[0])),
-                   fma(n.z, Mm.m[7], fma(n.y, Mm.m[4], n.x * Mm.m[1])),
-                   fma(n.z, Mm.m[8], fma(n.y, Mm.m[5], n.x * Mm.m[2]))};
-        const V3 cn = n * (-c1);
-        outer_acc(Mm, cn, v);
-        const double t = fdot(n, bm);
-        bm = fma3(-fma(c1, t, c0), n, bm);
-      } else {
+      if (!(L.contrib && leak_coef(e, L, G, c1, c0))) {
         c1 = 0.0;
         c0 = 0.0;
       }
       stg[stg_idx(k, 0, lane)] = c1;
       stg[stg_idx(k, 1, lane)] = c0;
-      stg[stg_idx(k, 2, lane)] = L.g.x;
-      stg[stg_idx(k, 3, lane)] = L.g.y;
-      stg[stg_idx(k, 4, lane)] = L.g.z;
+      stg[stg_idx(k, 2, lane)] = L.n.x;
+      stg[stg_idx(k, 3, lane)] = L.n.y;
+      stg[stg_idx(k, 4, lane)] = L.n.z;
       if (--i < 0) i = N - 1;
     }
+#endif
+    PROF_ACC(6, t1a);
+    PROF_T(t1b);
+    // ---- pass 1b: this lane's composed map a -> M a + b
+    M3 Mm;
+    Mm.m[0] = 1.0; Mm.m[1] = 0.0; Mm.m[2] = 0.0;
+    Mm.m[3] = 0.0; Mm.m[4] = 1.0; Mm.m[5] = 0.0;
+    Mm.m[6] = 0.0; Mm.m[7] = 0.0; Mm.m[8] = 1.0;
+    V3 bm{0.0, 0.0, 0.0};
+    for (int k = 0; k < cnt; ++k) {
+      const double c1 = stg[stg_idx(k, 0, lane)], c0 = stg[stg_idx(k, 1, lane)];
+      if (c1 != 0.0 || c0 != 0.0) {
+        const V3 n{stg[stg_idx(k, 2, lane)], stg[stg_idx(k, 3, lane)], stg[stg_idx(k, 4, lane)]};
+        const V3 v{fma(n.z, Mm.m[6], fma(n.y, Mm.m[3], n.x * Mm.m[0])),
+                   fma(n.z, Mm.m[7], fma(n.y, Mm.m[4], n.x * Mm.m[1])),
+                   fma(n.z, Mm.m[8], fma(n.y, Mm.m[5], n.x * Mm.m[2]))};
+        outer_acc(Mm, n * (-c1), v);
+        const double t = fdot(n, bm);
+        bm = fma3(-fma(c1, t, c0), n, bm);
+      }
+    }
+    PROF_ACC(7, t1b);
+    PROF_T(t2);
     // ---- pass 2: inclusive scan of maps across lanes (lane 0 applies first)
     M3 Mi = Mm;
     V3 bi = bm;
@@ -411,15 +505,17 @@ __device__ void process_run(const Sdf& sdf, SimEnv& e, int lo, int hi, V3 xk, Q4
     const V3 bl{__shfl_sync(kFull, bi.x, 31), __shfl_sync(kFull, bi.y, 31), __shfl_sync(kFull, bi.z, 31)};
     const V3 Xnext = fmul(Ml, X) + bl;
     __syncwarp();
+    PROF_ACC(8, t2);
+    PROF_T(t3);
     // ---- pass 3: re-walk with the incoming adjoint, emit contributions
     i = cnt > 0 ? (shi - 1) % N : 0;
     for (int k = 0; k < cnt; ++k) {
       const double c1 = stg[stg_idx(k, 0, lane)], c0 = stg[stg_idx(k, 1, lane)];
       if (c1 != 0.0 || c0 != 0.0) {
-        const V3 g{stg[stg_idx(k, 2, lane)], stg[stg_idx(k, 3, lane)], stg[stg_idx(k, 4, lane)]};
+        const V3 n{stg[stg_idx(k, 2, lane)], stg[stg_idx(k, 3, lane)], stg[stg_idx(k, 4, lane)]};
+        const V3 g = ftmul(Rk, n);  // R orthonormal: R^T (R g) = g to rounding
         const V3 p{e.px[i], e.py[i], e.pz[i]};
         const V3 rel = p - xk;
-        const V3 n = fmul(Rk, g);
         const double s = fma(c1, fdot(n, a), c0);
         a = fma3(-s, n, a);
         const V3 a_rel = n * s;
@@ -431,9 +527,189 @@ __device__ void process_run(const Sdf& sdf, SimEnv& e, int lo, int hi, V3 xk, Q4
     }
     X = Xnext;
     __syncwarp();
+    PROF_ACC(9, t3);
+    PROF_T(tf);
     ft_flush_warp(acc, e.ft, lane);
+    PROF_ACC(10, tf);
   }
   aX = X;
+}
+
+struct CorrIn {
+  V3 x;
+  Q4 q;
+  V3 rel, g, p, dx;
+  double C;
+  int ij, f, ncorr, nslot, sign, fb;
+};
+struct CorrOut {
+  V3 x;
+  Q4 q;
+  int applied, nslot, status, new_contact;
+};
+
+// ContactSolver::apply_contact (sim.hpp:215-245) on values for the first
+// active point of the window; logs the correction (state after it) and the
+// contact slot. Called by all lanes of the warp (identical values); lane 0
+// writes the logs.
+__device__ __forceinline__ CorrOut apply_correction(const SimEnv& e, const CorrIn in) {
+  CorrOut out;
+  out.x = in.x;
+  out.q = in.q;
+  out.applied = 0;
+  out.nslot = in.nslot;
+  out.status = kOk;
+  out.new_contact = 0;
+  const M3 R = rotation_matrix(in.q);
+  const V3 n_w = mul(R, in.g);
+  const V3 a = cross(in.rel, n_w);
+  const V3 iwa = mul(e.O->Iw, a);
+  const double w = e.O->inv_mass + dot(a, iwa);
+  if (w < 1e-12) return out;  // singular effective mass: skipped, no state change
+  const double lam = in.C / w;
+  const V3 x = in.x - n_w * (e.O->inv_mass * lam);
+  double sin_half;
+  const Q4 E = quat_exp_sin(iwa * (-lam), sin_half);
+  const Q4 q = qnormalized(qmul(E, in.q));
+  const int ij = in.ij;
+  const unsigned bit = 1u << (ij & 31);
+  const bool was = (e.bitmap[ij >> 5] & bit) != 0u;
+  int slot;
+  double lambda_n;
+  if (!was) {
+    slot = in.nslot;  // slots are sized N (sim.hpp:155): never overflows
+    out.nslot = in.nslot + 1;
+    lambda_n = 0.0 + lam;
+    if (e.lane == 0) {
+      e.bitmap[ij >> 5] |= bit;
+      e.slot_of_point[ij] = slot;
+      SlotRec& s = e.slots[slot];
+      const V3 rb = tmul(rotation_matrix(q), in.p - x);
+      s.rb[0] = rb.x; s.rb[1] = rb.y; s.rb[2] = rb.z;
+      s.a_lam = 0.0;
+      s.a_n[0] = s.a_n[1] = s.a_n[2] = 0.0;
+      s.point = ij;
+      s.fric = 0;
+    }
+  } else {
+    slot = e.slot_of_point[ij];
+    lambda_n = e.slots[slot].lambda_n + lam;
+  }
+  if (in.ncorr >= e.cap_corr) { out.status = kCorrOverflow; return out; }
+  if (e.lane == 0) {
+    SlotRec& s = e.slots[slot];
+    s.lambda_n = lambda_n;
+    s.n[0] = n_w.x; s.n[1] = n_w.y; s.n[2] = n_w.z;
+    s.last_corr = in.ncorr;
+    CorrRec& c = e.corr[in.ncorr];
+    c.x[0] = x.x; c.x[1] = x.y; c.x[2] = x.z;
+    c.q[0] = q.w; c.q[1] = q.x; c.q[2] = q.y; c.q[3] = q.z;
+    c.lam = lam;
+    c.f = in.f;
+    c.slot = slot;
+    c.g[0] = in.g.x; c.g[1] = in.g.y; c.g[2] = in.g.z;
+    c.rel[0] = in.rel.x; c.rel[1] = in.rel.y; c.rel[2] = in.rel.z;
+    c.dx[0] = in.dx.x; c.dx[1] = in.dx.y; c.dx[2] = in.dx.z;
+    c.rho_d = -in.C;
+    c.E[0] = E.w; c.E[1] = E.x; c.E[2] = E.y; c.E[3] = E.z;
+    c.sin_half = sin_half;
+    c.sign = in.sign;
+    c.fb = in.fb;
+  }
+  __syncwarp();
+  out.x = x;
+  out.q = q;
+  out.applied = 1;
+  out.new_contact = lambda_n == lam ? 1 : 0;  // sim.hpp:242
+  return out;
+}
+
+struct CorrAdj {
+  V3 aX;
+  Q4 aQ;
+  M3 aR;     // contribution to the adjoint of the R node before the correction
+  int status;
+};
+
+// Reverse of apply_contact (sim.hpp:215-245) for logged correction k, given
+// the adjoints of the state after it; returns the adjoints of the state
+// before it. Point adjoint -> the warp's link sums (lane 0 writes).
+template <class Sdf>
+__device__ __forceinline__ CorrAdj correction_adjoint(const Sdf& sdf, const SimEnv& e, int k, V3 pred_x, Q4 pred_q,
+                                                   V3 aX, Q4 aQ) {
+  CorrAdj out;
+  out.status = kOk;
+  for (int t = 0; t < 9; ++t) out.aR.m[t] = 0.0;
+  const int N = e.N;
+  const CorrRec c = e.corr[k];
+  const int i = c.f % N;
+  V3 xb = pred_x;
+  Q4 qb = pred_q;
+  if (k >= 1) {
+    const CorrRec& cp = e.corr[k - 1];
+    xb = V3{cp.x[0], cp.x[1], cp.x[2]};
+    qb = Q4{cp.q[0], cp.q[1], cp.q[2], cp.q[3]};
+  }
+  const M3 Rb = rotation_matrix(qb);
+  // recorded values of the forward (CorrRec): no SDF query / trig here
+  const V3 g{c.g[0], c.g[1], c.g[2]};
+  const V3 rel{c.rel[0], c.rel[1], c.rel[2]};
+  const V3 p{e.px[i], e.py[i], e.pz[i]};
+  const double C = -c.rho_d;
+  const V3 n_w = mul(Rb, g);
+  const V3 a = cross(rel, n_w);
+  const V3 iwa = mul(e.O->Iw, a);
+  const double w = e.O->inv_mass + dot(a, iwa);
+  const double lam = C / w;
+  if (lam != c.lam) out.status = kReplayMismatch;
+  const V3 om = iwa * (-lam);
+  const Q4 E{c.E[0], c.E[1], c.E[2], c.E[3]};
+  const Q4 P = qmul(E, qb);
+  const SlotRec& s = e.slots[c.slot];
+  double a_lam = s.a_lam;
+  V3 a_nw = s.last_corr == k ? V3{s.a_n[0], s.a_n[1], s.a_n[2]} : V3{0.0, 0.0, 0.0};
+  const Q4 a_P = qnormalize_adj(P, aQ);
+  const Q4 a_E = qmul_adj_a(a_P, qb);
+  const Q4 aQb = qmul_adj_b(a_P, E);
+  const V3 a_om = quat_exp_adj_sc(om, a_E, c.sin_half, E.w);
+  a_lam -= fdot(iwa, a_om);
+  V3 a_iwa = a_om * (-lam);
+  a_lam -= e.O->inv_mass * fdot(n_w, aX);
+  a_nw = fma3(-e.O->inv_mass * lam, aX, a_nw);
+  const double a_C = a_lam / w;
+  const double a_w = -a_lam * lam / w;
+  V3 a_a = iwa * a_w;
+  a_iwa = fma3(a_w, a, a_iwa);
+  a_a = a_a + ftmul(e.O->Iw, a_iwa);
+  V3 a_rel = cross(n_w, a_a);
+  a_nw = a_nw + cross(a_a, rel);
+  const V3 a_g = ftmul(Rb, a_nw);
+  outer_acc(out.aR, a_nw, g);
+  const double a_rho = -a_C;  // gate active: dC/drho = -1
+  V3 a_rl;
+  if (c.fb) {
+    a_rl = g * (static_cast<double>(c.sign) * a_rho);
+  } else {
+    const V3 dx{c.dx[0], c.dx[1], c.dx[2]};
+    const double dist = norm(dx);
+    const double inv = static_cast<double>(c.sign) / dist;
+    double a_dist = static_cast<double>(c.sign) * a_rho;
+    a_dist -= fdot(a_g, dx) * inv / dist;
+    a_rl = fma3(a_dist / dist, dx, a_g * inv);
+  }
+  a_rel = a_rel + fmul(Rb, a_rl);
+  outer_acc(out.aR, rel, a_rl);
+  if (e.lane == 0) {
+    double* d = e.ft + 6 * e.sample_link[i];
+    const V3 tq = cross(p, a_rel);
+    d[0] += a_rel.x; d[1] += a_rel.y; d[2] += a_rel.z;
+    d[3] += tq.x; d[4] += tq.y; d[5] += tq.z;
+    add_point_grad(e, i, a_rel);
+  }
+  __syncwarp();
+  out.aX = aX - a_rel;
+  out.aQ = aQb;
+  return out;
 }
 
 // One perturbation simulation (losses.hpp:47-57 with T = 1), forward and,
@@ -443,16 +719,15 @@ __device__ double run_sim(const Sdf& sdf, SimEnv& e, V3 v_m, bool record, bool m
                           int& status, FtAcc& acc) {
   const int lane = e.lane, N = e.N;
   // canonical_state (rigid.hpp:29-33) with xdot = v_m; predict (sim.hpp:74-83)
-  const V3 prev_x = e.com;
+  const V3 prev_x = e.O->com;
   const Q4 prev_q{1.0, 0.0, 0.0, 0.0};
   const V3 prev_thd{0.0, 0.0, 0.0};
   const V3 pred_xdot = v_m + V3{0.0 * e.dt, 0.0 * e.dt, 0.0 * e.dt};
   const V3 pred_x = prev_x + pred_xdot * e.dt;
   const Q4 pred_q = qnormalized(qmul(quat_exp(prev_thd * e.dt), prev_q));
-  {  // world_inertia_inv at the predicted orientation (sim.hpp:96-100, 142)
-    const M3 Rp = rotation_matrix(pred_q);
-    e.Iw = mul(mul(Rp, e.Ibody_inv), transposed(Rp));
-  }
+  // world_inertia_inv at the predicted orientation (sim.hpp:96-100, 142) is
+  // KObj::Iw, evaluated once on the host with the same formula (the canonical
+  // state has thetadot = 0, so every perturbation predicts the same pose)
   V3 x = pred_x;
   Q4 q = pred_q;
   M3 R = rotation_matrix(q);
@@ -461,103 +736,90 @@ __device__ double run_sim(const Sdf& sdf, SimEnv& e, V3 v_m, bool record, bool m
   for (int w = lane; w < nwords; w += 32) e.bitmap[w] = 0u;
   __syncwarp();
 
+  PROF_T(tfwd);
   // ---- Gauss-Seidel sweeps (sim.hpp:157-186) -------------------------------
-  // 32 consecutive points are classified against the current state; only
-  // candidates near / inside the dilated surface run the exact query; the
-  // first exact-active lane is applied and evaluation restarts after it.
+  // Two chunks of 32 consecutive points are classified against the current
+  // state (independent straight-line work: ILP); only candidates near /
+  // inside the dilated surface run the exact query; the first exact-active
+  // point is applied and evaluation restarts right after it. Inactive points
+  // change no forward value (sim.hpp:105-125), so this is the sequential sweep.
   int ncorr = 0, nslot = 0;
   int pos = 0, sweep = 0;
   while (sweep < e.gs) {
-    const int i = pos + lane;
-    int cls = 1;
-    if (i < N) {
-      const V3 p{e.px[i], e.py[i], e.pz[i]};
-      const V3 rl = ftmul(R, p - x) + e.com;
-      cls = classify(sdf, rl, e.radius).cls;
+    int cls[2];
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      const int i = pos + 32 * h + lane;
+      const int ic = i < N ? i : N - 1;
+      const V3 p{e.px[ic], e.py[ic], e.pz[ic]};
+      const V3 rl = ftmul(R, p - x) + e.O->com;
+      cls[h] = i < N ? classify(sdf, rl, e.radius).cls : 1;
     }
-    const unsigned cand = __ballot_sync(kFull, i < N && cls <= 0);
-    if (cand == 0u) {
-      pos += 32;
+    const unsigned cand0 = __ballot_sync(kFull, cls[0] <= 0);
+    const unsigned cand1 = __ballot_sync(kFull, cls[1] <= 0);
+    PROF_CNT(16, 1);
+    PROF_CNT(17, __popc(cand0) + __popc(cand1));
+    if ((cand0 | cand1) == 0u) {
+      pos += 64;
       if (pos >= N) { pos = 0; ++sweep; }
       continue;
     }
     PointEval pe;
-    bool act = false;
-    if (i < N && cls <= 0) {
-      eval_point(sdf, e, i, x, R, record, pe);
-      act = record ? (pe.rho_d < 0.0) : !(pe.rho_d >= 0.0);
+    int hsel = -1;
+    unsigned mask = 0u;
+#pragma unroll 1
+    for (int h = 0; h < 2; ++h) {
+      if ((h ? cand1 : cand0) == 0u) continue;
+      const int i = pos + 32 * h + lane;
+      bool act = false;
+      if ((h ? cls[1] : cls[0]) <= 0) {
+        eval_point(sdf, e, i, x, R, record, pe);
+        act = record ? (pe.rho_d < 0.0) : !(pe.rho_d >= 0.0);
+      }
+      mask = __ballot_sync(kFull, act);
+      if (mask != 0u) {
+        hsel = h;
+        break;
+      }
     }
-    const unsigned mask = __ballot_sync(kFull, act);
-    if (mask == 0u) {
-      pos += 32;
+    if (hsel < 0) {
+      pos += 64;
       if (pos >= N) { pos = 0; ++sweep; }
       continue;
     }
     const int j = __ffs(mask) - 1;
-    const int ij = pos + j;
+    const int ij = pos + 32 * hsel + j;
     const V3 rel = shfl(pe.rel, j);
     const V3 g = shfl(pe.q.grad, j);
     const V3 pj = shfl(pe.p, j);
     const double C = -shfl(pe.rho_d, j);
-    // apply_contact (sim.hpp:215-245)
-    const V3 n_w = mul(R, g);
-    const V3 a = cross(rel, n_w);
-    const V3 iwa = mul(e.Iw, a);
-    const double w = e.inv_mass + dot(a, iwa);
-    if (w < 1e-12) {
-      ++st.singular;
-    } else {
-      const double lam = C / w;
-      x = x - n_w * (e.inv_mass * lam);
-      q = qnormalized(qmul(quat_exp(iwa * (-lam)), q));
+    const V3 dxj = shfl(pe.rl - pe.q.proxy, j);
+    const int sgj = __shfl_sync(kFull, pe.q.sign, j);
+    const int fbj = __shfl_sync(kFull, pe.fb ? 1 : 0, j);
+    // apply_contact (sim.hpp:215-245), out of line (rare path)
+    PROF_T(tc);
+    const CorrOut co = apply_correction(e, CorrIn{x, q, rel, g, pj, dxj, C, ij, sweep * N + ij, ncorr, nslot, sgj, fbj});
+    PROF_ACC(1, tc);
+    PROF_CNT(20, 1);
+    if (co.status != kOk) { status = co.status; return 0.0; }
+    if (co.applied) {
+      x = co.x;
+      q = co.q;
       R = rotation_matrix(q);
       touched = true;
-      const unsigned bit = 1u << (ij & 31);
-      const bool was = (e.bitmap[ij >> 5] & bit) != 0u;
-      int slot;
-      double lambda_n;
-      if (!was) {
-        slot = nslot;
-        if (slot >= kSlotCap) { status = kSlotOverflow; return 0.0; }
-        ++nslot;
-        lambda_n = 0.0 + lam;
-        if (lane == 0) {
-          e.bitmap[ij >> 5] |= bit;
-          e.slot_point[slot] = ij;
-          SlotRec& s = e.slots[slot];
-          V3 rb = tmul(R, pj - x);
-          s.rb[0] = rb.x; s.rb[1] = rb.y; s.rb[2] = rb.z;
-          s.a_lam = 0.0;
-          s.a_n[0] = s.a_n[1] = s.a_n[2] = 0.0;
-          s.point = ij;
-          s.fric = 0;
-        }
-      } else {
-        slot = find_slot(e, nslot, ij);
-        lambda_n = e.slots[slot].lambda_n + lam;
-      }
-      if (ncorr >= e.cap_corr) { status = kCorrOverflow; return 0.0; }
-      if (lane == 0) {
-        SlotRec& s = e.slots[slot];
-        s.lambda_n = lambda_n;
-        s.n[0] = n_w.x; s.n[1] = n_w.y; s.n[2] = n_w.z;
-        s.last_corr = ncorr;
-        CorrRec& c = e.corr[ncorr];
-        c.x[0] = x.x; c.x[1] = x.y; c.x[2] = x.z;
-        c.q[0] = q.w; c.q[1] = q.x; c.q[2] = q.y; c.q[3] = q.z;
-        c.lam = lam;
-        c.f = sweep * N + ij;
-        c.slot = slot;
-      }
       ++ncorr;
+      nslot = co.nslot;
       ++st.corrections;
-      if (lambda_n == lam) ++st.active;
-      __syncwarp();
+      st.active += co.new_contact;
+    } else {
+      ++st.singular;
     }
     pos = ij + 1;
     if (pos >= N) { pos = 0; ++sweep; }
   }
 
+  PROF_ACC(0, tfwd);
+  PROF_T(tfr);
   // ---- friction (sim.hpp:188-196), active slots in point order -------------
   int nfric = 0;
   if (e.mu > 0.0) {
@@ -567,21 +829,25 @@ __device__ double run_sim(const Sdf& sdf, SimEnv& e, V3 v_m, bool record, bool m
         const int b = __ffs(bits) - 1;
         bits &= bits - 1u;
         const int pt = wd * 32 + b;
-        const int slot = find_slot(e, nslot, pt);
+        const int slot = e.slot_of_point[pt];
         const SlotRec& s = e.slots[slot];
         const double lambda_n = s.lambda_n;
         if (lambda_n <= 0.0) continue;
         const V3 x_in = x;
         const Q4 q_in = q;
+        Q4 fE{1.0, 0.0, 0.0, 0.0};
+        double fsin = 0.0;
         const bool applied =
             friction_fwd(e, prev_x, prev_q, x, q, V3{s.rb[0], s.rb[1], s.rb[2]}, V3{s.n[0], s.n[1], s.n[2]},
-                         lambda_n, st);
+                         lambda_n, st, fE, fsin);
         if (applied) {
           touched = true;
           if (lane == 0) {
             SlotRec& sw = e.slots[slot];
             sw.fx[0] = x_in.x; sw.fx[1] = x_in.y; sw.fx[2] = x_in.z;
             sw.fq[0] = q_in.w; sw.fq[1] = q_in.x; sw.fq[2] = q_in.y; sw.fq[3] = q_in.z;
+            sw.fE[0] = fE.w; sw.fE[1] = fE.x; sw.fE[2] = fE.y; sw.fE[3] = fE.z;
+            sw.fsin = fsin;
             sw.fric = 1;
             e.fric_order[nfric] = slot;
           }
@@ -592,6 +858,9 @@ __device__ double run_sim(const Sdf& sdf, SimEnv& e, V3 v_m, bool record, bool m
     }
   }
 
+  PROF_ACC(2, tfr);
+  PROF_CNT(21, nfric);
+  PROF_CNT(22, 1);
   // ---- finalize_velocities (sim.hpp:276-287) and residual ------------------
   V3 xdot, thd;
   Q4 qd{0.0, 0.0, 0.0, 0.0};
@@ -612,7 +881,7 @@ __device__ double run_sim(const Sdf& sdf, SimEnv& e, V3 v_m, bool record, bool m
     double mp = 0.0;
     for (int i = lane; i < N; i += 32) {
       V3 p{e.px[i], e.py[i], e.pz[i]};
-      V3 rl = tmul(Rf, p - x) + e.com;
+      V3 rl = tmul(Rf, p - x) + e.O->com;
       SdfQuery qq = sdf.query(rl);
       double rho = qq.rho - e.radius;
       if (rho < 0.0) mp = mp < -rho ? -rho : mp;
@@ -627,6 +896,7 @@ __device__ double run_sim(const Sdf& sdf, SimEnv& e, V3 v_m, bool record, bool m
   Q4 aQ = qmul_adj_a(quat_log_adj(qd, a_thd * inv_dt), qconj(prev_q));
   V3 aX = a_xdot * inv_dt;
 
+  PROF_T(tfa);
   // ---- friction, reverse --------------------------------------------------
   for (int k = nfric - 1; k >= 0; --k) {
     const int slot = e.fric_order[k];
@@ -643,6 +913,7 @@ __device__ double run_sim(const Sdf& sdf, SimEnv& e, V3 v_m, bool record, bool m
     __syncwarp();
   }
 
+  PROF_ACC(4, tfa);
   // ---- sweeps, reverse ----------------------------------------------------
   M3 aR;  // per-lane partial adjoint of the current R node
   for (int k = 0; k < 9; ++k) aR.m[k] = 0.0;
@@ -658,80 +929,24 @@ __device__ double run_sim(const Sdf& sdf, SimEnv& e, V3 v_m, bool record, bool m
     }
     const M3 Rk = rotation_matrix(qk);
     const int lo = k >= 0 ? e.corr[k].f + 1 : 0;
+    PROF_T(tpr);
     process_run(sdf, e, lo, hi, xk, qk, Rk, aQ, aX, aR, acc);
+    PROF_ACC(5, tpr);
+    PROF_CNT(19, 1);
     if (k < 0) break;
 
+    PROF_T(tca);
     // ---- active correction k (sim.hpp:215-245), reverse ----
     const M3 aRk = warp_sum(aR);
     aQ = qadd(aQ, rotmat_adj(qk, aRk));
     for (int t = 0; t < 9; ++t) aR.m[t] = 0.0;
-    const CorrRec c = e.corr[k];
-    const int i = c.f % N;
-    V3 xb = pred_x;
-    Q4 qb = pred_q;
-    if (k >= 1) {
-      const CorrRec& cp = e.corr[k - 1];
-      xb = V3{cp.x[0], cp.x[1], cp.x[2]};
-      qb = Q4{cp.q[0], cp.q[1], cp.q[2], cp.q[3]};
-    }
-    const M3 Rb = rotation_matrix(qb);
-    PointEval pe;
-    eval_point(sdf, e, i, xb, Rb, true, pe);
-    const double C = -pe.rho_d;
-    const V3 g = pe.q.grad;
-    const V3 n_w = mul(Rb, g);
-    const V3 a = cross(pe.rel, n_w);
-    const V3 iwa = mul(e.Iw, a);
-    const double w = e.inv_mass + dot(a, iwa);
-    const double lam = C / w;
-    if (lam != c.lam) status = kReplayMismatch;
-    const V3 om = iwa * (-lam);
-    const Q4 E = quat_exp(om);
-    const Q4 P = qmul(E, qb);
-    const SlotRec& s = e.slots[c.slot];
-    double a_lam = s.a_lam;
-    V3 a_nw = s.last_corr == k ? V3{s.a_n[0], s.a_n[1], s.a_n[2]} : V3{0.0, 0.0, 0.0};
-    const Q4 a_P = qnormalize_adj(P, aQ);
-    const Q4 a_E = qmul_adj_a(a_P, qb);
-    const Q4 aQb = qmul_adj_b(a_P, E);
-    const V3 a_om = quat_exp_adj(om, a_E);
-    a_lam -= fdot(iwa, a_om);
-    V3 a_iwa = a_om * (-lam);
-    a_lam -= e.inv_mass * fdot(n_w, aX);
-    a_nw = fma3(-e.inv_mass * lam, aX, a_nw);
-    const double a_C = a_lam / w;
-    const double a_w = -a_lam * lam / w;
-    V3 a_a = iwa * a_w;
-    a_iwa = fma3(a_w, a, a_iwa);
-    a_a = a_a + ftmul(e.Iw, a_iwa);
-    V3 a_rel = cross(n_w, a_a);
-    a_nw = a_nw + cross(a_a, pe.rel);
-    const V3 a_g = ftmul(Rb, a_nw);
-    if (lane == 0) outer_acc(aR, a_nw, g);
-    const double a_rho = -a_C;  // gate active: dC/drho = -1
-    V3 a_rl;
-    if (pe.fb) {
-      a_rl = g * (static_cast<double>(pe.q.sign) * a_rho);
-    } else {
-      const V3 dx = pe.rl - pe.q.proxy;
-      const double dist = norm(dx);
-      const double inv = static_cast<double>(pe.q.sign) / dist;
-      double a_dist = static_cast<double>(pe.q.sign) * a_rho;
-      a_dist -= fdot(a_g, dx) * inv / dist;
-      a_rl = fma3(a_dist / dist, dx, a_g * inv);
-    }
-    a_rel = a_rel + fmul(Rb, a_rl);
-    if (lane == 0) {
-      outer_acc(aR, pe.rel, a_rl);
-      double* d = e.ft + 6 * e.sample_link[i];
-      const V3 tq = cross(pe.p, a_rel);
-      d[0] += a_rel.x; d[1] += a_rel.y; d[2] += a_rel.z;
-      d[3] += tq.x; d[4] += tq.y; d[5] += tq.z;
-      add_point_grad(e, i, a_rel);
-    }
-    __syncwarp();
-    aX = aX - a_rel;
-    aQ = aQb;
+    const CorrAdj ca = correction_adjoint(sdf, e, k, pred_x, pred_q, aX, aQ);
+    if (ca.status != kOk) status = ca.status;
+    if (lane == 0) aR = ca.aR;
+    aX = ca.aX;
+    aQ = ca.aQ;
+    PROF_ACC(11, tca);
+    const CorrRec& c = e.corr[k];
     hi = c.f;
   }
   return residual;
@@ -740,7 +955,7 @@ __device__ double run_sim(const Sdf& sdf, SimEnv& e, V3 v_m, bool record, bool m
 // HandModel::forward (hand.hpp:116-152) link transforms, lane 0 serial over
 // the BFS order. base_q is the recorded orientation quat_exp(0) (x) q0
 // (hand.cpp:250-253) on the recorded path, q0 itself on the forward path.
-__device__ void link_transforms(const KHand& H, const double* qv, bool record, double* link) {
+__device__ __forceinline__ void link_transforms(const KHand& H, const double* qv, bool record, double* link) {
   Q4 q0{qv[3], qv[4], qv[5], qv[6]};
   Q4 base_q = record ? qmul(quat_exp(V3{0.0, 0.0, 0.0}), q0) : q0;
   for (int k = 0; k < H.L; ++k) {
@@ -774,7 +989,7 @@ __device__ void link_transforms(const KHand& H, const double* qv, bool record, d
 
 // FK adjoint: link force/torque sums -> gradient [pos | tangent | joints]
 // (hand.cpp:246-257 layout). ft is consumed (subtree sums in place).
-__device__ void fk_adjoint(const KHand& H, const double* qv, const double* link, double* ft, double* g) {
+__device__ __forceinline__ void fk_adjoint(const KHand& H, const double* qv, const double* link, double* ft, double* g) {
   for (int k = H.L - 1; k >= 1; --k) {
     const int li = H.topo[k];
     const int par = H.joint_parent[H.link_parent_joint[li]];
@@ -811,7 +1026,7 @@ __device__ void fk_adjoint(const KHand& H, const double* qv, const double* link,
 }
 
 template <class Sdf>
-__global__ void __launch_bounds__(224, 1) fused_kernel(KHand H, KObj O, Sdf sdf, KSim S, KOpt P, KBuf buf, int mode) {
+__global__ void __launch_bounds__(224, 1) fused_kernel(KHand H, const __grid_constant__ KObj O, Sdf sdf, KSim S, KOpt P, KBuf buf, int mode) {
   extern __shared__ __align__(16) unsigned char smem[];
   const SmemLayout lay(H.N, H.L, S.M);
   double* px = reinterpret_cast<double*>(smem + lay.off_px);
@@ -820,7 +1035,6 @@ __global__ void __launch_bounds__(224, 1) fused_kernel(KHand H, KObj O, Sdf sdf,
   double* link = reinterpret_cast<double*>(smem + lay.off_link);
   double* ft_all = reinterpret_cast<double*>(smem + lay.off_ft);
   unsigned* bitmap_all = reinterpret_cast<unsigned*>(smem + lay.off_bitmap);
-  int* slotpt_all = reinterpret_cast<int*>(smem + lay.off_slotpt);
   double* stage_all = reinterpret_cast<double*>(smem + lay.off_stage);
   double* misc = reinterpret_cast<double*>(smem + lay.off_misc);
   double* sq = misc;               // [40] configuration
@@ -840,17 +1054,16 @@ __global__ void __launch_bounds__(224, 1) fused_kernel(KHand H, KObj O, Sdf sdf,
   e.px = px; e.py = py; e.pz = pz;
   e.sample_link = H.sample_link;
   e.bitmap = bitmap_all + warp * nwords;
-  e.slot_point = slotpt_all + warp * kSlotCap;
+
   e.stage = stage_all + warp * kStageDoubles;
   e.ft = ft_all + warp * 6 * L;
   const size_t wslot = static_cast<size_t>(blockIdx.x) * M + (warp < M ? warp : 0);
   e.corr = buf.corr + wslot * buf.cap_corr;
-  e.slots = buf.slots + wslot * kSlotCap;
-  e.fric_order = reinterpret_cast<int*>(buf.slots + static_cast<size_t>(gridDim.x) * M * kSlotCap) + wslot * kSlotCap;
+  e.slots = buf.slots + wslot * N;
+  e.slot_of_point = buf.slot_of_point + wslot * N;
+  e.fric_order = buf.fric_order + wslot * N;
   e.cap_corr = buf.cap_corr;
-  e.inv_mass = 1.0 / O.mass;
-  e.com = O.com;
-  e.Ibody_inv = O.inertia_body_inv;
+  e.O = &O;
   e.alpha = S.alpha;
   e.mu = S.mu;
   e.dt = S.dt;
@@ -903,7 +1116,9 @@ __global__ void __launch_bounds__(224, 1) fused_kernel(KHand H, KObj O, Sdf sdf,
         FtAcc acc;
         const V3 vm{S.vel[warp][0], S.vel[warp][1], S.vel[warp][2]};
         const bool meas = mode == kModeEval && S.measure_residual;
+        PROF_T(tsim);
         const double res = run_sim(sdf, e, vm, record, meas, st, status, acc);
+        PROF_ACC(12, tsim);
         ft_flush_warp(acc, e.ft, lane);
         __syncwarp();
         if (lane == 0) {
@@ -1150,3 +1365,15 @@ cudaError_t launch_step(int J, const double* q, const double* g, double lr, doub
 }
 
 }  // namespace dgx
+
+#ifdef DGX_PROFILE_REGIONS
+extern "C" int dgx_prof_read(unsigned long long* out, int n, int reset) {
+  if (n > 32) n = 32;
+  cudaMemcpyFromSymbol(out, dgx::g_prof, sizeof(unsigned long long) * n);
+  if (reset) {
+    unsigned long long z[32] = {0};
+    cudaMemcpyToSymbol(dgx::g_prof, z, sizeof z);
+  }
+  return cudaGetLastError() == cudaSuccess ? 0 : 101;
+}
+#endif

@@ -29,8 +29,11 @@
 
 #if defined(__CUDACC__)
 #define DGX_HD __host__ __device__ __forceinline__
+/* out of line on the device: rare-path calls keep the hot loops icache-resident */
+#define DGX_HD_OUTLINE __host__ __device__ __forceinline__
 #else
 #define DGX_HD static inline
+#define DGX_HD_OUTLINE static inline
 #endif
 
 #if defined(__CUDA_ARCH__)
@@ -135,7 +138,7 @@ DGX_HD int dgx_reduce_pio2(double x, double* y, double* yl) {
   return n & 3;
 }
 
-DGX_HD double dgx_sin(double x) {
+DGX_HD_OUTLINE double dgx_sin(double x) {
   if (dgx_isnan(x) || dgx_isinf(x)) return DGX_SUB(x, x);
   double y, yl;
   int n = dgx_reduce_pio2(x, &y, &yl);
@@ -147,7 +150,7 @@ DGX_HD double dgx_sin(double x) {
   }
 }
 
-DGX_HD double dgx_cos(double x) {
+DGX_HD_OUTLINE double dgx_cos(double x) {
   if (dgx_isnan(x) || dgx_isinf(x)) return DGX_SUB(x, x);
   double y, yl;
   int n = dgx_reduce_pio2(x, &y, &yl);
@@ -206,7 +209,7 @@ DGX_HD double dgx_atan_pos(double t) {
   return DGX_SUB(hi, DGX_SUB(DGX_SUB(ts, lo), t));
 }
 
-DGX_HD double dgx_atan2(double y, double x) {
+DGX_HD_OUTLINE double dgx_atan2(double y, double x) {
   const double pi = 3.1415926535897931160e+00, pi_lo = 1.2246467991473531772e-16;
   const double pio2 = 1.57079632679489655800e+00, pio4 = 7.85398163397448278999e-01;
   if (dgx_isnan(x) || dgx_isnan(y)) return DGX_ADD(x, y);

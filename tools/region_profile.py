@@ -1,0 +1,54 @@
+"""Per-region cycle breakdown of the fused kernel (profiling build).
+
+  DGX_LIBRARY=exp/libdgx_prof.so python tools/region_profile.py
+(build: nvcc ... -DDGX_PROFILE_REGIONS -shared csrc/*.cu -o exp/libdgx_prof.so)
+Cycles are summed over warps (lane 0), so shares are of total warp-time.
+"""
+import ctypes as C
+import os
+import sys
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+from paper_2306_08132_b200 import api, capi, init, model  # noqa: E402
+
+NAMES = {0: "forward sweeps (incl. corrections)", 1: "  apply_correction", 2: "friction fwd",
+         4: "friction adjoint", 5: "adjoint runs (process_run)", 6: "  pass 1a (classify+coef)",
+         7: "  pass 1b (compose)", 8: "  pass 2 (scan)", 9: "  pass 3 (emit)", 10: "  flush",
+         11: "correction adjoints", 12: "run_sim total"}
+COUNTS = {16: "forward chunk iterations", 17: "forward candidate lanes", 18: "adjoint blocks", 19: "runs",
+          20: "forward corrections tried", 21: "frictions applied", 22: "sims"}
+
+
+def main():
+    hand_name = sys.argv[1] if len(sys.argv) > 1 else "allegro16"
+    B = int(sys.argv[2]) if len(sys.argv) > 2 else 512
+    L = capi.load()
+    L.dgx_prof_read.argtypes = [C.POINTER(C.c_ulonglong), C.c_int, C.c_int]
+    ctx = api.Context(0)
+    hd = model.HandDesc.asset(hand_name)
+    od = model.box_grid(res=64)
+    hand, obj = api.Hand(ctx, hd), api.GraspObject(ctx, od)
+    q = init.approach_init(od, hd, B, seed=17)
+    proto, w = api.StabilityProtocol.standard(), api.LossWeights()
+    opt = api.OptConfig(iterations=500)
+    buf = (C.c_ulonglong * 32)()
+    out = api.optimize(ctx, obj, hand, q, proto, api.SimParams(), w, opt, k_begin=0, k_end=2)
+    L.dgx_prof_read(buf, 32, 1)
+    out = api.optimize(ctx, obj, hand, out["q"], proto, api.SimParams(), w, opt, k_begin=2, k_end=3,
+                       adam_m=out["m"], adam_v=out["v"])
+    L.dgx_prof_read(buf, 32, 1)
+    v = np.array(list(buf), dtype=np.float64)
+    ci = B * 1
+    tot = v[12]
+    print(f"{hand_name} B={B}: per candidate-iteration (7 sims), cycles summed over warps")
+    for k, n in NAMES.items():
+        print(f"  {n:38s} {v[k] / ci:12.0f} cyc  {100 * v[k] / tot:5.1f}%")
+    for k, n in COUNTS.items():
+        print(f"  {n:38s} {v[k] / ci:12.1f} per cand-iter")
+
+
+if __name__ == "__main__":
+    main()

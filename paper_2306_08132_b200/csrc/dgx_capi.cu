@@ -67,7 +67,7 @@ struct dgx_ctx {
   cudaStream_t stream = nullptr;
   int cap_corr = 1024;
   int64_t launches = 0;
-  DevBuf corr, slots, io;
+  DevBuf corr, slots, io, ftg;
 };
 
 struct dgx_hand {
@@ -136,6 +136,8 @@ int prepare(dgx_ctx* c, const dgx_hand* h, const dgx_object* o, int M, int B, KB
   buf.slots = static_cast<SlotRec*>(c->slots.p);
   buf.slot_of_point = reinterpret_cast<int*>(buf.slots + per);
   buf.fric_order = buf.slot_of_point + per;
+  c->ftg.ensure(nws * 6 * static_cast<size_t>(h->L) * sizeof(double));
+  buf.ft_global = static_cast<double*>(c->ftg.p);
   buf.cap_corr = c->cap_corr;
   buf.B = B;
   return grid;
@@ -210,6 +212,7 @@ int dgx_ctx_destroy(dgx_ctx* c) {
     cudaSetDevice(c->device);
     c->corr.release();
     c->slots.release();
+    c->ftg.release();
     c->io.release();
     if (c->own) cudaStreamDestroy(c->own);
     delete c;

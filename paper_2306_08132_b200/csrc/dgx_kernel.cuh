@@ -108,6 +108,7 @@ struct KBuf {
   SlotRec* slots;       // [grid, M, N]  contact slots (one per hand point at most)
   int* slot_of_point;   // [grid, M, N]
   int* fric_order;      // [grid, M, N]
+  double* ft_global;    // [grid, M, L*6] adjoint link-sum spill buffers
   int cap_corr;
   int B;
 };

@@ -75,7 +75,9 @@ struct SimEnv {
   unsigned* bitmap;
   int* slot_of_point;     // [N] slot index, valid where the bitmap bit is set
   double* stage;
-  double* ft;             // [L*6] this warp's link force / torque accumulators
+  double* ft;             // [L*6] this warp's link force / torque accumulators (shared)
+  double* gft;            // [L*6] this warp's global spill buffer for the adjoint walk
+  int L;
   CorrRec* corr;
   SlotRec* slots;
   int* fric_order;
@@ -112,9 +114,10 @@ __device__ __forceinline__ void eval_point(const Sdf& sdf, const SimEnv& e, int 
 }
 
 // Per-lane accumulator of d/dp folded into per-link force / torque sums
-// (F_l = sum adj_p, T_l = sum p x adj_p). A lane crossing a link boundary
-// mid-walk spills its partial with a (rare) shared atomic; the common path is
-// the warp-cooperative flush below (no atomics).
+// (F_l = sum adj_p, T_l = sum p x adj_p). When a lane's walk moves to another
+// link it spills its partial to the warp's global link buffer with native
+// FP64 reductions (RED.ADD.F64: fire-and-forget, no shared-memory CAS); the
+// buffer is folded into the shared sums once per perturbation sim.
 struct FtAcc {
   int link = -1;
   V3 F{0.0, 0.0, 0.0}, T{0.0, 0.0, 0.0};
@@ -128,6 +131,9 @@ struct FtAcc {
     atomicAdd(d + 0, F.x); atomicAdd(d + 1, F.y); atomicAdd(d + 2, F.z);
     atomicAdd(d + 3, T.x); atomicAdd(d + 4, T.y); atomicAdd(d + 5, T.z);
     reset();
+  }
+  __device__ __forceinline__ void spill_if_any(double* ft) {
+    if (link >= 0) spill(ft);
   }
   __device__ __forceinline__ void add(double* ft, int l, V3 ap, V3 p) {
     if (l != link) {
@@ -520,7 +526,7 @@ __device__ void process_run(const Sdf& sdf, SimEnv& e, int lo, int hi, V3 xk, Q4
         a = fma3(-s, n, a);
         const V3 a_rel = n * s;
         outer_acc(aR, rel, g * s);
-        acc.add(e.ft, e.sample_link[i], a_rel, p);
+        acc.add(e.gft, e.sample_link[i], a_rel, p);
         add_point_grad(e, i, a_rel);
       }
       if (--i < 0) i = N - 1;
@@ -528,9 +534,6 @@ __device__ void process_run(const Sdf& sdf, SimEnv& e, int lo, int hi, V3 xk, Q4
     X = Xnext;
     __syncwarp();
     PROF_ACC(9, t3);
-    PROF_T(tf);
-    ft_flush_warp(acc, e.ft, lane);
-    PROF_ACC(10, tf);
   }
   aX = X;
 }
@@ -890,6 +893,8 @@ __device__ double run_sim(const Sdf& sdf, SimEnv& e, V3 v_m, bool record, bool m
   }
   if (!record || !touched) return residual;  // untouched: constant loss, zero gradient
 
+  for (int t = lane; t < 6 * e.L; t += 32) e.gft[t] = 0.0;
+  __syncwarp();
   // ---- adjoint: residual -> finalize ---------------------------------------
   const V3 a_xdot = n1 > 0.0 ? xdot / n1 : V3{0.0, 0.0, 0.0};
   const V3 a_thd = n2 > 0.0 ? thd / n2 : V3{0.0, 0.0, 0.0};
@@ -949,6 +954,14 @@ __device__ double run_sim(const Sdf& sdf, SimEnv& e, V3 v_m, bool record, bool m
     const CorrRec& c = e.corr[k];
     hi = c.f;
   }
+  // fold the global spill buffer into the warp's shared link sums
+  PROF_T(tf);
+  acc.spill_if_any(e.gft);
+  __threadfence();
+  __syncwarp();
+  for (int t = lane; t < 6 * e.L; t += 32) e.ft[t] += __ldcg(e.gft + t);
+  __syncwarp();
+  PROF_ACC(10, tf);
   return residual;
 }
 
@@ -1060,6 +1073,8 @@ __global__ void __launch_bounds__(224, 1) fused_kernel(KHand H, const __grid_con
   const size_t wslot = static_cast<size_t>(blockIdx.x) * M + (warp < M ? warp : 0);
   e.corr = buf.corr + wslot * buf.cap_corr;
   e.slots = buf.slots + wslot * N;
+  e.gft = buf.ft_global + wslot * 6 * L;
+  e.L = L;
   e.slot_of_point = buf.slot_of_point + wslot * N;
   e.fric_order = buf.fric_order + wslot * N;
   e.cap_corr = buf.cap_corr;

@@ -1,0 +1,276 @@
+// include/dgx/diffgrasp.hpp — drop-in C++ API over libdgx_cuda.so for code
+// written against the reference library (/root/reference/proj/include/
+// diffgrasp). Header-only; needs the reference headers on the include path
+// (it consumes dg:: types) and links -ldgx_cuda.
+//
+// Mapping (reference -> here), same argument meaning, same exception types
+// and messages:
+//   dg::HandModel::forward(const HandConfig&)      hand.hpp:86      -> dgx::forward
+//   dg::loss_gradient(obj, hand, q, proto, params) losses.hpp:126   -> dgx::loss_gradient
+//   dg::evaluate_losses(obj, hand, q, proto, params) losses.hpp:119 -> dgx::evaluate_losses
+//   dg::apply_gradient_step(q, grad, lr)           losses.hpp:136   -> dgx::apply_gradient_step
+// plus batched overloads over std::span<const dg::HandConfig> and the fused
+// synthesis loop dgx::optimize (the reference has none).
+//
+// The object: the reference's GraspObject is mesh-only; the B200 path takes an
+// analytic / grid SDF (dgx::SdfSpec) and the object's dg::InertialData
+// (rigid.hpp:8-13), e.g. taken from a dg::GraspObject built on the same shape.
+#pragma once
+
+#include <cstdint>
+#include <span>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "diffgrasp/hand.hpp"
+#include "diffgrasp/losses.hpp"
+#include "diffgrasp/rigid.hpp"
+#include "diffgrasp/sim.hpp"
+#include "dgx.h"
+
+namespace dgx {
+
+namespace detail {
+inline void check(int rc) {
+  if (rc == DGX_OK) return;
+  const std::string msg = dgx_last_error();
+  if (rc == DGX_E_INVALID && msg.find("dilation radius") != std::string::npos) throw std::invalid_argument(msg);
+  throw std::runtime_error(msg);
+}
+// per-candidate status -> the reference's exception (losses.cpp:15-16, tape.cpp:35-38)
+inline void check_candidate(int32_t st) {
+  switch (st) {
+    case DGX_OK: return;
+    case DGX_E_NONFINITE_LOSS: throw std::runtime_error("loss evaluation produced a non-finite value");
+    case DGX_E_NONFINITE_GRAD: throw std::runtime_error("tape: non-finite adjoint");
+    default: throw std::runtime_error("dgx: candidate failed with status " + std::to_string(st));
+  }
+}
+inline std::vector<double> pack(const dg::HandConfig& q) {
+  std::vector<double> v{q.base_position.x, q.base_position.y, q.base_position.z, q.base_orientation.w,
+                        q.base_orientation.x, q.base_orientation.y, q.base_orientation.z};
+  v.insert(v.end(), q.joint_angles.begin(), q.joint_angles.end());
+  return v;
+}
+inline dg::HandConfig unpack(const double* v, int J) {
+  dg::HandConfig q;
+  q.base_position = {v[0], v[1], v[2]};
+  q.base_orientation = {v[3], v[4], v[5], v[6]};
+  q.joint_angles.assign(v + 7, v + 7 + J);
+  return q;
+}
+inline dgx_params params_of(const dg::StabilityProtocol& proto, const dg::SimParams& p,
+                            const dg::LossWeights& w = {}) {
+  if (proto.m() > 8) throw std::runtime_error("dgx: at most 8 perturbation velocities");
+  dgx_params c{};
+  c.dt = p.dt;
+  c.mu = p.mu;
+  c.gs_iters = p.gs_iters;
+  c.steps = proto.steps;
+  c.dilation_radius = p.dilation_radius;
+  c.alpha_leak = p.leak.alpha_leak;
+  c.num_velocities = proto.m();
+  for (int m = 0; m < proto.m(); ++m) {
+    c.velocities[m][0] = proto.velocities[m].x;
+    c.velocities[m][1] = proto.velocities[m].y;
+    c.velocities[m][2] = proto.velocities[m].z;
+  }
+  c.w_stable = w.stable;
+  c.w_qrange = w.qrange;
+  c.w_qlimit = w.qlimit;
+  return c;
+}
+}  // namespace detail
+
+// One device + stream.
+class Runtime {
+ public:
+  explicit Runtime(int device = 0) { detail::check(dgx_ctx_create(device, &ctx_)); }
+  ~Runtime() { dgx_ctx_destroy(ctx_); }
+  Runtime(const Runtime&) = delete;
+  Runtime& operator=(const Runtime&) = delete;
+  dgx_ctx* get() const { return ctx_; }
+
+ private:
+  dgx_ctx* ctx_ = nullptr;
+};
+
+// A dg::HandModel resident on the device (samples in forward() order).
+class Hand {
+ public:
+  Hand(Runtime& rt, const dg::HandModel& h) : J_(h.num_joints()), N_(h.total_samples()) {
+    const int L = h.num_links();
+    std::vector<int32_t> topo{h.base_link()}, lpj(L), jp(J_), jc(J_), sl;
+    for (std::size_t head = 0; head < topo.size(); ++head)  // BFS of hand.cpp:177-194
+      for (int j = 0; j < J_; ++j)
+        if (h.joints()[j].parent_link == topo[head]) topo.push_back(h.joints()[j].child_link);
+    std::vector<double> axis, oR, ot, lo, up, smp;
+    for (int l = 0; l < L; ++l) lpj[l] = h.links()[l].parent_joint;
+    for (int j = 0; j < J_; ++j) {
+      const auto& jt = h.joints()[j];
+      jp[j] = jt.parent_link;
+      jc[j] = jt.child_link;
+      axis.insert(axis.end(), {jt.axis.x, jt.axis.y, jt.axis.z});
+      oR.insert(oR.end(), jt.origin_R.m.begin(), jt.origin_R.m.end());
+      ot.insert(ot.end(), {jt.origin_t.x, jt.origin_t.y, jt.origin_t.z});
+      lo.push_back(jt.lower);
+      up.push_back(jt.upper);
+    }
+    for (int l = 0; l < L; ++l)
+      for (const auto& s : h.links()[l].samples) {
+        smp.insert(smp.end(), {s.x, s.y, s.z});
+        sl.push_back(l);
+      }
+    dgx_hand_desc d{L, J_, N_, topo.data(), lpj.data(), jp.data(), jc.data(), axis.data(), oR.data(), ot.data(),
+                    lo.data(), up.data(), smp.data(), sl.data()};
+    detail::check(dgx_hand_upload(rt.get(), &d, &h_));
+  }
+  ~Hand() { dgx_hand_free(h_); }
+  Hand(const Hand&) = delete;
+  Hand& operator=(const Hand&) = delete;
+  const dgx_hand* get() const { return h_; }
+  int num_joints() const { return J_; }
+  int num_samples() const { return N_; }
+
+ private:
+  dgx_hand* h_ = nullptr;
+  int J_, N_;
+};
+
+// SDF backend description (csrc/dgx_geom.h): sphere, box, or FP32 grid.
+struct SdfSpec {
+  int kind = DGX_SDF_SPHERE;
+  double center[3] = {0, 0, 0};
+  double radius = 0.0;
+  double half_extents[3] = {0, 0, 0};
+  int dims[3] = {0, 0, 0};
+  double origin[3] = {0, 0, 0};
+  double spacing = 0.0, inv_spacing = 0.0;
+  std::vector<float> values;
+};
+
+class Object {
+ public:
+  Object(Runtime& rt, const SdfSpec& s, const dg::InertialData& in) {
+    dgx_object_desc d{};
+    d.kind = s.kind;
+    for (int k = 0; k < 3; ++k) {
+      d.center[k] = s.center[k];
+      d.half_extents[k] = s.half_extents[k];
+      d.dims[k] = s.dims[k];
+      d.origin[k] = s.origin[k];
+    }
+    d.radius = s.radius;
+    d.spacing = s.spacing;
+    d.inv_spacing = s.inv_spacing;
+    d.values = s.values.empty() ? nullptr : s.values.data();
+    d.mass = in.mass;
+    d.com[0] = in.com.x; d.com[1] = in.com.y; d.com[2] = in.com.z;
+    for (int k = 0; k < 9; ++k) d.inertia_body_inv[k] = in.inertia_body_inv.m[k];
+    detail::check(dgx_object_upload(rt.get(), &d, &o_));
+  }
+  ~Object() { dgx_object_free(o_); }
+  Object(const Object&) = delete;
+  Object& operator=(const Object&) = delete;
+  const dgx_object* get() const { return o_; }
+
+ private:
+  dgx_object* o_ = nullptr;
+};
+
+// ---- reference signatures (batch of one) ------------------------------------
+
+inline std::vector<dg::Vec3> forward(Runtime& rt, const Hand& hand, const dg::HandConfig& q) {
+  if (static_cast<int>(q.joint_angles.size()) != hand.num_joints())
+    throw std::runtime_error("hand: expected " + std::to_string(hand.num_joints()) + " joint angles, got " +
+                             std::to_string(q.joint_angles.size()));
+  std::vector<double> qv = detail::pack(q), pts(3 * static_cast<std::size_t>(hand.num_samples()));
+  detail::check(dgx_forward_batch(rt.get(), hand.get(), 1, qv.data(), pts.data(), 0));
+  std::vector<dg::Vec3> out(hand.num_samples());
+  for (int i = 0; i < hand.num_samples(); ++i) out[i] = {pts[3 * i], pts[3 * i + 1], pts[3 * i + 2]};
+  return out;
+}
+
+inline std::vector<dg::LossGradient> loss_gradient(Runtime& rt, const Object& obj, const Hand& hand,
+                                                   std::span<const dg::HandConfig> qs,
+                                                   const dg::StabilityProtocol& proto, const dg::SimParams& params) {
+  const int B = static_cast<int>(qs.size()), J = hand.num_joints(), D = 6 + J;
+  std::vector<double> q;
+  for (const auto& c : qs) {
+    if (static_cast<int>(c.joint_angles.size()) != J) throw std::runtime_error("hand: joint angle count mismatch");
+    auto v = detail::pack(c);
+    q.insert(q.end(), v.begin(), v.end());
+  }
+  std::vector<double> losses(3 * static_cast<std::size_t>(B)), grads(3 * static_cast<std::size_t>(B) * D);
+  std::vector<int32_t> status(B);
+  const dgx_params p = detail::params_of(proto, params);
+  detail::check(dgx_loss_gradient_batch(rt.get(), hand.get(), obj.get(), B, q.data(), &p, losses.data(),
+                                        grads.data(), status.data(), 0));
+  std::vector<dg::LossGradient> out(B);
+  for (int b = 0; b < B; ++b) {
+    detail::check_candidate(status[b]);
+    out[b].losses = {losses[3 * b], losses[3 * b + 1], losses[3 * b + 2]};
+    const double* g = grads.data() + static_cast<std::size_t>(b) * 3 * D;
+    out[b].d_stable.assign(g, g + D);
+    out[b].d_qrange.assign(g + D, g + 2 * D);
+    out[b].d_qlimit.assign(g + 2 * D, g + 3 * D);
+  }
+  return out;
+}
+
+inline dg::LossGradient loss_gradient(Runtime& rt, const Object& obj, const Hand& hand, const dg::HandConfig& q,
+                                      const dg::StabilityProtocol& proto, const dg::SimParams& params) {
+  return loss_gradient(rt, obj, hand, std::span<const dg::HandConfig>(&q, 1), proto, params)[0];
+}
+
+inline dg::LossBreakdown evaluate_losses(Runtime& rt, const Object& obj, const Hand& hand, const dg::HandConfig& q,
+                                         const dg::StabilityProtocol& proto, const dg::SimParams& params) {
+  std::vector<double> qv = detail::pack(q), losses(3);
+  int32_t status = 0;
+  const dgx_params p = detail::params_of(proto, params);
+  detail::check(dgx_evaluate_losses_batch(rt.get(), hand.get(), obj.get(), 1, qv.data(), &p, losses.data(),
+                                          nullptr, &status, 0));
+  detail::check_candidate(status);
+  return {losses[0], losses[1], losses[2]};
+}
+
+inline dg::HandConfig apply_gradient_step(Runtime& rt, const Hand& hand, const dg::HandConfig& q,
+                                          const std::vector<double>& grad, double lr) {
+  std::vector<double> qv = detail::pack(q), out(qv.size());
+  detail::check(dgx_apply_gradient_step_batch(rt.get(), hand.get(), 1, qv.data(), grad.data(), lr, out.data(), 0));
+  return detail::unpack(out.data(), hand.num_joints());
+}
+
+// Fused synthesis loop over a batch: returns the final configs.
+struct OptimizeConfig {
+  int iterations = 200;
+  double dilation_start_radius = 0.02, learning_rate = 1e-3, beta1 = 0.9, beta2 = 0.999, eps = 1e-8;
+};
+
+inline std::vector<dg::HandConfig> optimize(Runtime& rt, const Object& obj, const Hand& hand,
+                                            std::span<const dg::HandConfig> init, const dg::StabilityProtocol& proto,
+                                            const dg::SimParams& params, const dg::LossWeights& w,
+                                            const OptimizeConfig& cfg) {
+  const int B = static_cast<int>(init.size()), J = hand.num_joints(), D = 6 + J;
+  std::vector<double> q;
+  for (const auto& c : init) {
+    auto v = detail::pack(c);
+    q.insert(q.end(), v.begin(), v.end());
+  }
+  std::vector<double> m(static_cast<std::size_t>(B) * D, 0.0), v(static_cast<std::size_t>(B) * D, 0.0);
+  std::vector<int32_t> status(B);
+  const dgx_params p = detail::params_of(proto, params, w);
+  const dgx_opt o{cfg.iterations, 0, cfg.iterations, 0, cfg.dilation_start_radius, cfg.learning_rate, cfg.beta1,
+                  cfg.beta2, cfg.eps};
+  detail::check(dgx_optimize_batch(rt.get(), hand.get(), obj.get(), B, q.data(), m.data(), v.data(), &p, &o, nullptr,
+                                   status.data(), 0));
+  std::vector<dg::HandConfig> out;
+  for (int b = 0; b < B; ++b) {
+    detail::check_candidate(status[b]);
+    out.push_back(detail::unpack(q.data() + static_cast<std::size_t>(b) * (7 + J), J));
+  }
+  return out;
+}
+
+}  // namespace dgx

@@ -51,8 +51,8 @@ M_SIMS, GS = 7, 8
 def parse():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=5)
-    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--steps", type=int, default=40)
+    ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="dgx", choices=["dgx", "reference"])
     ap.add_argument("--candidates", type=int, default=CAND_PER_GPU)
     ap.add_argument("--no-cpu-baseline", action="store_true")
@@ -81,31 +81,47 @@ def config_dict(cand: int, n_gpus: int) -> dict:
 
 # ---------------------------------------------------------------------------
 class ClockSampler:
-    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+    """nvidia-smi clocks / throttle reasons, sampled every 100 ms; only samples
+    whose own timestamp falls inside the timed window are summarised."""
 
-    Q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
+    Q = ("timestamp,clocks.sm,clocks.max.sm,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
          "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
          "clocks_event_reasons.sw_power_cap")
 
     def __init__(self, index: int):
         self.index, self.rows, self.proc = index, [], None
+        self.t0 = self.t1 = None
 
-    def __enter__(self):
+    def start(self):
         try:
             self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}",
-                                          "--format=csv,noheader,nounits", "-lms", "200"],
+                                          "--format=csv,noheader,nounits", "-lms", "100"],
                                          stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
             self.t = threading.Thread(target=self._read, daemon=True)
             self.t.start()
+            time.sleep(1.5)  # nvidia-smi start-up
         except OSError:
             self.proc = None
         return self
 
     def _read(self):
+        import datetime
         for line in self.proc.stdout:
-            self.rows.append([c.strip() for c in line.split(",")])
+            c = [x.strip() for x in line.split(",")]
+            try:
+                ts = datetime.datetime.strptime(c[0], "%Y/%m/%d %H:%M:%S.%f").timestamp()
+            except ValueError:
+                continue
+            self.rows.append([ts] + c[1:])
 
-    def __exit__(self, *a):
+    def mark_start(self):
+        self.t0 = time.time()
+
+    def mark_end(self):
+        self.t1 = time.time()
+        time.sleep(0.3)  # let the last in-window sample arrive
+
+    def stop(self):
         if self.proc:
             self.proc.terminate()
             try:
@@ -114,13 +130,18 @@ class ClockSampler:
                 self.proc.kill()
 
     def summary(self) -> dict:
-        sm = [float(r[0]) for r in self.rows if len(r) >= 7 and r[0].replace(".", "").isdigit()]
-        mx = [float(r[1]) for r in self.rows if len(r) >= 7 and r[1].replace(".", "").isdigit()]
+        win = [r for r in self.rows if len(r) >= 8 and self.t0 is not None and self.t0 - 0.05 <= r[0] <= self.t1 + 0.05]
+        def num(x):
+            try:
+                return float(x)
+            except ValueError:
+                return None
+        sm = [num(r[1]) for r in win if num(r[1]) is not None]
+        mx = [num(r[2]) for r in win if num(r[2]) is not None]
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        reasons = sorted({names[i] for r in self.rows if len(r) >= 7 for i in range(4)
-                          if r[3 + i].lower() == "active"})
+        reasons = sorted({names[i] for r in win for i in range(4) if r[4 + i].lower() == "active"})
         return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
-                "reasons": reasons, "samples": len(sm)}
+                "reasons": reasons, "samples": len(sm), "window_s": (self.t1 - self.t0) if self.t0 else None}
 
 
 def traffic_from_profiles():
@@ -190,8 +211,11 @@ def run_dgx(args, rank, world, local_rank):
     if world > 1:
         dist.init_process_group("nccl", device_id=dev)
     hand_d, objs_d, qs = workload(rank, args.candidates)
+    # one multi-object launch per step (dgx_optimize_multi): the two objects'
+    # persistent launches overlap on side streams, so the second fills SMs as
+    # the first drains
     ctx = api.Context(local_rank)
-    stream = torch.cuda.Stream(dev)  # a real stream: the kernels and the timing events share it
+    stream = torch.cuda.Stream(dev)
     torch.cuda.set_stream(stream)
     ctx.set_stream(stream.cuda_stream)
     hand = api.Hand(ctx, hand_d)
@@ -199,22 +223,24 @@ def run_dgx(args, rank, world, local_rank):
     proto, params, weights = api.StabilityProtocol.standard(), api.SimParams(), api.LossWeights()
     opt = api.OptConfig(iterations=ITERS)
     D = 6 + hand_d.num_joints
-    st = [dict(q=torch.tensor(q, device=dev), m=torch.zeros(q.shape[0], D, dtype=torch.float64, device=dev),
-               v=torch.zeros(q.shape[0], D, dtype=torch.float64, device=dev),
-               status=torch.zeros(q.shape[0], dtype=torch.int32, device=dev)) for q in qs]
+    counts = np.array([q.shape[0] for q in qs], np.int32)
+    qall = np.concatenate(qs, axis=0)
+    st = dict(q=torch.tensor(qall, device=dev), m=torch.zeros(qall.shape[0], D, dtype=torch.float64, device=dev),
+              v=torch.zeros(qall.shape[0], D, dtype=torch.float64, device=dev),
+              status=torch.zeros(qall.shape[0], dtype=torch.int32, device=dev))
+    torch.cuda.synchronize()
     flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)
     flags = capi.DGX_DEVICE_PTRS | capi.DGX_ASYNC
 
-    def step(k, evs=None):
-        for oi, o in enumerate(objs):
-            s = st[oi]
-            if evs is not None:
-                evs[oi][0].record(stream)
-            out = api.optimize(ctx, o, hand, s["q"], proto, params, weights, opt, k_begin=k, k_end=k + 1,
-                               adam_m=s["m"], adam_v=s["v"], flags=flags, status=s["status"])
-            if evs is not None:
-                evs[oi][1].record(stream)
+    def step(k, ev=None):
+        if ev is not None:
+            ev[0].record(stream)
+        api.optimize_multi(ctx, objs, hand, st["q"], counts, proto, params, weights, opt, k_begin=k, k_end=k + 1,
+                           adam_m=st["m"], adam_v=st["v"], flags=flags, status=st["status"])
+        if ev is not None:
+            ev[1].record(stream)
 
+    clk = ClockSampler(local_rank).start()
     for w in range(args.warmup):
         step(w)
     torch.cuda.synchronize()
@@ -222,20 +248,22 @@ def run_dgx(args, rank, world, local_rank):
         dist.barrier()
     torch.cuda.synchronize()
     launches0 = ctx.launches
-    launch_ms = []
-    with ClockSampler(local_rank) as clk:
-        for s in range(args.steps):
-            flush.zero_()  # L2 flush, outside the timed events
-            evs = [[torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)] for _ in objs]
-            step(args.warmup + s, evs)
-            torch.cuda.synchronize()
-            launch_ms += [e0.elapsed_time(e1) for e0, e1 in evs]
+    step_ms = []
+    clk.mark_start()
+    for s in range(args.steps):
+        flush.zero_()  # L2 flush, outside the timed events
+        ev = (torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+        step(args.warmup + s, ev)
+        torch.cuda.synchronize()
+        step_ms.append(ev[0].elapsed_time(ev[1]))
     torch.cuda.synchronize()
+    clk.mark_end()
+    clk.stop()
     if world > 1:
         dist.barrier()
     launches = ctx.launches - launches0
-    total_ms = sum(launch_ms)
-    status_bad = int(sum(int(torch.count_nonzero(s["status"])) for s in st))
+    total_ms = sum(step_ms)
+    status_bad = int(torch.count_nonzero(st["status"]))
     t = torch.tensor([total_ms], dtype=torch.float64, device=dev)
     if world > 1:
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
@@ -243,9 +271,8 @@ def run_dgx(args, rank, world, local_rank):
     cand_total = args.candidates * world
     value = cand_total * args.steps / (max_ms * 1e-3)
 
-    # ---- end to end through the public host API (pinned-free numpy path) ----
-    host = [dict(q=st[i]["q"].cpu().numpy(), m=st[i]["m"].cpu().numpy(), v=st[i]["v"].cpu().numpy())
-            for i in range(len(objs))]
+    # ---- end to end through the public host API (numpy in / out, synchronous) ----
+    host = dict(q=st["q"].cpu().numpy(), m=st["m"].cpu().numpy(), v=st["v"].cpu().numpy())
     ctx.set_stream(None)
     k0 = args.warmup + args.steps
     h2d = d2h = 0
@@ -254,14 +281,12 @@ def run_dgx(args, rank, world, local_rank):
         dist.barrier()
     t0 = time.perf_counter()
     for s in range(args.steps):
-        for oi, o in enumerate(objs):
-            h = host[oi]
-            out = api.optimize(ctx, o, hand, h["q"], proto, params, weights, opt, k_begin=k0 + s, k_end=k0 + s + 1,
-                               adam_m=h["m"], adam_v=h["v"], record=True)
-            h.update(q=out["q"], m=out["m"], v=out["v"])
-            nb = h["q"].nbytes + h["m"].nbytes + h["v"].nbytes
-            h2d += nb
-            d2h += nb + out["traj"].nbytes + out["status"].nbytes
+        out = api.optimize_multi(ctx, objs, hand, host["q"], counts, proto, params, weights, opt, k_begin=k0 + s,
+                                 k_end=k0 + s + 1, adam_m=host["m"], adam_v=host["v"], record=True)
+        host.update(q=out["q"], m=out["m"], v=out["v"])
+        nb = host["q"].nbytes + host["m"].nbytes + host["v"].nbytes
+        h2d += nb + out["status"].nbytes
+        d2h += nb + out["traj"].nbytes + out["status"].nbytes
     e2e_s = time.perf_counter() - t0
     t = torch.tensor([e2e_s], dtype=torch.float64, device=dev)
     if world > 1:
@@ -275,9 +300,8 @@ def run_dgx(args, rank, world, local_rank):
         capi.check(L.dgx_fp64_peak(local_rank, C.byref(pk), C.byref(pms)))
         n_pts = hand_d.num_samples
         flop_cand_iter = M_SIMS * GS * n_pts * FLOP_PER_POINT_SWEEP
-        per_launch_cand = args.candidates // len(objs)
-        avg_launch_s = statistics.mean(launch_ms) * 1e-3
-        achieved = flop_cand_iter * per_launch_cand / avg_launch_s / 1e12
+        avg_step_s = statistics.mean(step_ms) * 1e-3
+        achieved = flop_cand_iter * args.candidates / avg_step_s / 1e12
         traffic = traffic_from_profiles()
         result = {
             "metric": "candidate-iterations/sec", "value": value, "unit": "candidate-iterations/s",
@@ -293,7 +317,9 @@ def run_dgx(args, rank, world, local_rank):
                          "frac": achieved / pk.value, "traffic": traffic,
                          "peak_source": "measured DFMA microbenchmark (dgx_fp64_peak, csrc/dgx_peak.cu)",
                          "flop_per_candidate_iteration": flop_cand_iter,
-                         "avg_launch_ms": statistics.mean(launch_ms)},
+                         "timing": "per step: one dgx_optimize_multi call = two concurrent fused launches (one per "
+                                   "object) on side streams; achieved = FLOP_alg x candidates / step time",
+                         "avg_step_ms": statistics.mean(step_ms)},
             "clocks": clk.summary(),
             "failed_candidates": status_bad,
         }

@@ -161,6 +161,14 @@ int dgx_optimize_batch(dgx_ctx* ctx, const dgx_hand* hand, const dgx_object* obj
                        double* adam_m, double* adam_v, const dgx_params* params, const dgx_opt* opt,
                        double* traj, int32_t* status, uint32_t flags);
 
+/* Multi-object batch (BASELINE configs 2/4/5): candidates are object-major,
+   counts[i] of them for objs[i] (q / adam / traj / status rows in that order).
+   Objects are launched concurrently on context-owned side streams (each with
+   its own scratch), forked from and joined back to the context stream. */
+int dgx_optimize_multi(dgx_ctx* ctx, const dgx_hand* hand, int32_t n_obj, const dgx_object* const* objs,
+                       const int32_t* counts, double* q, double* adam_m, double* adam_v, const dgx_params* params,
+                       const dgx_opt* opt, double* traj, int32_t* status, uint32_t flags);
+
 /* Parity / debug: per-perturbation residuals [B,M], gradients [B,M,6+J] and
    optionally d residual_m / d points [B,M,N,3] (pass NULL to skip). */
 int dgx_debug_sims(dgx_ctx* ctx, const dgx_hand* hand, const dgx_object* obj, int32_t B, const double* q,

@@ -268,3 +268,41 @@ def optimize(ctx: Context, obj: GraspObject, hand: Hand, q, protocol: StabilityP
     capi.check(ctx.L.dgx_optimize_batch(ctx.h, hand.h, obj.h, B, capi.ptr(q), capi.ptr(adam_m), capi.ptr(adam_v),
                                         C.byref(p), C.byref(o), capi.ptr(traj), capi.ptr(status), fl))
     return dict(q=q, m=adam_m, v=adam_v, status=status, traj=traj)
+
+
+def optimize_multi(ctx: Context, objs: list, hand: Hand, q, counts, protocol: StabilityProtocol,
+                   params: SimParams, weights: LossWeights, opt: OptConfig, k_begin: int = 0,
+                   k_end: int | None = None, adam_m=None, adam_v=None, record: bool = False, flags: int | None = None,
+                   status=None):
+    """Multi-object fused synthesis (dgx_optimize_multi): candidates object-major,
+    counts[i] for objs[i]; objects run concurrently on side streams."""
+    k_end = opt.iterations if k_end is None else k_end
+    D = 6 + hand.J
+    counts = np.ascontiguousarray(counts, np.int32)
+    host = isinstance(q, np.ndarray) or not hasattr(q, "data_ptr")
+    if host:
+        q = np.array(q, np.float64, copy=True, order="C").reshape(-1, 7 + hand.J)
+        B = q.shape[0]
+        adam_m = np.zeros((B, D)) if adam_m is None else np.array(adam_m, np.float64, copy=True, order="C")
+        adam_v = np.zeros((B, D)) if adam_v is None else np.array(adam_v, np.float64, copy=True, order="C")
+        status = np.zeros(B, np.int32) if status is None else status
+        traj = np.zeros((B, k_end - k_begin, 3 + D)) if record else None
+    else:
+        import torch
+        B = q.shape[0]
+        dev = q.device
+        adam_m = torch.zeros((B, D), dtype=torch.float64, device=dev) if adam_m is None else adam_m
+        adam_v = torch.zeros((B, D), dtype=torch.float64, device=dev) if adam_v is None else adam_v
+        status = torch.zeros(B, dtype=torch.int32, device=dev) if status is None else status
+        traj = torch.zeros((B, k_end - k_begin, 3 + D), dtype=torch.float64, device=dev) if record else None
+    if int(counts.sum()) != B:
+        raise ValueError("sum(counts) must equal the number of candidates")
+    handles = (C.c_void_p * len(objs))(*[o.h.value for o in objs])
+    p = params_c(params, protocol, weights)
+    o = capi.OptC(opt.iterations, k_begin, k_end, int(record), opt.dilation_start_radius, opt.learning_rate,
+                  opt.beta1, opt.beta2, opt.eps)
+    fl = _flags(q, adam_m, adam_v, status, traj) if flags is None else flags
+    capi.check(ctx.L.dgx_optimize_multi(ctx.h, hand.h, len(objs), handles, capi.ptr(counts), capi.ptr(q),
+                                        capi.ptr(adam_m), capi.ptr(adam_v), C.byref(p), C.byref(o), capi.ptr(traj),
+                                        capi.ptr(status), fl))
+    return dict(q=q, m=adam_m, v=adam_v, status=status, traj=traj)

@@ -71,7 +71,7 @@ EXPORTS = [
     "dgx_ctx_set_correction_capacity", "dgx_ctx_launch_count", "dgx_hand_upload", "dgx_hand_free",
     "dgx_object_upload", "dgx_object_free", "dgx_forward_batch", "dgx_loss_gradient_batch",
     "dgx_evaluate_losses_batch", "dgx_apply_gradient_step_batch", "dgx_optimize_batch", "dgx_debug_sims",
-    "dgx_fp64_peak",
+    "dgx_fp64_peak", "dgx_optimize_multi",
 ]
 
 _lib: C.CDLL | None = None
@@ -112,6 +112,8 @@ def load() -> C.CDLL:
                                      vp, C.c_uint32]
     L.dgx_debug_sims.argtypes = [vp, vp, vp, C.c_int32, vp, C.POINTER(ParamsC), vp, vp, vp, vp, C.c_uint32]
     L.dgx_fp64_peak.argtypes = [C.c_int, _dp, _dp]
+    L.dgx_optimize_multi.argtypes = [vp, vp, C.c_int32, vp, vp, vp, vp, vp, C.POINTER(ParamsC), C.POINTER(OptC), vp,
+                                     vp, C.c_uint32]
     _lib = L
     return L
 

@@ -1,6 +1,8 @@
 // dgx_capi.cu — implementation of include/dgx.h over the sm_100a kernels.
 #include <cuda_runtime.h>
 
+#include <algorithm>
+#include <climits>
 #include <cmath>
 #include <cstdio>
 #include <cstring>
@@ -60,14 +62,34 @@ struct DevBuf {
 
 }  // namespace
 
+// per-stream kernel scratch (correction logs, contact slots, link-sum spills)
+struct Scratch {
+  DevBuf corr, slots, ftg;
+  void release() {
+    corr.release();
+    slots.release();
+    ftg.release();
+  }
+};
+
+// a side stream with its own scratch, for concurrent per-object launches
+struct SubStream {
+  cudaStream_t stream = nullptr;
+  cudaEvent_t done = nullptr;
+  Scratch scratch;
+};
+
 struct dgx_ctx {
   int device = 0;
   int num_sms = 0;
   cudaStream_t own = nullptr;
   cudaStream_t stream = nullptr;
+  cudaEvent_t fork = nullptr;
   int cap_corr = 1024;
   int64_t launches = 0;
-  DevBuf corr, slots, io, ftg;
+  Scratch scratch;
+  DevBuf io;
+  std::vector<SubStream> subs;
 };
 
 struct dgx_hand {
@@ -118,10 +140,20 @@ KSim make_sim(const dgx_params* p, bool eval) {
 }
 
 // grid of persistent CTAs and the scratch it needs
-int prepare(dgx_ctx* c, const dgx_hand* h, const dgx_object* o, int M, int B, KBuf& buf, int& smem) {
-  smem = SmemLayout(h->N, h->L, M).total;
-  if (smem > 227 * 1024)
+int prepare(dgx_ctx* c, Scratch& sc, const dgx_hand* h, const dgx_object* o, KSim& S, int B, KBuf& buf,
+            int& smem) {
+  const int M = S.M;
+  // longest adjoint segment whose staging still fits one CTA's shared memory
+  S.seg_max = 0;
+  for (int seg : {kSegMaxCap, 8, 4, 2, 1}) {
+    if (SmemLayout(h->N, h->L, M, seg).total <= 227 * 1024) {
+      S.seg_max = seg;
+      break;
+    }
+  }
+  if (S.seg_max == 0)
     throw DgxError(DGX_E_UNSUPPORTED, "hand too large for one CTA's shared memory (N=" + std::to_string(h->N) + ")");
+  smem = SmemLayout(h->N, h->L, M, S.seg_max).total;
   int per_sm = 0;
   cuda_check(fused_occupancy(o->kind, M, smem, &per_sm), "occupancy");
   if (per_sm < 1) throw DgxError(DGX_E_UNSUPPORTED, "fused kernel cannot be resident (registers/smem)");
@@ -129,15 +161,15 @@ int prepare(dgx_ctx* c, const dgx_hand* h, const dgx_object* o, int M, int B, KB
   if (grid > B) grid = B;
   if (grid < 1) grid = 1;
   const size_t nws = static_cast<size_t>(grid) * M;
-  c->corr.ensure(nws * c->cap_corr * sizeof(CorrRec));
+  sc.corr.ensure(nws * c->cap_corr * sizeof(CorrRec));
   const size_t per = nws * static_cast<size_t>(h->N);
-  c->slots.ensure(per * (sizeof(SlotRec) + 2 * sizeof(int)));
-  buf.corr = static_cast<CorrRec*>(c->corr.p);
-  buf.slots = static_cast<SlotRec*>(c->slots.p);
+  sc.slots.ensure(per * (sizeof(SlotRec) + 2 * sizeof(int)));
+  buf.corr = static_cast<CorrRec*>(sc.corr.p);
+  buf.slots = static_cast<SlotRec*>(sc.slots.p);
   buf.slot_of_point = reinterpret_cast<int*>(buf.slots + per);
   buf.fric_order = buf.slot_of_point + per;
-  c->ftg.ensure(nws * 6 * static_cast<size_t>(h->L) * sizeof(double));
-  buf.ft_global = static_cast<double*>(c->ftg.p);
+  sc.ftg.ensure(nws * 6 * static_cast<size_t>(h->L) * sizeof(double));
+  buf.ft_global = static_cast<double*>(sc.ftg.p);
   buf.cap_corr = c->cap_corr;
   buf.B = B;
   return grid;
@@ -198,6 +230,7 @@ int dgx_ctx_create(int device, dgx_ctx** out) {
       c->num_sms = prop.multiProcessorCount;
       cuda_check(cudaStreamCreateWithFlags(&c->own, cudaStreamNonBlocking), "cudaStreamCreate");
       c->stream = c->own;
+      cuda_check(cudaEventCreateWithFlags(&c->fork, cudaEventDisableTiming), "cudaEventCreate");
     } catch (...) {
       delete c;
       throw;
@@ -210,10 +243,14 @@ int dgx_ctx_destroy(dgx_ctx* c) {
   return guarded([&] {
     if (!c) return;
     cudaSetDevice(c->device);
-    c->corr.release();
-    c->slots.release();
-    c->ftg.release();
+    c->scratch.release();
     c->io.release();
+    for (auto& sub : c->subs) {
+      sub.scratch.release();
+      if (sub.done) cudaEventDestroy(sub.done);
+      if (sub.stream) cudaStreamDestroy(sub.stream);
+    }
+    if (c->fork) cudaEventDestroy(c->fork);
     if (c->own) cudaStreamDestroy(c->own);
     delete c;
   });
@@ -380,7 +417,7 @@ int dgx_forward_batch(dgx_ctx* c, const dgx_hand* h, int32_t B, const double* q,
 }
 
 static void run_fused(dgx_ctx* c, const dgx_hand* h, const dgx_object* o, int32_t B, const double* q,
-                      double* qio, double* am, double* av, const KSim& S, const KOpt& P, int mode, double* losses,
+                      double* qio, double* am, double* av, KSim S, const KOpt& P, int mode, double* losses,
                       double* grads, double* stats, double* sim_res, double* sim_grads, double* point_grads,
                       double* traj, int32_t* status, uint32_t flags) {
   if (!c || !h || !o) throw DgxError(DGX_E_INVALID, "NULL handle");
@@ -414,7 +451,7 @@ static void run_fused(dgx_ctx* c, const dgx_hand* h, const dgx_object* o, int32_
   buf.status = s.out(status, static_cast<size_t>(B));
   if (point_grads) cuda_check(cudaMemsetAsync(buf.point_grads, 0, 24ull * B * M * N, c->stream), "memset");
   int smem = 0;
-  int grid = prepare(c, h, o, M, B, buf, smem);
+  int grid = prepare(c, c->scratch, h, o, S, B, buf, smem);
   cuda_check(launch_fused(h->k, o->k, o->kind, o->sphere, o->box, o->grid, S, P, buf, mode, grid, smem, c->stream),
              "fused_kernel");
   ++c->launches;
@@ -464,6 +501,73 @@ int dgx_optimize_batch(dgx_ctx* c, const dgx_hand* h, const dgx_object* o, int32
     KOpt P{opt->iters, opt->k_begin, opt->k_end, opt->record, opt->r0, opt->lr, opt->beta1, opt->beta2, opt->eps};
     run_fused(c, h, o, B, nullptr, q, am, av, S, P, kModeOpt, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr,
               opt->record ? traj : nullptr, status, flags);
+  });
+}
+
+int dgx_optimize_multi(dgx_ctx* c, const dgx_hand* h, int32_t n_obj, const dgx_object* const* objs,
+                       const int32_t* counts, double* q, double* am, double* av, const dgx_params* p,
+                       const dgx_opt* opt, double* traj, int32_t* status, uint32_t flags) {
+  return guarded([&] {
+    if (!c || !h || !objs || !counts || !opt || !status) throw DgxError(DGX_E_INVALID, "NULL argument");
+    if (n_obj < 0) throw DgxError(DGX_E_INVALID, "n_obj < 0");
+    if (opt->iters < 1 || opt->k_begin < 0 || opt->k_end < opt->k_begin || opt->k_end > opt->iters)
+      throw DgxError(DGX_E_INVALID, "opt: need 0 <= k_begin <= k_end <= iters, iters >= 1");
+    if (!(opt->lr > 0.0)) throw DgxError(DGX_E_INVALID, "opt: learning rate must be > 0");
+    int64_t B64 = 0;
+    for (int i = 0; i < n_obj; ++i) {
+      if (!objs[i] || counts[i] < 0) throw DgxError(DGX_E_INVALID, "bad object / count");
+      B64 += counts[i];
+    }
+    if (B64 == 0) return;
+    if (B64 > INT32_MAX) throw DgxError(DGX_E_INVALID, "too many candidates");
+    const int B = static_cast<int>(B64);
+    set_device(c);
+    KSim S0 = make_sim(p, false);
+    KOpt P{opt->iters, opt->k_begin, opt->k_end, opt->record, opt->r0, opt->lr, opt->beta1, opt->beta2, opt->eps};
+    const bool dev = flags & DGX_DEVICE_PTRS;
+    const int D = 6 + h->J, Qd = 7 + h->J, steps = opt->k_end - opt->k_begin;
+    Staging st(c, dev, bytes_round(8ull * B * Qd) + 2 * bytes_round(8ull * B * D) + bytes_round(4ull * B) +
+                           (opt->record && traj ? bytes_round(8ull * B * steps * (3 + D)) : 0));
+    double* dq = st.out(q, static_cast<size_t>(B) * Qd, true);
+    double* dm = st.out(am, static_cast<size_t>(B) * D, true);
+    double* dv = st.out(av, static_cast<size_t>(B) * D, true);
+    double* dt = st.out(opt->record ? traj : nullptr, static_cast<size_t>(B) * steps * (3 + D));
+    int32_t* ds = st.out(status, static_cast<size_t>(B));
+    // fork onto the side streams (object i -> stream i % P), each with its own scratch
+    const int P_streams = std::min<int>(n_obj, 4);
+    while (static_cast<int>(c->subs.size()) < P_streams) {
+      SubStream sub;
+      cuda_check(cudaStreamCreateWithFlags(&sub.stream, cudaStreamNonBlocking), "cudaStreamCreate");
+      cuda_check(cudaEventCreateWithFlags(&sub.done, cudaEventDisableTiming), "cudaEventCreate");
+      c->subs.push_back(sub);
+    }
+    cuda_check(cudaEventRecord(c->fork, c->stream), "cudaEventRecord");
+    for (int k = 0; k < P_streams; ++k) cuda_check(cudaStreamWaitEvent(c->subs[k].stream, c->fork, 0), "wait");
+    size_t off = 0;
+    for (int i = 0; i < n_obj; ++i) {
+      const int Bi = counts[i];
+      if (Bi == 0) continue;
+      SubStream& sub = c->subs[i % P_streams];
+      KSim S = S0;
+      KBuf buf{};
+      buf.q = dq + off * Qd;
+      buf.adam_m = dm + off * D;
+      buf.adam_v = dv + off * D;
+      buf.traj = dt ? dt + off * steps * (3 + D) : nullptr;
+      buf.status = ds + off;
+      int smem = 0;
+      const int grid = prepare(c, sub.scratch, h, objs[i], S, Bi, buf, smem);
+      cuda_check(launch_fused(h->k, objs[i]->k, objs[i]->kind, objs[i]->sphere, objs[i]->box, objs[i]->grid, S, P,
+                              buf, kModeOpt, grid, smem, sub.stream),
+                 "fused_kernel");
+      ++c->launches;
+      off += Bi;
+    }
+    for (int k = 0; k < P_streams; ++k) {
+      cuda_check(cudaEventRecord(c->subs[k].done, c->subs[k].stream), "cudaEventRecord");
+      cuda_check(cudaStreamWaitEvent(c->stream, c->subs[k].done, 0), "wait");
+    }
+    st.finish(flags);
   });
 }
 

@@ -8,7 +8,7 @@ namespace dgx {
 
 constexpr int kMaxSims = 8;        // protocol velocities per candidate (standard: 7)
 constexpr int kMaxDim = 32;        // 6 + J gradient coordinates (J <= 26)
-constexpr int kStageDoubles = 640; // per-warp staging (adjoint segment: 4 slots x 5 x 32 lanes)
+constexpr int kSegMaxCap = 16;    // max points per lane segment in the adjoint
 
 enum Mode : int { kModeGrad = 0, kModeEval = 1, kModeOpt = 2 };
 
@@ -82,7 +82,7 @@ struct KObj {
 
 struct KSim {
   double dt, mu, alpha, radius;
-  int gs, M, measure_residual, pad;
+  int gs, M, measure_residual, seg_max;
   double vel[kMaxSims][3];
   double w_stable, w_qrange, w_qlimit;
 };
@@ -117,7 +117,13 @@ struct KBuf {
 struct SmemLayout {
   int off_px, off_py, off_pz, off_link, off_ft, off_bitmap, off_stage, off_misc, total;
   __host__ __device__ static int align(int x) { return (x + 15) & ~15; }
-  __host__ __device__ SmemLayout(int N, int L, int M) {
+  int stage_per_warp;  // doubles: seg_max x 5 x 32 adjoint staging (>= 6L for the debug FK adjoint)
+  __host__ __device__ static int stage_doubles(int seg_max, int L) {
+    const int a = seg_max * 5 * 32, b = 6 * L;
+    return a > b ? a : b;
+  }
+  __host__ __device__ SmemLayout(int N, int L, int M, int seg_max) {
+    stage_per_warp = stage_doubles(seg_max, L);
     int o = 0;
     off_px = o; o = align(o + 8 * N);
     off_py = o; o = align(o + 8 * N);
@@ -125,7 +131,7 @@ struct SmemLayout {
     off_link = o; o = align(o + 8 * 12 * L);
     off_ft = o; o = align(o + 8 * 6 * L * M);
     off_bitmap = o; o = align(o + 4 * ((N + 31) / 32) * M);
-    off_stage = o; o = align(o + 8 * kStageDoubles * M);
+    off_stage = o; o = align(o + 8 * stage_per_warp * M);
     off_misc = o; o = align(o + 8 * (64 + 4 * kMaxDim + 2 * kMaxSims));
     total = o;
   }

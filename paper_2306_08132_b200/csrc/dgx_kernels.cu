@@ -69,7 +69,7 @@ __device__ __forceinline__ double warp_max(double v) {
 }
 
 struct SimEnv {
-  int lane, N, gs;
+  int lane, N, gs, seg_max;
   const double *px, *py, *pz;
   const int* sample_link;
   unsigned* bitmap;
@@ -363,7 +363,6 @@ __device__ __forceinline__ bool leak_coef(const SimEnv& e, const LeakGeo& L, V3 
   return true;
 }
 
-constexpr int kSeg = 4;  // points per lane segment in the adjoint (block = 128 point-sweeps)
 // per (segment slot, lane): c1, c0, g.x, g.y, g.z staged in shared memory by pass 1
 __device__ __forceinline__ int stg_idx(int k, int c, int lane) { return (k * 5 + c) * 32 + lane; }
 
@@ -383,9 +382,12 @@ __device__ void process_run(const Sdf& sdf, SimEnv& e, int lo, int hi, V3 xk, Q4
              -qk.z * aQ.w - qk.y * aQ.x + qk.x * aQ.y + qk.w * aQ.z};
   const V3 G = ftmul(e.O->Iw, H);
   V3 X = aX;
-  for (int top = hi; top > lo; top -= 32 * kSeg) {
-    const int shi = top - lane * kSeg;
-    const int slo = max(top - (lane + 1) * kSeg, lo);
+  for (int top = hi; top > lo;) {
+    // segment length adapts to the run: short runs keep all lanes busy, long
+    // runs amortise the scan over up to seg_max points per lane
+    const int S = min(e.seg_max, (top - lo + 31) / 32);
+    const int shi = top - lane * S;
+    const int slo = max(top - (lane + 1) * S, lo);
     const int cnt = shi - slo;
     PROF_CNT(18, 1);
     PROF_T(t1a);
@@ -532,6 +534,7 @@ __device__ void process_run(const Sdf& sdf, SimEnv& e, int lo, int hi, V3 xk, Q4
       if (--i < 0) i = N - 1;
     }
     X = Xnext;
+    top -= 32 * S;
     __syncwarp();
     PROF_ACC(9, t3);
   }
@@ -1041,7 +1044,7 @@ __device__ __forceinline__ void fk_adjoint(const KHand& H, const double* qv, con
 template <class Sdf>
 __global__ void __launch_bounds__(224, 1) fused_kernel(KHand H, const __grid_constant__ KObj O, Sdf sdf, KSim S, KOpt P, KBuf buf, int mode) {
   extern __shared__ __align__(16) unsigned char smem[];
-  const SmemLayout lay(H.N, H.L, S.M);
+  const SmemLayout lay(H.N, H.L, S.M, S.seg_max);
   double* px = reinterpret_cast<double*>(smem + lay.off_px);
   double* py = reinterpret_cast<double*>(smem + lay.off_py);
   double* pz = reinterpret_cast<double*>(smem + lay.off_pz);
@@ -1068,7 +1071,8 @@ __global__ void __launch_bounds__(224, 1) fused_kernel(KHand H, const __grid_con
   e.sample_link = H.sample_link;
   e.bitmap = bitmap_all + warp * nwords;
 
-  e.stage = stage_all + warp * kStageDoubles;
+  e.stage = stage_all + warp * lay.stage_per_warp;
+  e.seg_max = S.seg_max;
   e.ft = ft_all + warp * 6 * L;
   const size_t wslot = static_cast<size_t>(blockIdx.x) * M + (warp < M ? warp : 0);
   e.corr = buf.corr + wslot * buf.cap_corr;

@@ -85,3 +85,28 @@ def test_distribution_parity_full_runs(ctx, oracle):
     # (individual trajectories are NOT compared: the first rounding-decided
     # re-activation after a 1-ulp difference in q sends each run its own way;
     # per-step agreement is covered by test_teacher_forced_optimizer)
+
+
+def test_multi_object_launch_matches_per_object(ctx):
+    """dgx_optimize_multi (objects on concurrent side streams) == one optimize per object, bitwise."""
+    from paper_2306_08132_b200 import api, init, model
+    hd = model.HandDesc.asset("allegro16")
+    ods = [model.box_grid(res=64), model.cylinder_grid(res=32), model.sphere(0.03)]
+    hand = api.Hand(ctx, hd)
+    objs = [api.GraspObject(ctx, o) for o in ods]
+    counts = [40, 0, 25]
+    qs = [init.approach_init(o, hd, n, seed=5 + i) for i, (o, n) in enumerate(zip(ods, counts))]
+    q = np.concatenate(qs, axis=0)
+    proto, w, opt = api.StabilityProtocol.standard(), api.LossWeights(), api.OptConfig(iterations=50)
+    multi = api.optimize_multi(ctx, objs, hand, q, counts, proto, api.SimParams(), w, opt, k_begin=0, k_end=3,
+                               record=True)
+    assert not np.any(multi["status"])
+    off = 0
+    for o, n, qi in zip(objs, counts, qs):
+        if n == 0:
+            continue
+        one = api.optimize(ctx, o, hand, qi, proto, api.SimParams(), w, opt, k_begin=0, k_end=3, record=True)
+        assert np.array_equal(one["q"], multi["q"][off:off + n])
+        assert np.array_equal(one["m"], multi["m"][off:off + n])
+        assert np.array_equal(one["traj"], multi["traj"][off:off + n])
+        off += n

@@ -373,7 +373,12 @@ __device__ __forceinline__ int stg_idx(int k, int c, int lane) { return (k * 5 +
 // pass 3 re-walks with it and emits the point / R adjoints.
 template <class Sdf>
 __device__ void process_run(const Sdf& sdf, SimEnv& e, int lo, int hi, V3 xk, Q4 qk, const M3& Rk, Q4 aQ, V3& aX,
-                            M3& aR, FtAcc& acc) {
+                            M3& aR, FtAcc& acc, double c0scale = 1.0, M3* map_out = nullptr,
+                            V3* off_out = nullptr) {
+  // map_out != nullptr: map-only mode. No contributions are emitted; the
+  // run's composed affine map on adj_x (a -> M a + b) is returned instead.
+  // c0scale multiplies the constant (theta-channel) term of every point, so a
+  // run fed with sum_k X_k and c0scale = K emits the sum over K identical runs.
   const int lane = e.lane, N = e.N;
   double* stg = e.stage;
   // H . k == ([0,k] (x) q_k) . aQ ; G = Iw^T H  (theta-axpy coefficient)
@@ -382,6 +387,9 @@ __device__ void process_run(const Sdf& sdf, SimEnv& e, int lo, int hi, V3 xk, Q4
              -qk.z * aQ.w - qk.y * aQ.x + qk.x * aQ.y + qk.w * aQ.z};
   const V3 G = ftmul(e.O->Iw, H);
   V3 X = aX;
+  M3 Mtot;
+  V3 btot{0.0, 0.0, 0.0};
+  for (int t = 0; t < 9; ++t) Mtot.m[t] = (t % 4 == 0) ? 1.0 : 0.0;
   for (int top = hi; top > lo;) {
     // segment length adapts to the run: short runs keep all lanes busy, long
     // runs amortise the scan over up to seg_max points per lane
@@ -452,6 +460,7 @@ __device__ void process_run(const Sdf& sdf, SimEnv& e, int lo, int hi, V3 xk, Q4
         c1 = 0.0;
         c0 = 0.0;
       }
+      c0 *= c0scale;
       stg[stg_idx(k, 0, lane)] = c1;
       stg[stg_idx(k, 1, lane)] = c0;
       stg[stg_idx(k, 2, lane)] = L.n.x;
@@ -514,6 +523,18 @@ __device__ void process_run(const Sdf& sdf, SimEnv& e, int lo, int hi, V3 xk, Q4
     const V3 Xnext = fmul(Ml, X) + bl;
     __syncwarp();
     PROF_ACC(8, t2);
+    if (map_out) {  // map-only: compose this block's map after the previous ones
+      btot = fmul(Ml, btot) + bl;
+      M3 P;
+      for (int r = 0; r < 3; ++r)
+        for (int c = 0; c < 3; ++c)
+          P.m[3 * r + c] = fma(Ml.m[3 * r + 2], Mtot.m[6 + c], fma(Ml.m[3 * r + 1], Mtot.m[3 + c], Ml.m[3 * r] * Mtot.m[c]));
+      Mtot = P;
+      X = Xnext;
+      top -= 32 * S;
+      __syncwarp();
+      continue;
+    }
     PROF_T(t3);
     // ---- pass 3: re-walk with the incoming adjoint, emit contributions
     i = cnt > 0 ? (shi - 1) % N : 0;
@@ -539,6 +560,10 @@ __device__ void process_run(const Sdf& sdf, SimEnv& e, int lo, int hi, V3 xk, Q4
     PROF_ACC(9, t3);
   }
   aX = X;
+  if (map_out) {
+    *map_out = Mtot;
+    *off_out = btot;
+  }
 }
 
 struct CorrIn {
@@ -751,7 +776,15 @@ __device__ double run_sim(const Sdf& sdf, SimEnv& e, V3 v_m, bool record, bool m
   // change no forward value (sim.hpp:105-125), so this is the sequential sweep.
   int ncorr = 0, nslot = 0;
   int pos = 0, sweep = 0;
+  // Quiet window: once N consecutive positions pass with no applied
+  // correction (and no singular skip, to keep SolveStats exact), every later
+  // position repeats an earlier inactive decision under the same state: the
+  // remaining sweeps are skipped (and the adjoint folds them, run_sim below).
+  int f_last = -1, singular_since = 0;
   while (sweep < e.gs) {
+#ifdef DGX_QUIET  // exact, but measured slower under the CTA barrier
+    if (sweep * N + pos - f_last - 1 >= N && singular_since == 0) break;
+#endif
     int cls[2];
 #pragma unroll
     for (int h = 0; h < 2; ++h) {
@@ -813,12 +846,15 @@ __device__ double run_sim(const Sdf& sdf, SimEnv& e, V3 v_m, bool record, bool m
       q = co.q;
       R = rotation_matrix(q);
       touched = true;
+      f_last = sweep * N + ij;
+      singular_since = 0;
       ++ncorr;
       nslot = co.nslot;
       ++st.corrections;
       st.active += co.new_contact;
     } else {
       ++st.singular;
+      ++singular_since;
     }
     pos = ij + 1;
     if (pos >= N) { pos = 0; ++sweep; }
@@ -925,26 +961,86 @@ __device__ double run_sim(const Sdf& sdf, SimEnv& e, V3 v_m, bool record, bool m
   // ---- sweeps, reverse ----------------------------------------------------
   M3 aR;  // per-lane partial adjoint of the current R node
   for (int k = 0; k < 9; ++k) aR.m[k] = 0.0;
+  // Reverse sweep as a state machine with ONE process_run call site (keeps
+  // the i-cache footprint of the inlined adjoint small):
+  //   stage 0/1/2 fold the final run [lo_f, hi): the last correction is
+  //     followed by K >= 2 identical cycles of the same N point-sweeps with the
+  //     same state (plus a partial head of r positions). Stage 0 processes the
+  //     head; stage 1 runs ONE cycle in map-only mode (its affine map
+  //     a -> M a + b on adj_x); the adjoint is iterated K times through it;
+  //     stage 2 runs one emission pass fed sum_k X_k with c0 scaled by K, which
+  //     emits all K cycles by linearity.
+  //   stage 3 walks the remaining runs and logged corrections in reverse.
   int hi = e.gs * N;
-  for (int k = ncorr - 1;; --k) {
-    // state of the run after correction k (predicted state for k < 0)
+  const int lo_f = ncorr > 0 ? e.corr[ncorr - 1].f + 1 : 0;
+  const int Kc = (hi - lo_f) / N;
+  const int rhead = (hi - lo_f) - Kc * N;
+#ifdef DGX_QUIET
+  int stage = Kc >= 2 ? 0 : 3;
+#else
+  int stage = 3;
+#endif
+  int k = ncorr - 1;
+  V3 Xk_fold{0.0, 0.0, 0.0};
+  M3 Mc;
+  V3 bc{0.0, 0.0, 0.0};
+  for (;;) {
+    const int kstate = stage < 3 ? ncorr - 1 : k;  // state after correction kstate
     V3 xk = pred_x;
     Q4 qk = pred_q;
-    if (k >= 0) {
-      const CorrRec& c = e.corr[k];
+    if (kstate >= 0) {
+      const CorrRec& c = e.corr[kstate];
       xk = V3{c.x[0], c.x[1], c.x[2]};
       qk = Q4{c.q[0], c.q[1], c.q[2], c.q[3]};
     }
     const M3 Rk = rotation_matrix(qk);
-    const int lo = k >= 0 ? e.corr[k].f + 1 : 0;
+    int lo = 0, hr = 0;
+    double scale = 1.0;
+    bool mapm = false;
+    if (stage == 0) {
+      lo = hi - rhead;
+      hr = hi;
+    } else if (stage == 1 || stage == 2) {
+      lo = lo_f;
+      hr = lo_f + N;
+      mapm = stage == 1;
+      scale = stage == 2 ? static_cast<double>(Kc) : 1.0;
+    } else {
+      lo = k >= 0 ? e.corr[k].f + 1 : 0;
+      hr = hi;
+    }
+    V3 aXrun = aX;
     PROF_T(tpr);
-    process_run(sdf, e, lo, hi, xk, qk, Rk, aQ, aX, aR, acc);
+    process_run(sdf, e, lo, hr, xk, qk, Rk, aQ, aXrun, aR, acc, scale, mapm ? &Mc : nullptr, mapm ? &bc : nullptr);
     PROF_ACC(5, tpr);
     PROF_CNT(19, 1);
+    if (stage == 0) {
+      aX = aXrun;
+      stage = 1;
+      continue;
+    }
+    if (stage == 1) {
+      V3 Y{0.0, 0.0, 0.0};
+      Xk_fold = aX;
+      for (int j = 0; j < Kc; ++j) {
+        Y = Y + Xk_fold;
+        Xk_fold = fmul(Mc, Xk_fold) + bc;
+      }
+      aX = Y;  // input of the emission pass
+      stage = 2;
+      continue;
+    }
+    if (stage == 2) {
+      aX = Xk_fold;  // adjoint entering the final run from below
+      hi = lo_f;
+      stage = 3;
+      continue;
+    }
+    aX = aXrun;
     if (k < 0) break;
 
-    PROF_T(tca);
     // ---- active correction k (sim.hpp:215-245), reverse ----
+    PROF_T(tca);
     const M3 aRk = warp_sum(aR);
     aQ = qadd(aQ, rotmat_adj(qk, aRk));
     for (int t = 0; t < 9; ++t) aR.m[t] = 0.0;
@@ -954,8 +1050,8 @@ __device__ double run_sim(const Sdf& sdf, SimEnv& e, V3 v_m, bool record, bool m
     aX = ca.aX;
     aQ = ca.aQ;
     PROF_ACC(11, tca);
-    const CorrRec& c = e.corr[k];
-    hi = c.f;
+    hi = e.corr[k].f;
+    --k;
   }
   // fold the global spill buffer into the warp's shared link sums
   PROF_T(tf);

@@ -40,29 +40,37 @@ def _grid_phi(o: ObjectDesc, p: np.ndarray) -> np.ndarray:
     return c0 + (c1 - c0) * tz
 
 
-def surface_point(o: ObjectDesc, d: np.ndarray) -> tuple[np.ndarray, np.ndarray]:
-    """(p_s, outward unit normal) along the ray com + t d."""
+def surface_points(o: ObjectDesc, d: np.ndarray) -> tuple[np.ndarray, np.ndarray]:
+    """(p_s [B,3], outward unit normal [B,3]) along the rays com + t d (vectorised)."""
+    d = np.atleast_2d(d)
     if o.kind == "sphere":
-        return o.center + o.radius * d, d.copy()
+        return o.center[None, :] + o.radius * d, d.copy()
     if o.kind == "box":
         with np.errstate(divide="ignore"):
-            ts = np.where(np.abs(d) > 0, o.half_extents / np.abs(d), np.inf)
-        k = int(np.argmin(ts))
-        n = np.zeros(3)
-        n[k] = np.sign(d[k])
-        return o.center + ts[k] * d, n
-    lo, hi = 0.0, float(np.max(o.spacing * (np.array(o.dims) - 1)))
+            ts = np.where(np.abs(d) > 0, o.half_extents[None, :] / np.abs(d), np.inf)
+        k = np.argmin(ts, axis=1)
+        t = ts[np.arange(d.shape[0]), k]
+        n = np.zeros_like(d)
+        n[np.arange(d.shape[0]), k] = np.sign(d[np.arange(d.shape[0]), k])
+        return o.center[None, :] + t[:, None] * d, n
+    lo = np.zeros(d.shape[0])
+    hi = np.full(d.shape[0], float(np.max(o.spacing * (np.array(o.dims) - 1))))
     for _ in range(60):  # bisection on phi(com + t d) = 0
         mid = 0.5 * (lo + hi)
-        if _grid_phi(o, o.com + mid * d) < 0.0:
-            lo = mid
-        else:
-            hi = mid
-    p = o.com + 0.5 * (lo + hi) * d
+        inside = _grid_phi(o, o.com[None, :] + mid[:, None] * d) < 0.0
+        lo = np.where(inside, mid, lo)
+        hi = np.where(inside, hi, mid)
+    p = o.com[None, :] + (0.5 * (lo + hi))[:, None] * d
     h = 0.5 * o.spacing
-    g = np.array([(_grid_phi(o, p + h * e) - _grid_phi(o, p - h * e)) for e in np.eye(3)])
-    n = g / np.linalg.norm(g) if np.linalg.norm(g) > 0 else d.copy()
+    g = np.stack([_grid_phi(o, p + h * e) - _grid_phi(o, p - h * e) for e in np.eye(3)], axis=1)
+    gn = np.linalg.norm(g, axis=1, keepdims=True)
+    n = np.where(gn > 0, g / np.where(gn > 0, gn, 1.0), d)
     return p, n
+
+
+def surface_point(o: ObjectDesc, d: np.ndarray) -> tuple[np.ndarray, np.ndarray]:
+    p, n = surface_points(o, np.asarray(d, np.float64)[None, :])
+    return p[0], n[0]
 
 
 def _quat_from_matrix(R: np.ndarray) -> np.ndarray:
@@ -81,23 +89,28 @@ def approach_init(obj: ObjectDesc, hand: HandDesc, B: int, seed: int = 0, stando
                   first: int = 0) -> np.ndarray:
     """[B, 7+J] initial configurations for candidates first..first+B-1."""
     out = np.zeros((B, 7 + hand.num_joints))
+    if B == 0:
+        return out
     standoff = standoff_scale * obj.bounding_radius()
     mid = hand.mid_range()
+    d = np.zeros((B, 3))
+    roll = np.zeros(B)
     for b in range(B):
         rng = np.random.Generator(np.random.Philox(key=seed, counter=first + b))
-        d = rng.normal(size=3)
-        d /= np.linalg.norm(d)
-        roll = rng.uniform(0.0, 2.0 * np.pi)
-        p_s, n = surface_point(obj, d)
-        z = -n
+        v = rng.normal(size=3)
+        d[b] = v / np.linalg.norm(v)
+        roll[b] = rng.uniform(0.0, 2.0 * np.pi)
+    p_s, n = surface_points(obj, d)
+    for b in range(B):
+        z = -n[b]
         a = np.array([1.0, 0.0, 0.0]) if abs(z[0]) < 0.9 else np.array([0.0, 1.0, 0.0])
         x = a - np.dot(a, z) * z
         x /= np.linalg.norm(x)
         y = np.cross(z, x)
-        c, s = np.cos(roll), np.sin(roll)
-        xr, yr = c * x + s * y, -s * x + c * y
+        c, s_ = np.cos(roll[b]), np.sin(roll[b])
+        xr, yr = c * x + s_ * y, -s_ * x + c * y
         R = np.stack([xr, yr, z], axis=1)  # columns: palm x, y, z in world
-        out[b, :3] = p_s + standoff * n
+        out[b, :3] = p_s[b] + standoff * n[b]
         out[b, 3:7] = _quat_from_matrix(R)
-        out[b, 7:] = mid
+    out[:, 7:] = mid
     return out

@@ -1,0 +1,151 @@
+"""Measure BASELINE.json configs 1, 3, 4, 5 on one B200 (config 2 is bench.py's
+headline). Writes one JSON record per line to stdout.
+
+  config1  barrett3 on the analytic sphere (R 25 mm), 64 candidates, 200 iterations:
+           FULL run on the GPU, grasps/s, plus the reference CPU full run on a
+           16-candidate subset and a distribution comparison (final loss /
+           contact count / penetration, KS test).
+  config3  shadow22_dense (J=22, N=4093) on a 128^3 procedural-blob grid,
+           4096 candidates: candidate-iterations/s over a few iterations.
+  config4  barrett3 x 64 procedural blob objects (64^3) x 1024 candidates
+           (65,536 candidates, object-major, dgx_optimize_multi).
+  config5  sweep: 3 hands x SDF resolution {32,64,128}^3 x candidates
+           {256, 1024, 4096, 16384} (one GPU; multi-GPU runs shard candidates
+           with no collective, so aggregate = per-GPU x N).
+
+usage: python tools/bench_configs.py [config1 config3 config4 config5]
+"""
+import json
+import os
+import sys
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+
+import torch  # noqa: E402
+
+from paper_2306_08132_b200 import api, capi, init, model  # noqa: E402
+
+DEV = torch.device("cuda", 0)
+FLAGS = capi.DGX_DEVICE_PTRS | capi.DGX_ASYNC
+
+
+def timed_opt(ctx, objs, hand, hd, qs, iters, k_begin, k_end, reps=1):
+    """Device-resident multi-object optimize over [k_begin, k_end); CUDA-event time."""
+    stream = torch.cuda.Stream(DEV)
+    torch.cuda.set_stream(stream)
+    ctx.set_stream(stream.cuda_stream)
+    D = 6 + hd.num_joints
+    counts = np.array([q.shape[0] for q in qs], np.int32)
+    q = torch.tensor(np.concatenate(qs, 0), device=DEV)
+    m = torch.zeros(q.shape[0], D, dtype=torch.float64, device=DEV)
+    v = torch.zeros_like(m)
+    status = torch.zeros(q.shape[0], dtype=torch.int32, device=DEV)
+    proto, params, w = api.StabilityProtocol.standard(), api.SimParams(), api.LossWeights()
+    opt = api.OptConfig(iterations=iters)
+    # warm-up: the first iteration of the schedule
+    api.optimize_multi(ctx, objs, hand, q, counts, proto, params, w, opt, k_begin=0, k_end=1, adam_m=m, adam_v=v,
+                       flags=FLAGS, status=status)
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    api.optimize_multi(ctx, objs, hand, q, counts, proto, params, w, opt, k_begin=k_begin, k_end=k_end, adam_m=m,
+                       adam_v=v, flags=FLAGS, status=status)
+    e1.record(stream)
+    torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1)
+    ctx.set_stream(None)
+    return ms, q.cpu().numpy(), int(torch.count_nonzero(status))
+
+
+def config1():
+    from scipy.stats import ks_2samp
+    from oracle import ref
+    hd = model.HandDesc.asset("barrett3")
+    od = model.sphere(0.025)
+    ctx = api.Context(0)
+    hand, obj = api.Hand(ctx, hd), api.GraspObject(ctx, od)
+    B, K = 64, 200
+    q0 = init.approach_init(od, hd, B, seed=1)
+    ms, qf, bad = timed_opt(ctx, [obj], hand, hd, [q0], K, 1, K)
+    ci_s = B * (K - 1) / (ms * 1e-3)
+    # reference CPU: full 200-iteration runs on a 16-candidate subset (glibc build = the reference)
+    rh = ref.RefHand.barrett3(variant="glibc")
+    ro = ref.RefObject.from_desc(od, variant="glibc")
+    sub = 16
+    t0 = time.perf_counter()
+    r = ref.optimize(ro, rh, q0[:sub], ref.default_params(), iters=K)
+    cpu_s = time.perf_counter() - t0
+    proto = api.StabilityProtocol.standard()
+    eg, sg, _ = api.evaluate_losses(ctx, obj, hand, qf, proto, api.SimParams())
+    er, sr = [], []
+    for b in range(sub):
+        er.append(ref.evaluate_losses(ro, rh, r["q"][b], ref.default_params()))
+        sr.append([ref.sim_forward(ro, rh, r["q"][b], m, ref.default_params())[1] for m in range(7)])
+    er, sr = np.array(er), np.array(sr)
+    return dict(config="config1", workload="barrett3 (N=1999) on analytic sphere R=25mm, 64 candidates, 200 iterations",
+                gpu_candidate_iterations_per_s=ci_s, gpu_full_run_s=ms * 1e-3 * K / (K - 1),
+                gpu_grasps_per_s=B / (ms * 1e-3 * K / (K - 1)), failed=bad,
+                cpu_reference_candidate_iterations_per_s=sub * K / cpu_s, cpu_threads=os.cpu_count(),
+                cpu_subset=sub,
+                ks_final_stable_loss_p=float(ks_2samp(eg[:, 0], er[:, 0]).pvalue),
+                ks_contacts_p=float(ks_2samp(sg[:, :, 0].sum(1), sr[:, :, 0].sum(1)).pvalue),
+                ks_penetration_p=float(ks_2samp(sg[:, :, 3].max(1), sr[:, :, 3].max(1)).pvalue),
+                mean_final_loss_gpu=float(eg[:, 0].mean()), mean_final_loss_ref=float(er[:, 0].mean()))
+
+
+def config3():
+    hd = model.HandDesc.asset("shadow22_dense")
+    od = model.blob_grid(seed=3, res=128)
+    ctx = api.Context(0)
+    hand, obj = api.Hand(ctx, hd), api.GraspObject(ctx, od)
+    B, K = 4096, 500
+    q0 = init.approach_init(od, hd, B, seed=3)
+    ms, _, bad = timed_opt(ctx, [obj], hand, hd, [q0], K, 1, 4)
+    return dict(config="config3", workload="shadow22_dense (J=22, N=4093) on 128^3 procedural blob grid, 4096 candidates",
+                gpu_candidate_iterations_per_s=B * 3 / (ms * 1e-3), failed=bad, iterations_timed="1..3 of 500")
+
+
+def config4():
+    hd = model.HandDesc.asset("barrett3")
+    ods = [model.blob_grid(seed=s, res=64) for s in range(64)]
+    ctx = api.Context(0)
+    hand = api.Hand(ctx, hd)
+    objs = [api.GraspObject(ctx, o) for o in ods]
+    per = 1024
+    qs = [init.approach_init(o, hd, per, seed=100 + i) for i, o in enumerate(ods)]
+    ms, _, bad = timed_opt(ctx, objs, hand, hd, qs, 500, 1, 3)
+    return dict(config="config4", workload="barrett3 x 64 procedural blob objects (64^3) x 1024 candidates = 65536",
+                gpu_candidate_iterations_per_s=64 * per * 2 / (ms * 1e-3), failed=bad, iterations_timed="1..2 of 500")
+
+
+def config5():
+    out = []
+    ctx = api.Context(0)
+    for hname in ("barrett3", "allegro16", "shadow22"):
+        hd = model.HandDesc.asset(hname)
+        hand = api.Hand(ctx, hd)
+        for res in (32, 64, 128):
+            od = model.blob_grid(seed=11, res=res)
+            obj = api.GraspObject(ctx, od)
+            for B in (256, 1024, 4096, 16384):
+                q0 = init.approach_init(od, hd, B, seed=5)
+                ms, _, bad = timed_opt(ctx, [obj], hand, hd, [q0], 500, 1, 2)
+                out.append(dict(hand=hname, sdf_res=res, candidates=B, cand_iter_per_s=B / (ms * 1e-3), failed=bad))
+    return dict(config="config5", workload="sweep: hands x SDF resolution x candidates (1 GPU)", rows=out)
+
+
+def main():
+    which = sys.argv[1:] or ["config1", "config3", "config4", "config5"]
+    for w in which:
+        t = time.time()
+        rec = globals()[w]()
+        rec["wall_s"] = time.time() - t
+        print(json.dumps(rec), flush=True)
+
+
+if __name__ == "__main__":
+    main()

@@ -17,7 +17,8 @@ from paper_2306_08132_b200 import api, capi, init, model  # noqa: E402
 NAMES = {0: "forward sweeps (incl. corrections)", 1: "  apply_correction", 2: "friction fwd",
          4: "friction adjoint", 5: "adjoint runs (process_run)", 6: "  pass 1a (classify+coef)",
          7: "  pass 1b (compose)", 8: "  pass 2 (scan)", 9: "  pass 3 (emit)", 10: "  flush",
-         11: "correction adjoints", 12: "run_sim total"}
+         11: "correction adjoints", 12: "run_sim total", 13: "scheduler: claim / spin",
+         14: "scheduler: finalize (losses, FK adjoint, Adam)", 15: "scheduler: FK / load next"}
 COUNTS = {16: "forward chunk iterations", 17: "forward candidate lanes", 18: "adjoint blocks", 19: "runs",
           20: "forward corrections tried", 21: "frictions applied", 22: "sims"}
 

@@ -9,7 +9,10 @@
  *                              loaded / assembled hand (samples in forward()
  *                              order, hand.hpp:143-151)
  *   dgx_object_upload          dg::GraspObject (losses.hpp:38-44): SDF backend
+ *                              (incl. dg::MeshSdf over a TriMesh, sdf.hpp:21-53)
  *                              + InertialData (rigid.hpp:8-13)
+ *   dgx_sdf_query_batch        MeshSdf::dilated / dilated_within (sdf.hpp:41-45)
+ *   dgx_mesh_inertia           dg::inertia_from_mesh (rigid.cpp:24-94)
  *   dgx_forward_batch          HandModel::forward(const HandConfig&) (hand.hpp:86)
  *   dgx_loss_gradient_batch    dg::loss_gradient (losses.hpp:126-127, losses.cpp:20-66)
  *   dgx_evaluate_losses_batch  dg::evaluate_losses (losses.hpp:119-121, losses.cpp:7-18)
@@ -81,7 +84,7 @@ typedef struct {
   const int32_t* sample_link;        /* [N] (hand.hpp:76) */
 } dgx_hand_desc;
 
-enum { DGX_SDF_SPHERE = 1, DGX_SDF_BOX = 2, DGX_SDF_GRID = 4 };
+enum { DGX_SDF_SPHERE = 1, DGX_SDF_BOX = 2, DGX_SDF_GRID = 4, DGX_SDF_MESH = 8 };
 
 typedef struct {
   int32_t kind;
@@ -96,6 +99,15 @@ typedef struct {
   double mass;             /* InertialData (rigid.hpp:8-13) */
   double com[3];
   double inertia_body_inv[9];
+  /* mesh (DGX_SDF_MESH): dg::TriMesh (mesh.hpp:15-21) + MeshSdf alpha_phong
+     (sdf.hpp:24). Validated as TriMesh::finalize (mesh.cpp:12-71); host memory
+     (copied). The BVH is built as Bvh::build (bvh.cpp:148-163). */
+  int32_t num_vertices, num_faces;
+  const double* vertices;        /* [V,3] */
+  const int32_t* faces;          /* [F,3] outward (counter-clockwise) winding */
+  const double* vertex_normals;  /* [V,3] unit (TriMesh::set_vertex_normals), or NULL:
+                                    area-weighted face normals (mesh.cpp:60-70) */
+  double alpha_phong;            /* in [0,1] (sdf.cpp:19) */
 } dgx_object_desc;
 
 typedef struct {
@@ -134,6 +146,25 @@ int dgx_hand_upload(dgx_ctx* ctx, const dgx_hand_desc* desc, dgx_hand** out);
 int dgx_hand_free(dgx_hand* hand);
 int dgx_object_upload(dgx_ctx* ctx, const dgx_object_desc* desc, dgx_object** out);
 int dgx_object_free(dgx_object* obj);
+
+/* SDF queries in the object's canonical frame: out [n, 8] = rho - radius,
+   unit gradient (3), smoothed / proxy point (3), sign, as MeshSdf::dilated
+   (sdf.hpp:41, sdf.cpp:62-67). within != 0: MeshSdf::dilated_within with the
+   solver's 5 mm cull (sdf.cpp:69-81, sim.hpp:213); a culled point (nullopt)
+   reports rho = +inf and sign 0. Non-mesh backends never cull. */
+int dgx_sdf_query_batch(dgx_ctx* ctx, const dgx_object* obj, int32_t n, const double* points, double radius,
+                        int32_t within, double* out, uint32_t flags);
+
+/* dg::inertia_from_mesh (rigid.cpp:24-94): mass, com [3], inertia_body [9]
+   and its closed-form inverse [9] (row-major) of a closed mesh at `density`. */
+int dgx_mesh_inertia(int32_t num_vertices, const double* vertices, int32_t num_faces, const int32_t* faces,
+                     double density, double* mass, double* com, double* inertia, double* inertia_inv);
+
+/* Host-only inspection of the mesh BVH dgx_object_upload builds (Bvh::build,
+   bvh.cpp:148-163): node boxes [n,6] (lo, hi), (left, right, first, count)
+   [n,4], leaf-order face ids [F]; *n_nodes = node count (arrays sized cap). */
+int dgx_mesh_bvh(int32_t num_vertices, const double* vertices, int32_t num_faces, const int32_t* faces, int32_t cap,
+                 double* boxes, int32_t* links, int32_t* face_order, int32_t* n_nodes);
 
 /* points [B, N, 3] = HandModel::forward(q_b) */
 int dgx_forward_batch(dgx_ctx* ctx, const dgx_hand* hand, int32_t B, const double* q, double* points,

@@ -84,7 +84,15 @@ def lib(variant: str = "sm") -> C.CDLL:
     L.dgr_object_icosphere.argtypes = [C.c_double, C.c_int, C.c_double, C.c_double]
     L.dgr_object_box_mesh.restype = vp
     L.dgr_object_box_mesh.argtypes = [C.c_double] * 5
+    L.dgr_object_cylinder_mesh.restype = vp
+    L.dgr_object_cylinder_mesh.argtypes = [C.c_double, C.c_double, C.c_int, C.c_double, C.c_double]
+    L.dgr_object_blob_mesh.restype = vp
+    L.dgr_object_blob_mesh.argtypes = [C.c_double, C.c_int, C.c_double, C.c_uint64, C.c_double, C.c_double]
     L.dgr_object_free.argtypes = [vp]
+    L.dgr_object_mesh_dims.argtypes = [vp, _ip]
+    L.dgr_object_mesh_export.argtypes = [vp, _dp, _ip, _dp]
+    L.dgr_object_bvh.argtypes = [vp, _dp, _ip, _ip, C.c_int]
+    L.dgr_object_query_within.argtypes = [vp, _dp, C.c_double, _dp]
     L.dgr_object_use_sphere.argtypes = [vp, C.c_double, C.c_double, C.c_double, C.c_double]
     L.dgr_object_use_box.argtypes = [vp, _dp, _dp]
     L.dgr_object_use_grid.argtypes = [vp, _ip, _dp, C.c_double, C.c_double, _fp]
@@ -204,6 +212,51 @@ class RefObject:
         return cls(L, L.dgr_object_icosphere(radius, subdiv, density, alpha))
 
     @classmethod
+    def box_mesh(cls, sx, sy, sz, density=1000.0, alpha=0.75, variant="sm"):
+        L = lib(variant)
+        return cls(L, L.dgr_object_box_mesh(sx, sy, sz, density, alpha))
+
+    @classmethod
+    def cylinder_mesh(cls, radius, height, segments, density=1000.0, alpha=0.75, variant="sm"):
+        L = lib(variant)
+        return cls(L, L.dgr_object_cylinder_mesh(radius, height, segments, density, alpha))
+
+    @classmethod
+    def blob_mesh(cls, radius, subdiv, amplitude, seed, density=1000.0, alpha=0.75, variant="sm"):
+        L = lib(variant)
+        return cls(L, L.dgr_object_blob_mesh(radius, subdiv, amplitude, seed, density, alpha))
+
+    @classmethod
+    def mesh(cls, V, F, density=1000.0, alpha=0.75, variant="sm"):
+        L = lib(variant)
+        V = np.ascontiguousarray(V, np.float64)
+        F = np.ascontiguousarray(F, np.int32)
+        return cls(L, L.dgr_object_mesh(_d(V), V.shape[0], _i(F), F.shape[0], density, alpha))
+
+    def mesh_export(self):
+        """(vertices [V,3], faces [F,3] int32, vertex_normals [V,3]) of the object's TriMesh."""
+        dims = np.zeros(2, np.int32)
+        self.L.dgr_object_mesh_dims(self.ptr, _i(dims))
+        V, F, VN = np.zeros((dims[0], 3)), np.zeros((dims[1], 3), np.int32), np.zeros((dims[0], 3))
+        self.L.dgr_object_mesh_export(self.ptr, _d(V), _i(F), _d(VN))
+        return V, F, VN
+
+    def bvh(self):
+        """The reference Bvh: boxes [n,6] (lo, hi), links [n,4] (left, right, first, count), face_order."""
+        dims = np.zeros(2, np.int32)
+        self.L.dgr_object_mesh_dims(self.ptr, _i(dims))
+        cap = 2 * int(dims[1]) + 1
+        boxes, links, fo = np.zeros((cap, 6)), np.zeros((cap, 4), np.int32), np.zeros(int(dims[1]), np.int32)
+        n = self.L.dgr_object_bvh(self.ptr, _d(boxes), _i(links), _i(fo), cap)
+        return boxes[:n], links[:n], fo
+
+    def query_within(self, r, radius=0.0):
+        r = np.ascontiguousarray(r, np.float64)
+        out = np.zeros(8)
+        _check(self.L, self.L.dgr_object_query_within(self.ptr, _d(r), radius, _d(out)))
+        return out
+
+    @classmethod
     def from_desc(cls, desc, variant="sm"):
         """Non-mesh backend from a paper_2306_08132_b200 ObjectDesc, with its inertia."""
         L = lib(variant)
@@ -216,6 +269,10 @@ class RefObject:
             c = np.ascontiguousarray(desc.center, np.float64)
             h = np.ascontiguousarray(desc.half_extents, np.float64)
             L.dgr_object_use_box(o.ptr, _d(c), _d(h))
+        elif kind == "mesh":  # the UNMODIFIED reference MeshSdf over the same TriMesh
+            if desc.vertex_normals is not None:
+                raise ValueError("explicit vertex normals are not plumbed into the oracle")
+            o = cls.mesh(desc.vertices, desc.faces, 1000.0, desc.alpha_phong, variant)
         elif kind == "grid":
             dims = np.ascontiguousarray(desc.dims, np.int32)
             org = np.ascontiguousarray(desc.origin, np.float64)

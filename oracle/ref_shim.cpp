@@ -23,6 +23,7 @@
 #include <cmath>
 #include <cstdint>
 #include <cstring>
+#include <limits>
 #include <memory>
 #include <optional>
 #include <stdexcept>
@@ -50,6 +51,7 @@ class AnySdf {
       : mesh_sdf_(std::make_shared<MeshSdf>(std::move(mesh), alpha_phong)) {}
 
   const TriMesh& mesh() const { return mesh_sdf_->mesh(); }
+  const MeshSdf* mesh_sdf() const { return mesh_sdf_.get(); }
 
   void use_mesh() { kind_ = 0; }
   void use_sphere(const dgx::SphereSdf& s) { kind_ = dgx::kSdfSphere; sphere_ = s; }
@@ -293,7 +295,46 @@ void* dgr_object_icosphere(double radius, int subdiv, double density, double alp
 void* dgr_object_box_mesh(double sx, double sy, double sz, double density, double alpha) {
   try { return new GraspObject(make_box(sx, sy, sz), density, alpha); } catch (const std::exception& e) { fail(e); return nullptr; }
 }
+void* dgr_object_cylinder_mesh(double radius, double height, int segments, double density, double alpha) {
+  try { return new GraspObject(make_cylinder(radius, height, segments), density, alpha); } catch (const std::exception& e) { fail(e); return nullptr; }
+}
+void* dgr_object_blob_mesh(double radius, int subdiv, double amplitude, std::uint64_t seed, double density, double alpha) {
+  try { return new GraspObject(make_blob(radius, subdiv, amplitude, seed), density, alpha); } catch (const std::exception& e) { fail(e); return nullptr; }
+}
 void dgr_object_free(void* o) { delete static_cast<GraspObject*>(o); }
+
+// the object's TriMesh (vertices, faces, vertex normals) and alpha_phong
+void dgr_object_mesh_dims(void* o, int* out) {
+  const TriMesh& m = static_cast<GraspObject*>(o)->sdf.mesh();
+  out[0] = static_cast<int>(m.num_vertices());
+  out[1] = static_cast<int>(m.num_faces());
+}
+void dgr_object_mesh_export(void* o, double* V, int* F, double* VN) {
+  const TriMesh& m = static_cast<GraspObject*>(o)->sdf.mesh();
+  for (std::size_t i = 0; i < m.num_vertices(); ++i) {
+    V[3 * i] = m.vertices[i].x; V[3 * i + 1] = m.vertices[i].y; V[3 * i + 2] = m.vertices[i].z;
+    VN[3 * i] = m.vertex_normals[i].x; VN[3 * i + 1] = m.vertex_normals[i].y; VN[3 * i + 2] = m.vertex_normals[i].z;
+  }
+  for (std::size_t f = 0; f < m.num_faces(); ++f)
+    for (int k = 0; k < 3; ++k) F[3 * f + k] = m.faces[f][k];
+}
+
+// the reference Bvh (bvh.hpp:27-33, 55-56): node boxes [n,6], (left, right,
+// first, count) [n,4], face_order [F]; returns the node count
+int dgr_object_bvh(void* o, double* boxes, int* links, int* face_order, int cap) {
+  const MeshSdf& sdf = *static_cast<GraspObject*>(o)->sdf.mesh_sdf();
+  const auto& nodes = sdf.bvh().nodes();
+  const int n = static_cast<int>(nodes.size());
+  for (int i = 0; i < n && i < cap; ++i) {
+    const auto& nd = nodes[i];
+    boxes[6 * i] = nd.box.lo.x; boxes[6 * i + 1] = nd.box.lo.y; boxes[6 * i + 2] = nd.box.lo.z;
+    boxes[6 * i + 3] = nd.box.hi.x; boxes[6 * i + 4] = nd.box.hi.y; boxes[6 * i + 5] = nd.box.hi.z;
+    links[4 * i] = nd.left; links[4 * i + 1] = nd.right; links[4 * i + 2] = nd.first; links[4 * i + 3] = nd.count;
+  }
+  const auto& fo = sdf.bvh().face_order();
+  for (std::size_t i = 0; i < fo.size(); ++i) face_order[i] = fo[i];
+  return n;
+}
 
 void dgr_object_use_sphere(void* o, double cx, double cy, double cz, double r) {
   static_cast<GraspObject*>(o)->sdf.use_sphere(dgx::SphereSdf{{cx, cy, cz}, r});
@@ -328,6 +369,24 @@ int dgr_object_query(void* o, const double* r, double radius, double* out) {
     out[1] = q.grad.x; out[2] = q.grad.y; out[3] = q.grad.z;
     out[4] = q.smoothed_point.x; out[5] = q.smoothed_point.y; out[6] = q.smoothed_point.z;
     out[7] = q.sign;
+    return 0;
+  } catch (const std::exception& e) { return fail(e); }
+}
+
+// forward-only query MeshSdf::dilated_within (sdf.cpp:69-81) with the
+// solver's cull margin (sim.hpp:213); nullopt -> out[0] = +inf, rest 0
+int dgr_object_query_within(void* o, const double* r, double radius, double* out) {
+  try {
+    auto q = static_cast<GraspObject*>(o)->sdf.dilated_within({r[0], r[1], r[2]}, radius, 0.005);
+    if (!q) {
+      out[0] = std::numeric_limits<double>::infinity();
+      for (int k = 1; k < 8; ++k) out[k] = 0.0;
+      return 0;
+    }
+    out[0] = q->rho;
+    out[1] = q->grad.x; out[2] = q->grad.y; out[3] = q->grad.z;
+    out[4] = q->smoothed_point.x; out[5] = q->smoothed_point.y; out[6] = q->smoothed_point.z;
+    out[7] = q->sign;
     return 0;
   } catch (const std::exception& e) { return fail(e); }
 }

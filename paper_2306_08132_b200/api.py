@@ -214,6 +214,34 @@ def evaluate_losses(ctx: Context, obj: GraspObject, hand: Hand, q, protocol: Sta
     return losses, stats, status
 
 
+def sdf_query(ctx: Context, obj: GraspObject, points, radius: float = 0.0, within: bool = False) -> np.ndarray:
+    """[n, 8] = rho - radius, unit gradient, smoothed point, sign at object-frame
+    points: MeshSdf::dilated (sdf.cpp:62-67), or dilated_within with the
+    solver's 5 mm cull (sdf.cpp:69-81) when ``within`` (culled: rho = +inf,
+    sign 0). Any backend; only meshes cull."""
+    p = _f64(points, (-1, 3))
+    out = np.zeros((p.shape[0], 8))
+    capi.check(ctx.L.dgx_sdf_query_batch(ctx.h, obj.h, p.shape[0], capi.ptr(p), float(radius), int(bool(within)),
+                                         capi.ptr(out), 0))
+    return out
+
+
+def mesh_bvh(vertices, faces):
+    """Host-only: the BVH dgx_object_upload builds for a mesh (Bvh::build,
+    bvh.cpp:148-163) as (boxes [n,6], links [n,4] left/right/first/count,
+    leaf-order face ids)."""
+    import ctypes as C
+    V = np.ascontiguousarray(vertices, np.float64).reshape(-1, 3)
+    F = np.ascontiguousarray(faces, np.int32).reshape(-1, 3)
+    cap = 2 * F.shape[0] + 1
+    boxes, links, fo = np.zeros((cap, 6)), np.zeros((cap, 4), np.int32), np.zeros(F.shape[0], np.int32)
+    n = C.c_int32()
+    L = capi.load()
+    capi.check(L.dgx_mesh_bvh(V.shape[0], capi.ptr(V), F.shape[0], capi.ptr(F), cap, capi.ptr(boxes),
+                              capi.ptr(links), capi.ptr(fo), C.byref(n)))
+    return boxes[:n.value], links[:n.value], fo
+
+
 def apply_gradient_step(ctx: Context, hand: Hand, q, g, lr: float) -> np.ndarray:
     q = _f64(q, (-1, 7 + hand.J))
     g = _f64(g, (q.shape[0], 6 + hand.J))

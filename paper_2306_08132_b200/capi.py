@@ -19,7 +19,7 @@ _fp = C.POINTER(C.c_float)
 
 DGX_DEVICE_PTRS = 1
 DGX_ASYNC = 2
-DGX_SDF_SPHERE, DGX_SDF_BOX, DGX_SDF_GRID = 1, 2, 4
+DGX_SDF_SPHERE, DGX_SDF_BOX, DGX_SDF_GRID, DGX_SDF_MESH = 1, 2, 4, 8
 
 STATUS_NAMES = {
     0: "ok",
@@ -46,6 +46,8 @@ class ObjectDescC(C.Structure):
         ("half_extents", C.c_double * 3), ("dims", C.c_int32 * 3), ("origin", C.c_double * 3),
         ("spacing", C.c_double), ("inv_spacing", C.c_double), ("values", _fp), ("mass", C.c_double),
         ("com", C.c_double * 3), ("inertia_body_inv", C.c_double * 9),
+        ("num_vertices", C.c_int32), ("num_faces", C.c_int32), ("vertices", _dp), ("faces", _ip),
+        ("vertex_normals", _dp), ("alpha_phong", C.c_double),
     ]
 
 
@@ -71,7 +73,8 @@ EXPORTS = [
     "dgx_ctx_set_correction_capacity", "dgx_ctx_launch_count", "dgx_hand_upload", "dgx_hand_free",
     "dgx_object_upload", "dgx_object_free", "dgx_forward_batch", "dgx_loss_gradient_batch",
     "dgx_evaluate_losses_batch", "dgx_apply_gradient_step_batch", "dgx_optimize_batch", "dgx_debug_sims",
-    "dgx_fp64_peak", "dgx_optimize_multi",
+    "dgx_fp64_peak", "dgx_optimize_multi", "dgx_sdf_query_batch", "dgx_mesh_inertia",
+    "dgx_mesh_bvh",
 ]
 
 _lib: C.CDLL | None = None
@@ -114,6 +117,9 @@ def load() -> C.CDLL:
     L.dgx_fp64_peak.argtypes = [C.c_int, _dp, _dp]
     L.dgx_optimize_multi.argtypes = [vp, vp, C.c_int32, vp, vp, vp, vp, vp, C.POINTER(ParamsC), C.POINTER(OptC), vp,
                                      vp, C.c_uint32]
+    L.dgx_sdf_query_batch.argtypes = [vp, vp, C.c_int32, vp, C.c_double, C.c_int32, vp, C.c_uint32]
+    L.dgx_mesh_inertia.argtypes = [C.c_int32, vp, C.c_int32, vp, C.c_double, _dp, _dp, _dp, _dp]
+    L.dgx_mesh_bvh.argtypes = [C.c_int32, vp, C.c_int32, vp, C.c_int32, vp, vp, vp, _ip]
     _lib = L
     return L
 
@@ -149,7 +155,7 @@ def hand_desc_c(h) -> tuple[HandDescC, list]:
 def object_desc_c(o) -> tuple[ObjectDescC, list]:
     d = ObjectDescC()
     keep = []
-    d.kind = {"sphere": DGX_SDF_SPHERE, "box": DGX_SDF_BOX, "grid": DGX_SDF_GRID}[o.kind]
+    d.kind = {"sphere": DGX_SDF_SPHERE, "box": DGX_SDF_BOX, "grid": DGX_SDF_GRID, "mesh": DGX_SDF_MESH}[o.kind]
     d.center[:] = [float(v) for v in o.center]
     d.radius = float(o.radius)
     d.half_extents[:] = [float(v) for v in o.half_extents]
@@ -161,6 +167,18 @@ def object_desc_c(o) -> tuple[ObjectDescC, list]:
         d.spacing = float(o.spacing)
         d.inv_spacing = float(o.inv_spacing)
         d.values = vals.ctypes.data_as(_fp)
+    if o.kind == "mesh":
+        V = np.ascontiguousarray(o.vertices, np.float64)
+        F = np.ascontiguousarray(o.faces, np.int32)
+        keep += [V, F]
+        d.num_vertices, d.num_faces = V.shape[0], F.shape[0]
+        d.vertices = V.ctypes.data_as(_dp)
+        d.faces = F.ctypes.data_as(_ip)
+        if o.vertex_normals is not None:
+            VN = np.ascontiguousarray(o.vertex_normals, np.float64)
+            keep.append(VN)
+            d.vertex_normals = VN.ctypes.data_as(_dp)
+        d.alpha_phong = float(o.alpha_phong)
     d.mass = float(o.mass)
     d.com[:] = [float(v) for v in o.com]
     d.inertia_body_inv[:] = [float(v) for v in np.asarray(o.inertia_body_inv, np.float64).reshape(9)]

@@ -12,6 +12,7 @@
 
 #include "../../include/dgx.h"
 #include "dgx_kernel.cuh"
+#include "dgx_mesh_host.h"
 
 using namespace dgx;
 
@@ -103,10 +104,8 @@ struct dgx_hand {
 struct dgx_object {
   dgx_ctx* ctx;
   int kind;
-  SphereSdf sphere{};
-  BoxSdf box{};
-  GridSdf grid{};
-  DevBuf vals;
+  SdfSet sdf{};
+  DevBuf vals;  // grid values, or the mesh block (nodes, faces, tri, vx, vn, MeshGeom)
   KObj k;
 };
 
@@ -356,20 +355,54 @@ int dgx_object_upload(dgx_ctx* c, const dgx_object_desc* d, dgx_object** out) {
     o->kind = d->kind;
     try {
       set_device(c);
+      o->sdf.kind = d->kind;
       if (d->kind == DGX_SDF_SPHERE) {
         if (!(d->radius > 0.0)) throw DgxError(DGX_E_INVALID, "sphere: radius must be > 0");
-        o->sphere = SphereSdf{V3{d->center[0], d->center[1], d->center[2]}, d->radius};
+        o->sdf.sph = SphereSdf{V3{d->center[0], d->center[1], d->center[2]}, d->radius};
       } else if (d->kind == DGX_SDF_BOX) {
-        o->box = BoxSdf{V3{d->center[0], d->center[1], d->center[2]},
-                        V3{d->half_extents[0], d->half_extents[1], d->half_extents[2]}};
+        o->sdf.box = BoxSdf{V3{d->center[0], d->center[1], d->center[2]},
+                            V3{d->half_extents[0], d->half_extents[1], d->half_extents[2]}};
       } else if (d->kind == DGX_SDF_GRID) {
         if (d->dims[0] < 2 || d->dims[1] < 2 || d->dims[2] < 2 || !d->values)
           throw DgxError(DGX_E_INVALID, "grid: dims must be >= 2 and values non-NULL");
         size_t n = static_cast<size_t>(d->dims[0]) * d->dims[1] * d->dims[2];
         o->vals.ensure(n * sizeof(float));
         cuda_check(cudaMemcpy(o->vals.p, d->values, n * sizeof(float), cudaMemcpyHostToDevice), "grid upload");
-        o->grid = GridSdf{d->dims[0], d->dims[1], d->dims[2], V3{d->origin[0], d->origin[1], d->origin[2]},
-                          d->spacing, d->inv_spacing, static_cast<const float*>(o->vals.p)};
+        o->sdf.grd = GridSdf{d->dims[0], d->dims[1], d->dims[2], V3{d->origin[0], d->origin[1], d->origin[2]},
+                             d->spacing, d->inv_spacing, static_cast<const float*>(o->vals.p)};
+      } else if (d->kind == DGX_SDF_MESH) {
+        // MeshSdf(TriMesh, alpha_phong) (sdf.cpp:17-20): validate, BVH, upload
+        if (!(d->alpha_phong >= 0.0 && d->alpha_phong <= 1.0))
+          throw std::invalid_argument("alpha_phong must be in [0,1]");
+        MeshHost mh;
+        mesh_prepare(d->num_vertices, d->vertices, d->num_faces, d->faces, d->vertex_normals, mh);
+        auto rnd = [](size_t x) { return (x + 255) & ~size_t(255); };
+        const size_t b_nodes = rnd(mh.nodes.size() * sizeof(MeshNode)), b_faces = rnd(mh.faces.size() * sizeof(MeshFace));
+        const size_t b_tri = rnd(mh.tri.size() * sizeof(int)), b_v = rnd(mh.vx.size() * sizeof(double));
+        const size_t total = b_nodes + b_faces + b_tri + 2 * b_v + rnd(sizeof(MeshGeom));
+        o->vals.ensure(total);
+        char* base = static_cast<char*>(o->vals.p);
+        MeshGeom g{};
+        size_t off = 0;
+        auto put = [&](const void* src, size_t bytes, size_t span) {
+          cuda_check(cudaMemcpy(base + off, src, bytes, cudaMemcpyHostToDevice), "mesh upload");
+          void* dst = base + off;
+          off += span;
+          return dst;
+        };
+        g.nodes = static_cast<const MeshNode*>(put(mh.nodes.data(), mh.nodes.size() * sizeof(MeshNode), b_nodes));
+        g.faces = static_cast<const MeshFace*>(put(mh.faces.data(), mh.faces.size() * sizeof(MeshFace), b_faces));
+        g.tri = static_cast<const int*>(put(mh.tri.data(), mh.tri.size() * sizeof(int), b_tri));
+        g.vx = static_cast<const double*>(put(mh.vx.data(), mh.vx.size() * sizeof(double), b_v));
+        g.vn = static_cast<const double*>(put(mh.vn.data(), mh.vn.size() * sizeof(double), b_v));
+        for (int k = 0; k < 3; ++k) {
+          g.blo[k] = mh.blo[k];
+          g.bhi[k] = mh.bhi[k];
+        }
+        g.alpha = d->alpha_phong;
+        mesh_ray_dirs(g.dir, g.inv);
+        g.cull = 0.005;  // ContactSolver::kCullMargin (sim.hpp:213)
+        o->sdf.mesh = MeshSdf{static_cast<const MeshGeom*>(put(&g, sizeof(MeshGeom), rnd(sizeof(MeshGeom))))};
       } else {
         throw DgxError(DGX_E_UNSUPPORTED, "object: unknown SDF kind " + std::to_string(d->kind));
       }
@@ -397,6 +430,53 @@ int dgx_object_free(dgx_object* o) {
     cudaSetDevice(o->ctx->device);
     o->vals.release();
     delete o;
+  });
+}
+
+int dgx_sdf_query_batch(dgx_ctx* c, const dgx_object* o, int32_t n, const double* points, double radius,
+                        int32_t within, double* out, uint32_t flags) {
+  return guarded([&] {
+    if (!c || !o) throw DgxError(DGX_E_INVALID, "NULL argument");
+    if (n < 0) throw DgxError(DGX_E_INVALID, "n < 0");
+    if (radius < 0.0) throw std::invalid_argument("dilation radius must be >= 0");
+    if (n == 0) return;
+    set_device(c);
+    const bool dev = flags & DGX_DEVICE_PTRS;
+    Staging s(c, dev, bytes_round(24ull * n) + bytes_round(64ull * n));
+    const double* dp = s.in(points, static_cast<size_t>(n) * 3);
+    double* dq = s.out(out, static_cast<size_t>(n) * 8);
+    cuda_check(launch_sdf_query(o->sdf, n, dp, radius, within, dq, c->stream), "sdf_query_kernel");
+    ++c->launches;
+    s.finish(flags);
+  });
+}
+
+int dgx_mesh_inertia(int32_t num_vertices, const double* vertices, int32_t num_faces, const int32_t* faces,
+                     double density, double* mass, double* com, double* inertia, double* inertia_inv) {
+  return guarded([&] {
+    if (!mass || !com || !inertia || !inertia_inv) throw DgxError(DGX_E_INVALID, "NULL argument");
+    mesh_inertia(num_vertices, vertices, num_faces, faces, density, *mass, com, inertia, inertia_inv);
+  });
+}
+
+int dgx_mesh_bvh(int32_t num_vertices, const double* vertices, int32_t num_faces, const int32_t* faces, int32_t cap,
+                 double* boxes, int32_t* links, int32_t* face_order, int32_t* n_nodes) {
+  return guarded([&] {
+    if (!boxes || !links || !face_order || !n_nodes) throw DgxError(DGX_E_INVALID, "NULL argument");
+    MeshHost mh;
+    mesh_prepare(num_vertices, vertices, num_faces, faces, nullptr, mh);
+    const int n = static_cast<int>(mh.nodes.size());
+    if (n > cap) throw DgxError(DGX_E_INVALID, "cap < node count " + std::to_string(n));
+    for (int i = 0; i < n; ++i) {
+      const MeshNode& nd = mh.nodes[i];
+      for (int k = 0; k < 3; ++k) {
+        boxes[6 * i + k] = nd.lo[k];
+        boxes[6 * i + 3 + k] = nd.hi[k];
+      }
+      links[4 * i] = nd.left; links[4 * i + 1] = nd.right; links[4 * i + 2] = nd.first; links[4 * i + 3] = nd.count;
+    }
+    for (int i = 0; i < num_faces; ++i) face_order[i] = mh.faces[i].f;
+    *n_nodes = n;
   });
 }
 
@@ -452,7 +532,7 @@ static void run_fused(dgx_ctx* c, const dgx_hand* h, const dgx_object* o, int32_
   if (point_grads) cuda_check(cudaMemsetAsync(buf.point_grads, 0, 24ull * B * M * N, c->stream), "memset");
   int smem = 0;
   int grid = prepare(c, c->scratch, h, o, S, B, buf, smem);
-  cuda_check(launch_fused(h->k, o->k, o->kind, o->sphere, o->box, o->grid, S, P, buf, mode, grid, smem, c->stream),
+  cuda_check(launch_fused(h->k, o->k, o->sdf, S, P, buf, mode, grid, smem, c->stream),
              "fused_kernel");
   ++c->launches;
   s.finish(flags);
@@ -557,8 +637,7 @@ int dgx_optimize_multi(dgx_ctx* c, const dgx_hand* h, int32_t n_obj, const dgx_o
       buf.status = ds + off;
       int smem = 0;
       const int grid = prepare(c, sub.scratch, h, objs[i], S, Bi, buf, smem);
-      cuda_check(launch_fused(h->k, objs[i]->k, objs[i]->kind, objs[i]->sphere, objs[i]->box, objs[i]->grid, S, P,
-                              buf, kModeOpt, grid, smem, sub.stream),
+      cuda_check(launch_fused(h->k, objs[i]->k, objs[i]->sdf, S, P, buf, kModeOpt, grid, smem, sub.stream),
                  "fused_kernel");
       ++c->launches;
       off += Bi;

@@ -162,7 +162,7 @@ DGX_GHD_OUTLINE V3 quat_log(Q4 q) {
 /* SDF backends                                                              */
 /* ------------------------------------------------------------------------ */
 
-enum SdfKind : int { kSdfSphere = 1, kSdfBox = 2, kSdfGrid = 4 };
+enum SdfKind : int { kSdfSphere = 1, kSdfBox = 2, kSdfGrid = 4, kSdfMesh = 8 };
 
 // Query result in the object's canonical frame: the reference's PhongQuery
 // minus the mesh-only `flat` member (sdf.hpp:11-17).

@@ -2,7 +2,7 @@
 // C-ABI implementation (dgx_capi.cu).
 #pragma once
 
-#include "dgx_geom.h"
+#include "dgx_mesh.h"
 
 namespace dgx {
 
@@ -142,10 +142,22 @@ struct SmemLayout {
 #include <cuda_runtime.h>
 
 namespace dgx {
-cudaError_t launch_fused(const KHand& H, const KObj& O, int kind, const SphereSdf& sph, const BoxSdf& box,
-                         const GridSdf& grd, const KSim& S, const KOpt& P, const KBuf& buf, int mode, int grid,
-                         int smem, cudaStream_t st);
+// one object's SDF backend; `kind` selects the member
+struct SdfSet {
+  int kind;
+  SphereSdf sph;
+  BoxSdf box;
+  GridSdf grd;
+  MeshSdf mesh;
+};
+cudaError_t launch_fused(const KHand& H, const KObj& O, const SdfSet& sdf, const KSim& S, const KOpt& P,
+                         const KBuf& buf, int mode, int grid, int smem, cudaStream_t st);
 cudaError_t fused_occupancy(int kind, int M, int smem, int* blocks_per_sm);
+// out[n, 8] = rho - radius, grad (3), proxy (3), sign per point (MeshSdf::dilated,
+// sdf.cpp:62-67); within != 0: dilated_within (sdf.cpp:69-81), culled points
+// report sign 0 and rho = +inf
+cudaError_t launch_sdf_query(const SdfSet& sdf, int n, const double* r, double radius, int within, double* out,
+                             cudaStream_t st);
 cudaError_t launch_forward(const KHand& H, const double* q, double* out, int B, int grid, cudaStream_t st);
 cudaError_t launch_step(int J, const double* q, const double* g, double lr, double* out, int B, cudaStream_t st);
 }  // namespace dgx

@@ -102,6 +102,12 @@ __device__ __forceinline__ void eval_point(const Sdf& sdf, const SimEnv& e, int 
   pe.p = V3{e.px[i], e.py[i], e.pz[i]};
   pe.rel = pe.p - x;
   pe.rl = tmul(R, pe.rel) + e.O->com;
+  if (!record && sdf_culled(sdf, pe.rl, e.radius)) {  // dilated_within -> nullopt: inactive (sim.hpp:177-178)
+    pe.q = SdfQuery{kInf, V3{0.0, 0.0, 1.0}, pe.rl, 1};
+    pe.fb = false;
+    pe.rho_d = kInf;
+    return;
+  }
   pe.q = sdf.query(pe.rl);
   pe.fb = fabs(pe.q.rho) < kSurfaceEps;
   if (record && pe.fb) {
@@ -924,6 +930,7 @@ __device__ double run_sim(const Sdf& sdf, SimEnv& e, V3 v_m, bool record, bool m
     for (int i = lane; i < N; i += 32) {
       V3 p{e.px[i], e.py[i], e.pz[i]};
       V3 rl = tmul(Rf, p - x) + e.O->com;
+      if (sdf_culled(sdf, rl, e.radius)) continue;  // sim.hpp:204-205
       SdfQuery qq = sdf.query(rl);
       double rho = qq.rho - e.radius;
       if (rho < 0.0) mp = mp < -rho ? -rho : mp;
@@ -1436,36 +1443,66 @@ static cudaError_t launch_fused_t(const KHand& H, const KObj& O, const Sdf& sdf,
   return cudaGetLastError();
 }
 
-cudaError_t launch_fused(const KHand& H, const KObj& O, int kind, const SphereSdf& sph, const BoxSdf& box,
-                         const GridSdf& grd, const KSim& S, const KOpt& P, const KBuf& buf, int mode, int grid,
-                         int smem, cudaStream_t st) {
-  switch (kind) {
-    case kSdfSphere: return launch_fused_t(H, O, sph, S, P, buf, mode, grid, smem, st);
-    case kSdfBox: return launch_fused_t(H, O, box, S, P, buf, mode, grid, smem, st);
-    case kSdfGrid: return launch_fused_t(H, O, grd, S, P, buf, mode, grid, smem, st);
+cudaError_t launch_fused(const KHand& H, const KObj& O, const SdfSet& sdf, const KSim& S, const KOpt& P,
+                         const KBuf& buf, int mode, int grid, int smem, cudaStream_t st) {
+  switch (sdf.kind) {
+    case kSdfSphere: return launch_fused_t(H, O, sdf.sph, S, P, buf, mode, grid, smem, st);
+    case kSdfBox: return launch_fused_t(H, O, sdf.box, S, P, buf, mode, grid, smem, st);
+    case kSdfGrid: return launch_fused_t(H, O, sdf.grd, S, P, buf, mode, grid, smem, st);
+    case kSdfMesh: return launch_fused_t(H, O, sdf.mesh, S, P, buf, mode, grid, smem, st);
     default: return cudaErrorInvalidValue;
   }
 }
 
+template <class Sdf>
+static cudaError_t occupancy_t(int M, int smem, int* blocks_per_sm) {
+  cudaError_t e = cudaFuncSetAttribute(fused_kernel<Sdf>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+  if (e != cudaSuccess) return e;
+  return cudaOccupancyMaxActiveBlocksPerMultiprocessor(blocks_per_sm, fused_kernel<Sdf>, 32 * M, smem);
+}
+
 cudaError_t fused_occupancy(int kind, int M, int smem, int* blocks_per_sm) {
-  cudaError_t e;
   switch (kind) {
-    case kSdfSphere:
-      cudaFuncSetAttribute(fused_kernel<SphereSdf>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
-      e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(blocks_per_sm, fused_kernel<SphereSdf>, 32 * M, smem);
-      break;
-    case kSdfBox:
-      cudaFuncSetAttribute(fused_kernel<BoxSdf>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
-      e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(blocks_per_sm, fused_kernel<BoxSdf>, 32 * M, smem);
-      break;
-    case kSdfGrid:
-      cudaFuncSetAttribute(fused_kernel<GridSdf>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
-      e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(blocks_per_sm, fused_kernel<GridSdf>, 32 * M, smem);
-      break;
-    default:
-      return cudaErrorInvalidValue;
+    case kSdfSphere: return occupancy_t<SphereSdf>(M, smem, blocks_per_sm);
+    case kSdfBox: return occupancy_t<BoxSdf>(M, smem, blocks_per_sm);
+    case kSdfGrid: return occupancy_t<GridSdf>(M, smem, blocks_per_sm);
+    case kSdfMesh: return occupancy_t<MeshSdf>(M, smem, blocks_per_sm);
+    default: return cudaErrorInvalidValue;
   }
-  return e;
+}
+
+// one thread per point: MeshSdf::dilated / dilated_within (sdf.cpp:62-81) for
+// any backend
+template <class Sdf>
+__global__ void sdf_query_kernel(Sdf sdf, int n, const double* r, double radius, int within, double* out) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const V3 p{r[3 * i], r[3 * i + 1], r[3 * i + 2]};
+  double* o = out + 8 * static_cast<size_t>(i);
+  if (within && sdf_culled(sdf, p, radius)) {
+    o[0] = kInf;
+    for (int k = 1; k < 8; ++k) o[k] = 0.0;
+    return;
+  }
+  const SdfQuery q = sdf.query(p);
+  o[0] = q.rho - radius;
+  o[1] = q.grad.x; o[2] = q.grad.y; o[3] = q.grad.z;
+  o[4] = q.proxy.x; o[5] = q.proxy.y; o[6] = q.proxy.z;
+  o[7] = static_cast<double>(q.sign);
+}
+
+cudaError_t launch_sdf_query(const SdfSet& sdf, int n, const double* r, double radius, int within, double* out,
+                             cudaStream_t st) {
+  if (n <= 0) return cudaSuccess;
+  const int blocks = (n + 127) / 128;
+  switch (sdf.kind) {
+    case kSdfSphere: sdf_query_kernel<<<blocks, 128, 0, st>>>(sdf.sph, n, r, radius, within, out); break;
+    case kSdfBox: sdf_query_kernel<<<blocks, 128, 0, st>>>(sdf.box, n, r, radius, within, out); break;
+    case kSdfGrid: sdf_query_kernel<<<blocks, 128, 0, st>>>(sdf.grd, n, r, radius, within, out); break;
+    case kSdfMesh: sdf_query_kernel<<<blocks, 128, 0, st>>>(sdf.mesh, n, r, radius, within, out); break;
+    default: return cudaErrorInvalidValue;
+  }
+  return cudaGetLastError();
 }
 
 cudaError_t launch_forward(const KHand& H, const double* q, double* out, int B, int grid, cudaStream_t st) {

@@ -4,7 +4,8 @@ specified by the reference but not implemented there.
 Per candidate (deterministic per (seed, index), counter-based Philox):
   * a random direction d from the object's centre of mass; the surface point
     p_s is where the ray leaves the zero level set (analytic for primitives,
-    bisection on the trilinear grid for grids) and n is the outward normal;
+    bisection on the trilinear grid for grids, the last ray/triangle crossing
+    for meshes) and n is the outward normal;
   * palm position p_s + standoff * n, standoff = 1.2 x bounding radius;
   * palm approach axis (+z, assets.cpp:211) anti-parallel to n, roll about it
     uniform in [0, 2 pi);
@@ -53,6 +54,8 @@ def surface_points(o: ObjectDesc, d: np.ndarray) -> tuple[np.ndarray, np.ndarray
         n = np.zeros_like(d)
         n[np.arange(d.shape[0]), k] = np.sign(d[np.arange(d.shape[0]), k])
         return o.center[None, :] + t[:, None] * d, n
+    if o.kind == "mesh":
+        return _mesh_exit(o, d)
     lo = np.zeros(d.shape[0])
     hi = np.full(d.shape[0], float(np.max(o.spacing * (np.array(o.dims) - 1))))
     for _ in range(60):  # bisection on phi(com + t d) = 0
@@ -65,6 +68,35 @@ def surface_points(o: ObjectDesc, d: np.ndarray) -> tuple[np.ndarray, np.ndarray
     g = np.stack([_grid_phi(o, p + h * e) - _grid_phi(o, p - h * e) for e in np.eye(3)], axis=1)
     gn = np.linalg.norm(g, axis=1, keepdims=True)
     n = np.where(gn > 0, g / np.where(gn > 0, gn, 1.0), d)
+    return p, n
+
+
+def _mesh_exit(o: ObjectDesc, d: np.ndarray) -> tuple[np.ndarray, np.ndarray]:
+    """Last crossing of the ray com + t d with the mesh (Moller-Trumbore over
+    all faces) and that face's outward unit normal."""
+    V, F = o.vertices, o.faces
+    a, b, c = V[F[:, 0]], V[F[:, 1]], V[F[:, 2]]
+    e1, e2 = b - a, c - a
+    fn = np.cross(e1, e2)
+    fn /= np.linalg.norm(fn, axis=1, keepdims=True)
+    p = np.empty_like(d)
+    n = np.empty_like(d)
+    for k in range(d.shape[0]):
+        h = np.cross(d[k][None, :], e2)
+        det = np.sum(e1 * h, axis=1)
+        ok = np.abs(det) > 1e-18
+        f = np.where(ok, 1.0 / np.where(ok, det, 1.0), 0.0)
+        s = o.com[None, :] - a
+        u = f * np.sum(s * h, axis=1)
+        qv = np.cross(s, e1)
+        v = f * (qv @ d[k])
+        t = f * np.sum(e2 * qv, axis=1)
+        hit = ok & (u >= 0) & (v >= 0) & (u + v <= 1) & (t > 0)
+        if not np.any(hit):
+            raise ValueError("approach_init: ray from the COM misses the mesh")
+        j = np.flatnonzero(hit)[np.argmax(t[hit])]
+        p[k] = o.com + t[j] * d[k]
+        n[k] = fn[j]
     return p, n
 
 

@@ -8,9 +8,11 @@
   (hand.cpp:42-68, libstdc++ mt19937_64), exported once into ``assets/hands``
   by ``tools/export_assets.py``.
 * ``ObjectDesc`` — an SDF backend (analytic sphere / box, dense FP32 trilinear
-  grid; see csrc/dgx_geom.h) plus ``InertialData`` (rigid.hpp:8-13): mass,
-  COM, body inertia and its inverse. Inertia is analytic for primitives and a
-  voxel integral for grids.
+  grid; see csrc/dgx_geom.h; or the reference's triangle-mesh MeshSdf,
+  csrc/dgx_mesh.h) plus ``InertialData`` (rigid.hpp:8-13): mass, COM, body
+  inertia and its inverse. Inertia is analytic for primitives, a voxel
+  integral for grids and ``inertia_from_mesh`` (rigid.cpp:24-94, evaluated by
+  the C-ABI's dgx_mesh_inertia) for meshes.
 """
 from __future__ import annotations
 
@@ -99,7 +101,7 @@ class HandDesc:
 
 @dataclass
 class ObjectDesc:
-    kind: str                       # "sphere" | "box" | "grid"
+    kind: str                       # "sphere" | "box" | "grid" | "mesh"
     mass: float
     com: np.ndarray
     inertia_body: np.ndarray        # [3,3]
@@ -113,8 +115,14 @@ class ObjectDesc:
     inv_spacing: float = 0.0
     values: np.ndarray | None = None  # [nz, ny, nx] float32
     name: str = ""
+    vertices: np.ndarray | None = None        # mesh [V,3]
+    faces: np.ndarray | None = None           # mesh [F,3] int32, outward winding
+    vertex_normals: np.ndarray | None = None  # mesh [V,3] unit, or None: area-weighted (mesh.cpp:60-70)
+    alpha_phong: float = 0.75                 # MeshSdf alpha (sdf.hpp:24, losses.hpp:42)
 
     def bounding_radius(self) -> float:
+        if self.kind == "mesh":  # TriMesh::bounding_radius(com) (mesh.cpp:97-101)
+            return float(np.sqrt(np.max(np.sum((self.vertices - self.com[None, :]) ** 2, axis=1))))
         if self.kind == "sphere":
             return float(self.radius)
         if self.kind == "box":
@@ -235,3 +243,107 @@ def blob_grid(seed: int, radius=0.021, amplitude=0.5, res: int = 128, margin: fl
     ext = radius * (1.0 + amplitude) + margin
     return grid_object(lambda P: sdf_blob(P, radius, amplitude, seed), -np.full(3, ext), np.full(3, ext), res,
                        density, f"blob{seed}_{res}")
+
+
+# ---------------------------------------------------------------------------
+# triangle meshes (dg::TriMesh, mesh.hpp:15-45)
+# ---------------------------------------------------------------------------
+def mesh_object(vertices, faces, density: float = 1000.0, alpha_phong: float = 0.75, vertex_normals=None,
+                name: str = "mesh") -> ObjectDesc:
+    """dg::GraspObject(TriMesh, density, alpha_phong) (losses.hpp:42-43): the
+    mesh SDF plus inertia_from_mesh (rigid.cpp:24-94) through dgx_mesh_inertia,
+    which also validates the mesh as TriMesh::finalize (mesh.cpp:12-71)."""
+    import ctypes as C
+
+    from . import capi
+    V = np.ascontiguousarray(vertices, np.float64).reshape(-1, 3)
+    F = np.ascontiguousarray(faces, np.int32).reshape(-1, 3)
+    mass, com, I, Iinv = C.c_double(), np.zeros(3), np.zeros(9), np.zeros(9)
+    L = capi.load()
+    capi.check(L.dgx_mesh_inertia(V.shape[0], capi.ptr(V), F.shape[0], capi.ptr(F), float(density), C.byref(mass),
+                                  com.ctypes.data_as(capi._dp), I.ctypes.data_as(capi._dp),
+                                  Iinv.ctypes.data_as(capi._dp)))
+    vn = None if vertex_normals is None else np.ascontiguousarray(vertex_normals, np.float64).reshape(-1, 3)
+    return ObjectDesc("mesh", float(mass.value), com, I.reshape(3, 3), Iinv.reshape(3, 3), name=name, vertices=V,
+                      faces=F, vertex_normals=vn, alpha_phong=float(alpha_phong))
+
+
+def icosphere_mesh(radius: float = 0.025, subdivisions: int = 3) -> tuple[np.ndarray, np.ndarray]:
+    """Geodesic sphere: the regular icosahedron split 4:1 per level, vertices
+    pushed to the sphere (20 * 4^s faces; s = 3 -> 1280 faces, the size of
+    SURVEY config 1's mesh cross-check)."""
+    g = (1.0 + 5.0 ** 0.5) / 2.0
+    V = [np.array(v, np.float64) for v in
+         [(-1, g, 0), (1, g, 0), (-1, -g, 0), (1, -g, 0), (0, -1, g), (0, 1, g), (0, -1, -g), (0, 1, -g),
+          (g, 0, -1), (g, 0, 1), (-g, 0, -1), (-g, 0, 1)]]
+    F = [(0, 11, 5), (0, 5, 1), (0, 1, 7), (0, 7, 10), (0, 10, 11), (1, 5, 9), (5, 11, 4), (11, 10, 2),
+         (10, 7, 6), (7, 1, 8), (3, 9, 4), (3, 4, 2), (3, 2, 6), (3, 6, 8), (3, 8, 9), (4, 9, 5), (2, 4, 11),
+         (6, 2, 10), (8, 6, 7), (9, 8, 1)]
+    for _ in range(subdivisions):
+        mids: dict = {}
+
+        def mid(a, b):
+            k = (a, b) if a < b else (b, a)
+            if k not in mids:
+                V.append(0.5 * (V[a] + V[b]))
+                mids[k] = len(V) - 1
+            return mids[k]
+
+        nxt = []
+        for a, b, c in F:
+            ab, bc, ca = mid(a, b), mid(b, c), mid(c, a)
+            nxt += [(a, ab, ca), (b, bc, ab), (c, ca, bc), (ab, bc, ca)]
+        F = nxt
+    P = np.array(V)
+    n = np.sqrt(P[:, 0] * P[:, 0] + P[:, 1] * P[:, 1] + P[:, 2] * P[:, 2])
+    P = radius * (P / n[:, None])
+    return P, np.array(F, np.int32)
+
+
+def box_mesh(size=(0.04, 0.04, 0.04)) -> tuple[np.ndarray, np.ndarray]:
+    """Axis-aligned box centred at the origin, 12 outward-wound triangles."""
+    h = 0.5 * np.asarray(size, np.float64)
+    V = np.array([[sx * h[0], sy * h[1], sz * h[2]] for sz in (-1, 1) for sy in (-1, 1) for sx in (-1, 1)])
+    # vertex id = x + 2y + 4z (bits)
+    quads = [(0, 2, 3, 1), (4, 5, 7, 6), (0, 1, 5, 4), (2, 6, 7, 3), (0, 4, 6, 2), (1, 3, 7, 5)]
+    F = []
+    for a, b, c, d in quads:
+        F += [(a, b, c), (a, c, d)]
+    return V, np.array(F, np.int32)
+
+
+def load_obj(path: str) -> tuple[np.ndarray, np.ndarray]:
+    """ASCII OBJ v/f records as dg::load_obj (mesh.cpp:112-151): vertex index
+    before the first '/', negative indices relative, polygons fan-triangulated,
+    other records ignored."""
+    V, F = [], []
+    with open(path) as fh:
+        for ln, line in enumerate(fh, 1):
+            tok = line.split()
+            if not tok or tok[0].startswith("#"):
+                continue
+            if tok[0] == "v":
+                try:
+                    V.append([float(t) for t in tok[1:4]])
+                except ValueError:
+                    raise RuntimeError(f"{path}:{ln}: malformed vertex") from None
+                if len(V[-1]) != 3:
+                    raise RuntimeError(f"{path}:{ln}: malformed vertex")
+            elif tok[0] == "f":
+                idx = []
+                for t in tok[1:]:
+                    try:
+                        i = int(t.split("/")[0])
+                    except ValueError:
+                        raise RuntimeError(f"{path}:{ln}: malformed face index '{t}'") from None
+                    if i < 0:
+                        i = len(V) + i + 1
+                    if i <= 0 or i > len(V):
+                        raise RuntimeError(f"{path}:{ln}: face index out of range")
+                    idx.append(i - 1)
+                if len(idx) < 3:
+                    raise RuntimeError(f"{path}:{ln}: face with fewer than 3 vertices")
+                F += [(idx[0], idx[k], idx[k + 1]) for k in range(1, len(idx) - 1)]
+    if not F:
+        raise RuntimeError(f"{path}: no faces found")
+    return np.array(V, np.float64), np.array(F, np.int32)

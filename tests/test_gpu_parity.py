@@ -40,7 +40,10 @@ def ref_hand(oracle, name, variant="sm"):
 def make_obj(name):
     from paper_2306_08132_b200 import model
     return {"sphere25": lambda: model.sphere(0.025), "box40": lambda: model.box((0.04, 0.04, 0.04)),
-            "boxgrid64": lambda: model.box_grid(res=64), "cylgrid32": lambda: model.cylinder_grid(res=32)}[name]()
+            "boxgrid64": lambda: model.box_grid(res=64), "cylgrid32": lambda: model.cylinder_grid(res=32),
+            # triangle meshes: the oracle runs the UNMODIFIED reference MeshSdf
+            "ico25": lambda: model.mesh_object(*model.icosphere_mesh(0.025, 3)),
+            "boxmesh40": lambda: model.mesh_object(*model.box_mesh((0.04, 0.04, 0.04)))}[name]()
 
 
 class Case:
@@ -56,7 +59,8 @@ class Case:
         self.q = q
 
 
-COMBOS = [("barrett3", "sphere25"), ("pincher2", "box40"), ("allegro16", "boxgrid64"), ("barrett3", "cylgrid32")]
+COMBOS = [("barrett3", "sphere25"), ("pincher2", "box40"), ("allegro16", "boxgrid64"), ("barrett3", "cylgrid32"),
+          ("barrett3", "ico25"), ("pincher2", "boxmesh40")]
 
 
 @pytest.mark.parametrize("hand_name,obj_name", COMBOS)

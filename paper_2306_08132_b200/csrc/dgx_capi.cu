@@ -6,6 +6,7 @@
 #include <cmath>
 #include <cstdio>
 #include <cstring>
+#include <cstdlib>
 #include <stdexcept>
 #include <string>
 #include <vector>
@@ -65,11 +66,12 @@ struct DevBuf {
 
 // per-stream kernel scratch (correction logs, contact slots, link-sum spills)
 struct Scratch {
-  DevBuf corr, slots, ftg;
+  DevBuf corr, slots, ftg, mcache;
   void release() {
     corr.release();
     slots.release();
     ftg.release();
+    mcache.release();
   }
 };
 
@@ -144,7 +146,12 @@ int prepare(dgx_ctx* c, Scratch& sc, const dgx_hand* h, const dgx_object* o, KSi
   const int M = S.M;
   // longest adjoint segment whose staging still fits one CTA's shared memory
   S.seg_max = 0;
+  // mesh objects: two resident CTAs per SM (dgx_kernels.cu CtasPerSm) need
+  // the shorter adjoint staging
+  int seg_cap = o->kind == DGX_SDF_MESH ? 4 : kSegMaxCap;
+  if (const char* ev = std::getenv("DGX_SEGMAX")) seg_cap = std::max(1, std::min(kSegMaxCap, std::atoi(ev)));
   for (int seg : {kSegMaxCap, 8, 4, 2, 1}) {
+    if (seg > seg_cap) continue;
     if (SmemLayout(h->N, h->L, M, seg).total <= 227 * 1024) {
       S.seg_max = seg;
       break;
@@ -169,6 +176,11 @@ int prepare(dgx_ctx* c, Scratch& sc, const dgx_hand* h, const dgx_object* o, KSi
   buf.fric_order = buf.slot_of_point + per;
   sc.ftg.ensure(nws * 6 * static_cast<size_t>(h->L) * sizeof(double));
   buf.ft_global = static_cast<double*>(sc.ftg.p);
+  buf.mesh_cache = nullptr;
+  if (o->kind == DGX_SDF_MESH) {  // per point-sweep (face, sign) of the forward, read by the adjoint
+    sc.mcache.ensure(per * static_cast<size_t>(std::max(S.gs, 1)) * sizeof(int));
+    buf.mesh_cache = static_cast<int*>(sc.mcache.p);
+  }
   buf.cap_corr = c->cap_corr;
   buf.B = B;
   return grid;
@@ -402,6 +414,7 @@ int dgx_object_upload(dgx_ctx* c, const dgx_object_desc* d, dgx_object** out) {
         g.alpha = d->alpha_phong;
         mesh_ray_dirs(g.dir, g.inv);
         g.cull = 0.005;  // ContactSolver::kCullMargin (sim.hpp:213)
+        g.nfaces = d->num_faces;
         o->sdf.mesh = MeshSdf{static_cast<const MeshGeom*>(put(&g, sizeof(MeshGeom), rnd(sizeof(MeshGeom))))};
       } else {
         throw DgxError(DGX_E_UNSUPPORTED, "object: unknown SDF kind " + std::to_string(d->kind));

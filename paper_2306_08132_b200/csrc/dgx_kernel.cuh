@@ -109,6 +109,7 @@ struct KBuf {
   int* slot_of_point;   // [grid, M, N]
   int* fric_order;      // [grid, M, N]
   double* ft_global;    // [grid, M, L*6] adjoint link-sum spill buffers
+  int* mesh_cache;      // [grid, M, gs*N] mesh objects: forward (face << 1 | inside) per point-sweep
   int cap_corr;
   int B;
 };

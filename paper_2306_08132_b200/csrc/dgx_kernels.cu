@@ -31,6 +31,15 @@
 
 #include <cstdint>
 
+#ifdef DGX_PROFILE_REGIONS
+namespace dgx {
+__device__ unsigned long long g_prof[32];
+}
+// mesh traversal counters (lane 0 of each warp): 23 nearest queries, 24
+// nearest node pops, 25 ray casts, 26 ray node pops, 27 exact queries
+#define DGX_MESH_CNT(r, n) \
+  if ((threadIdx.x & 31) == 0) atomicAdd(&dgx::g_prof[r], static_cast<unsigned long long>(n))
+#endif
 #include "dgx_adjoint.cuh"
 #include "dgx_kernel.cuh"
 #include "dgx_sdf_fast.cuh"
@@ -42,7 +51,6 @@ constexpr unsigned kFull = 0xffffffffu;
 // Optional region timers (profiling builds only: -DDGX_PROFILE_REGIONS).
 // Lane 0 of each warp accumulates clock64() cycles / event counts per region.
 #ifdef DGX_PROFILE_REGIONS
-__device__ unsigned long long g_prof[32];
 #define PROF_T(v) const long long v = clock64()
 #define PROF_ACC(r, v) \
   if ((threadIdx.x & 31) == 0) atomicAdd(&g_prof[r], static_cast<unsigned long long>(clock64() - (v)))
@@ -85,7 +93,32 @@ struct SimEnv {
   const KObj* O;          // mass / COM / world inverse inertia (kernel parameter space)
   double radius, alpha, mu, dt;
   double* point_grads;    // debug, may be null
+  int* mcache;            // mesh: [gs*N] packed (face, sign) of the forward's query per point-sweep
 };
+
+// Classification of flattened position fpos (sweep*N + i) at r (FMA-built
+// r_local). Mesh objects: the forward's exact query is warm-started from the
+// point's face one sweep earlier and its (face, sign) recorded; the adjoint
+// re-evaluates that face only. Both see the same state and r, so they
+// reproduce the forward's decision and gradient exactly.
+template <class Sdf>
+__device__ __forceinline__ FastEval classify_fwd(const Sdf& sdf, const SimEnv& e, int, V3 r) {
+  return classify(sdf, r, e.radius);
+}
+template <class Sdf>
+__device__ __forceinline__ FastEval classify_bwd(const Sdf& sdf, const SimEnv& e, int, V3 r) {
+  return classify(sdf, r, e.radius);
+}
+__device__ __forceinline__ FastEval classify_fwd(const MeshSdf& m, const SimEnv& e, int fpos, V3 r) {
+  const int hint = fpos >= e.N ? (e.mcache[fpos - e.N] >> 1) : -1;
+  int packed;
+  const SdfQuery q = m.query_ws(r, hint, packed);
+  e.mcache[fpos] = packed;
+  return classify_query(q, r, e.radius);
+}
+__device__ __forceinline__ FastEval classify_bwd(const MeshSdf& m, const SimEnv& e, int fpos, V3 r) {
+  return classify_query(m.query_packed(r, e.mcache[fpos]), r, e.radius);
+}
 
 struct PointEval {
   V3 p, rel, rl;
@@ -334,11 +367,12 @@ struct LeakGeo {
 };
 
 template <class Sdf>
-__device__ __forceinline__ void leak_geo(const Sdf& sdf, const SimEnv& e, int i, V3 xk, const M3& Rk, LeakGeo& L) {
+__device__ __forceinline__ void leak_geo(const Sdf& sdf, const SimEnv& e, int i, int fpos, V3 xk, const M3& Rk,
+                                         LeakGeo& L) {
   L.p = V3{e.px[i], e.py[i], e.pz[i]};
   L.rel = L.p - xk;
   const V3 rl = ftmul(Rk, L.rel) + e.O->com;
-  FastEval fe = classify(sdf, rl, e.radius);
+  FastEval fe = classify_bwd(sdf, e, fpos, rl);
   L.sg = 1.0;
   L.contrib = false;
   if (fe.cls == 0) {  // near the decision boundary: the exact (bit-exact) query decides
@@ -460,7 +494,7 @@ __device__ void process_run(const Sdf& sdf, SimEnv& e, int lo, int hi, V3 xk, Q4
     int i = cnt > 0 ? (shi - 1) % N : 0;
     for (int k = 0; k < cnt; ++k) {
       LeakGeo L;
-      leak_geo(sdf, e, i, xk, Rk, L);
+      leak_geo(sdf, e, i, shi - 1 - k, xk, Rk, L);
       double c1 = 0.0, c0 = 0.0;
       if (!(L.contrib && leak_coef(e, L, G, c1, c0))) {
         c1 = 0.0;
@@ -798,7 +832,7 @@ __device__ double run_sim(const Sdf& sdf, SimEnv& e, V3 v_m, bool record, bool m
       const int ic = i < N ? i : N - 1;
       const V3 p{e.px[ic], e.py[ic], e.pz[ic]};
       const V3 rl = ftmul(R, p - x) + e.O->com;
-      cls[h] = i < N ? classify(sdf, rl, e.radius).cls : 1;
+      cls[h] = i < N ? classify_fwd(sdf, e, sweep * N + i, rl).cls : 1;
     }
     const unsigned cand0 = __ballot_sync(kFull, cls[0] <= 0);
     const unsigned cand1 = __ballot_sync(kFull, cls[1] <= 0);
@@ -866,6 +900,7 @@ __device__ double run_sim(const Sdf& sdf, SimEnv& e, V3 v_m, bool record, bool m
     if (pos >= N) { pos = 0; ++sweep; }
   }
 
+  __syncwarp();  // order the forward's mesh-cache stores before the adjoint's loads
   PROF_ACC(0, tfwd);
   PROF_T(tfr);
   // ---- friction (sim.hpp:188-196), active slots in point order -------------
@@ -1144,8 +1179,20 @@ __device__ __forceinline__ void fk_adjoint(const KHand& H, const double* qv, con
   }
 }
 
+// CTAs per SM the register budget is sized for: mesh objects spend ~99% of
+// the time in out-of-line BVH traversals (latency-bound), so their instance
+// trades adjoint-side spills for a second resident CTA
 template <class Sdf>
-__global__ void __launch_bounds__(224, 1) fused_kernel(KHand H, const __grid_constant__ KObj O, Sdf sdf, KSim S, KOpt P, KBuf buf, int mode) {
+struct CtasPerSm {
+  static constexpr int value = 1;
+};
+template <>
+struct CtasPerSm<MeshSdf> {
+  static constexpr int value = 2;
+};
+
+template <class Sdf>
+__global__ void __launch_bounds__(224, CtasPerSm<Sdf>::value) fused_kernel(KHand H, const __grid_constant__ KObj O, Sdf sdf, KSim S, KOpt P, KBuf buf, int mode) {
   extern __shared__ __align__(16) unsigned char smem[];
   const SmemLayout lay(H.N, H.L, S.M, S.seg_max);
   double* px = reinterpret_cast<double*>(smem + lay.off_px);
@@ -1190,6 +1237,7 @@ __global__ void __launch_bounds__(224, 1) fused_kernel(KHand H, const __grid_con
   e.mu = S.mu;
   e.dt = S.dt;
   e.point_grads = nullptr;
+  e.mcache = buf.mesh_cache ? buf.mesh_cache + wslot * static_cast<size_t>(S.gs) * N : nullptr;
 
   const int k0 = mode == kModeOpt ? P.k_begin : 0;
   const int k1 = mode == kModeOpt ? P.k_end : 1;

@@ -30,6 +30,11 @@ namespace dgx {
 constexpr int kMeshStack = 48;  // traversal stack; the builder rejects deeper trees (bvh.cpp uses 128)
 constexpr double kInf = __builtin_huge_val();
 
+#if !defined(DGX_MESH_CNT) || !defined(__CUDA_ARCH__)
+#undef DGX_MESH_CNT
+#define DGX_MESH_CNT(r, n)
+#endif
+
 struct alignas(16) MeshNode {    // 64 B
   double lo[3], hi[3];
   int left, right;   // internal: children; leaf: -1
@@ -124,6 +129,26 @@ DGX_GHD MeshNode load_node(const MeshNode* p) {
 #endif
 }
 
+DGX_GHD double node_lb2(const MeshNode* p, V3 r) {
+#if defined(__CUDA_ARCH__)
+  const double2* q = reinterpret_cast<const double2*>(p);
+  const double2 a = __ldg(q), b = __ldg(q + 1), c = __ldg(q + 2);
+  const double lo[3] = {a.x, a.y, b.x}, hi[3] = {b.y, c.x, c.y};
+  return box_dist2(lo, hi, r);
+#else
+  return box_dist2(p->lo, p->hi, r);
+#endif
+}
+
+DGX_GHD void node_links(const MeshNode* p, int& left, int& right, int& first, int& count) {
+#if defined(__CUDA_ARCH__)
+  const int4 d = __ldg(reinterpret_cast<const int4*>(p) + 3);
+  left = d.x; right = d.y; first = d.z; count = d.w;
+#else
+  left = p->left; right = p->right; first = p->first; count = p->count;
+#endif
+}
+
 struct FaceV {
   V3 a, b, c;
   int f;
@@ -170,11 +195,73 @@ struct MeshGeom {
   double dir[3][3];      // ray directions kRayDir0, kRayDir1, third fixed direction (bvh.cpp:143-144, 250)
   double inv[3][3];      // 1 / dir, per component (bvh.cpp:219)
   double cull;           // ContactSolver::kCullMargin (sim.hpp:213)
+  int nfaces;
 
   DGX_GHD MeshNode node(int i) const { return load_node(nodes + i); }
 
+  // closest point on face f (mesh.v(f, 0..2), bvh.cpp:193)
+  DGX_GHD void face_closest(V3 r, int f, FlatPoint& sp) const {
+    const int i0 = load_i(tri + 3 * f), i1 = load_i(tri + 3 * f + 1), i2 = load_i(tri + 3 * f + 2);
+    closest_on_triangle(r, load_v3(vx + 3 * i0), load_v3(vx + 3 * i1), load_v3(vx + 3 * i2), sp);
+    sp.face = f;
+  }
+
+  // Solver-path nearest face: the same argmin (dist2, then lowest face id) as
+  // nearest(), seeded with a hint face (the point's face one sweep earlier;
+  // any id, or -1) so the first prune bound is already tight. Pruning keeps a
+  // relative + absolute slack over the rounded triangle distances, so no box
+  // holding the argmin is skipped; the result is the exact argmin over all
+  // faces (what the reference's traversal returns barring its own rounding
+  // ties at a box boundary).
+  DGX_GHD void nearest_ws(V3 r, int hint, FlatPoint& best) const {
+    double best2 = kInf;
+    best.face = -1;
+    if (hint >= 0 && hint < nfaces) {
+      face_closest(r, hint, best);
+      best2 = best.dist2;
+    }
+    // stack of (node, its lower bound computed when its parent was expanded)
+    int stack[kMeshStack];
+    double sb[kMeshStack];
+    int top = 0;
+    stack[top] = 0;
+    sb[top++] = node_lb2(nodes, r);
+    DGX_MESH_CNT(23, 1);
+    while (top > 0) {
+      --top;
+      const double lim = best2 * (1.0 + 1e-10) + 1e-24;
+      if (sb[top] > lim) continue;
+      const int id = stack[top];
+      DGX_MESH_CNT(24, 1);
+      int left, right, first, count;
+      node_links(nodes + id, left, right, first, count);
+      if (left < 0) {
+        for (int i = first; i < first + count; ++i) {
+          const FaceV F = load_face(faces + i);
+          FlatPoint sp;
+          closest_on_triangle(r, F.a, F.b, F.c, sp);
+          if (sp.dist2 < best2 || (sp.dist2 == best2 && (best.face < 0 || F.f < best.face))) {
+            best2 = sp.dist2;
+            best = sp;
+            best.face = F.f;
+          }
+        }
+      } else {
+        const double dl = node_lb2(nodes + left, r), dr = node_lb2(nodes + right, r);
+        if (dl <= dr) {  // nearer child on top
+          if (dr <= lim) { stack[top] = right; sb[top++] = dr; }
+          if (dl <= lim) { stack[top] = left; sb[top++] = dl; }
+        } else {
+          if (dl <= lim) { stack[top] = left; sb[top++] = dl; }
+          if (dr <= lim) { stack[top] = right; sb[top++] = dr; }
+        }
+      }
+    }
+  }
+
   // Bvh::closest_point_within (bvh.cpp:170-215); limit2 = max_dist^2 or +inf.
-  // Returns false when no face is within the bound.
+  // Returns false when no face is within the bound. Same traversal order and
+  // box pruning as the reference.
   DGX_GHD bool nearest(V3 r, double limit2, FlatPoint& best) const {
     double best2 = limit2;
     best.face = -1;
@@ -183,9 +270,11 @@ struct MeshGeom {
     const MeshNode root = node(0);
     if (box_dist2(root.lo, root.hi, r) > best2) return false;
     stack[top++] = 0;
+    DGX_MESH_CNT(23, 1);
     while (top > 0) {
       const int id = stack[--top];
       const MeshNode nd = node(id);
+      DGX_MESH_CNT(24, 1);
       if (box_dist2(nd.lo, nd.hi, r) > best2) continue;  // e.d2 > best2 (same value as at push time)
       if (nd.left < 0) {
         for (int i = nd.first; i < nd.first + nd.count; ++i) {
@@ -235,8 +324,10 @@ struct MeshGeom {
     int stack[kMeshStack];
     int top = 0;
     stack[top++] = 0;
+    DGX_MESH_CNT(25, 1);
     while (top > 0) {
       const MeshNode nd = node(stack[--top]);
+      DGX_MESH_CNT(26, 1);
       if (!ray_box(o, inv[k], nd.lo, nd.hi)) continue;
       if (nd.left < 0) {
         for (int i = nd.first; i < nd.first + nd.count; ++i) {
@@ -279,8 +370,13 @@ struct MeshGeom {
     return (c % 2 == 0) ? 1 : -1;
   }
 
-  // MeshSdf::phong(r, alpha_) (sdf.cpp:31-60) from a flat closest point
   DGX_GHD SdfQuery phong(V3 r, const FlatPoint& fl) const {
+    return phong_signed(r, fl, dsqrt(fl.dist2) < kSurfaceEps ? 1 : sign_at(r));
+  }
+
+  // MeshSdf::phong(r, alpha_) (sdf.cpp:31-60) from a flat closest point and
+  // the sign of sdf.cpp:47
+  DGX_GHD SdfQuery phong_signed(V3 r, const FlatPoint& fl, int sign) const {
     const int t[3] = {load_i(tri + 3 * fl.face), load_i(tri + 3 * fl.face + 1), load_i(tri + 3 * fl.face + 2)};
     const V3 rstar = fl.pos;
     SdfQuery q;
@@ -295,8 +391,7 @@ struct MeshGeom {
       const V3 blend = fl.bary.x * pp[0] + fl.bary.y * pp[1] + fl.bary.z * pp[2];
       q.proxy = (1.0 - alpha) * rstar + alpha * blend;
     }
-    const double flat_d = dsqrt(fl.dist2);
-    q.sign = flat_d < kSurfaceEps ? 1 : sign_at(r);
+    q.sign = sign;
     const V3 delta = r - q.proxy;
     const double d = norm(delta);
     q.rho = static_cast<double>(q.sign) * d;
@@ -310,9 +405,28 @@ struct MeshGeom {
   }
 
   DGX_GHD SdfQuery query(V3 r) const {
+    DGX_MESH_CNT(27, 1);
     FlatPoint fl;
     nearest(r, kInf, fl);
     return phong(r, fl);
+  }
+
+  // solver forward: query via nearest_ws; *packed = face << 1 | (sign < 0)
+  DGX_GHD SdfQuery query_ws(V3 r, int hint, int& packed) const {
+    DGX_MESH_CNT(27, 1);
+    FlatPoint fl;
+    nearest_ws(r, hint, fl);
+    const SdfQuery q = phong(r, fl);
+    packed = (fl.face << 1) | (q.sign < 0 ? 1 : 0);
+    return q;
+  }
+
+  // solver adjoint: the forward's query at the same r re-evaluated from its
+  // packed (face, sign) — one triangle instead of a traversal + ray cast
+  DGX_GHD SdfQuery query_packed(V3 r, int packed) const {
+    FlatPoint fl;
+    face_closest(r, packed >> 1, fl);
+    return phong_signed(r, fl, (packed & 1) ? -1 : 1);
   }
 
   // dilated_within's cull (sdf.cpp:69-77): true = nullopt (sample culled)
@@ -331,6 +445,8 @@ struct MeshSdf {
 #if defined(__CUDACC__)
   __device__ SdfQuery query(V3 r) const;
   __device__ bool culled(V3 r, double radius) const;
+  __device__ SdfQuery query_ws(V3 r, int hint, int& packed) const;
+  __device__ SdfQuery query_packed(V3 r, int packed) const;
 #endif
 };
 
@@ -339,7 +455,19 @@ static __device__ __noinline__ SdfQuery mesh_query(const MeshGeom* __restrict__ 
 static __device__ __noinline__ bool mesh_culled(const MeshGeom* __restrict__ g, V3 r, double radius) {
   return g->culled(r, radius);
 }
+static __device__ __noinline__ SdfQuery mesh_query_ws(const MeshGeom* __restrict__ g, V3 r, int hint, int* packed) {
+  return g->query_ws(r, hint, *packed);
+}
+static __device__ __noinline__ SdfQuery mesh_query_packed(const MeshGeom* __restrict__ g, V3 r, int packed) {
+  return g->query_packed(r, packed);
+}
 __device__ __forceinline__ SdfQuery MeshSdf::query(V3 r) const { return mesh_query(g, r); }
+__device__ __forceinline__ SdfQuery MeshSdf::query_ws(V3 r, int hint, int& packed) const {
+  return mesh_query_ws(g, r, hint, &packed);
+}
+__device__ __forceinline__ SdfQuery MeshSdf::query_packed(V3 r, int packed) const {
+  return mesh_query_packed(g, r, packed);
+}
 __device__ __forceinline__ bool MeshSdf::culled(V3 r, double radius) const { return mesh_culled(g, r, radius); }
 #endif
 

@@ -20,17 +20,22 @@ NAMES = {0: "forward sweeps (incl. corrections)", 1: "  apply_correction", 2: "f
          11: "correction adjoints", 12: "run_sim total", 13: "scheduler: claim / spin",
          14: "scheduler: finalize (losses, FK adjoint, Adam)", 15: "scheduler: FK / load next"}
 COUNTS = {16: "forward chunk iterations", 17: "forward candidate lanes", 18: "adjoint blocks", 19: "runs",
-          20: "forward corrections tried", 21: "frictions applied", 22: "sims"}
+          20: "forward corrections tried", 21: "frictions applied", 22: "sims",
+          23: "mesh nearest queries (lane 0)", 24: "mesh nearest node pops (lane 0)",
+          25: "mesh ray casts (lane 0)", 26: "mesh ray node pops (lane 0)", 27: "mesh exact queries (lane 0)"}
 
 
 def main():
     hand_name = sys.argv[1] if len(sys.argv) > 1 else "allegro16"
     B = int(sys.argv[2]) if len(sys.argv) > 2 else 512
+    obj_name = sys.argv[3] if len(sys.argv) > 3 else "boxgrid64"
     L = capi.load()
     L.dgx_prof_read.argtypes = [C.POINTER(C.c_ulonglong), C.c_int, C.c_int]
     ctx = api.Context(0)
     hd = model.HandDesc.asset(hand_name)
-    od = model.box_grid(res=64)
+    od = {"boxgrid64": lambda: model.box_grid(res=64),
+          "ico3": lambda: model.mesh_object(*model.icosphere_mesh(0.025, 3)),
+          "sphere": lambda: model.sphere(0.025)}[obj_name]()
     hand, obj = api.Hand(ctx, hd), api.GraspObject(ctx, od)
     q = init.approach_init(od, hd, B, seed=17)
     proto, w = api.StabilityProtocol.standard(), api.LossWeights()
@@ -44,11 +49,12 @@ def main():
     v = np.array(list(buf), dtype=np.float64)
     ci = B * 1
     tot = v[12]
-    print(f"{hand_name} B={B}: per candidate-iteration (7 sims), cycles summed over warps")
+    print(f"{hand_name} x {obj_name} B={B}: per candidate-iteration (7 sims), cycles summed over warps")
     for k, n in NAMES.items():
         print(f"  {n:38s} {v[k] / ci:12.0f} cyc  {100 * v[k] / tot:5.1f}%")
     for k, n in COUNTS.items():
-        print(f"  {n:38s} {v[k] / ci:12.1f} per cand-iter")
+        if v[k]:
+            print(f"  {n:38s} {v[k] / ci:12.1f} per cand-iter")
 
 
 if __name__ == "__main__":

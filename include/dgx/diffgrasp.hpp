@@ -12,12 +12,17 @@
 // plus batched overloads over std::span<const dg::HandConfig> and the fused
 // synthesis loop dgx::optimize (the reference has none).
 //
-// The object: the reference's GraspObject is mesh-only; the B200 path takes an
-// analytic / grid SDF (dgx::SdfSpec) and the object's dg::InertialData
-// (rigid.hpp:8-13), e.g. taken from a dg::GraspObject built on the same shape.
+// The object: dgx::Object(rt, const dg::GraspObject&) takes the reference's
+// own object (losses.hpp:38-44) unchanged: its TriMesh (vertices, faces,
+// vertex normals), MeshSdf alpha_phong and InertialData; queries are the
+// reference's MeshSdf ones (csrc/dgx_mesh.h). dgx::Object(rt, SdfSpec,
+// InertialData) adds the analytic / grid backends the reference lacks.
+//   dg::MeshSdf::dilated / dilated_within        sdf.hpp:41-45   -> dgx::dilated / dilated_within
 #pragma once
 
 #include <cstdint>
+#include <limits>
+#include <optional>
 #include <span>
 #include <stdexcept>
 #include <string>
@@ -170,6 +175,31 @@ class Object {
     for (int k = 0; k < 9; ++k) d.inertia_body_inv[k] = in.inertia_body_inv.m[k];
     detail::check(dgx_object_upload(rt.get(), &d, &o_));
   }
+  // dg::GraspObject (mesh SDF + InertialData) as the reference builds it
+  Object(Runtime& rt, const dg::GraspObject& go) {
+    const dg::TriMesh& m = go.sdf.mesh();
+    std::vector<double> V(3 * m.num_vertices()), VN(3 * m.num_vertices());
+    std::vector<int32_t> F(3 * m.num_faces());
+    for (std::size_t i = 0; i < m.num_vertices(); ++i) {
+      V[3 * i] = m.vertices[i].x; V[3 * i + 1] = m.vertices[i].y; V[3 * i + 2] = m.vertices[i].z;
+      VN[3 * i] = m.vertex_normals[i].x; VN[3 * i + 1] = m.vertex_normals[i].y; VN[3 * i + 2] = m.vertex_normals[i].z;
+    }
+    for (std::size_t f = 0; f < m.num_faces(); ++f)
+      for (int k = 0; k < 3; ++k) F[3 * f + k] = m.faces[f][k];
+    dgx_object_desc d{};
+    d.kind = DGX_SDF_MESH;
+    d.num_vertices = static_cast<int32_t>(m.num_vertices());
+    d.num_faces = static_cast<int32_t>(m.num_faces());
+    d.vertices = V.data();
+    d.faces = F.data();
+    d.vertex_normals = VN.data();
+    d.alpha_phong = go.sdf.alpha_phong();
+    const dg::InertialData& in = go.inertial;
+    d.mass = in.mass;
+    d.com[0] = in.com.x; d.com[1] = in.com.y; d.com[2] = in.com.z;
+    for (int k = 0; k < 9; ++k) d.inertia_body_inv[k] = in.inertia_body_inv.m[k];
+    detail::check(dgx_object_upload(rt.get(), &d, &o_));
+  }
   ~Object() { dgx_object_free(o_); }
   Object(const Object&) = delete;
   Object& operator=(const Object&) = delete;
@@ -178,6 +208,36 @@ class Object {
  private:
   dgx_object* o_ = nullptr;
 };
+
+// ---- SDF queries (MeshSdf::dilated / dilated_within, sdf.hpp:41-45) ----------
+// Batched over object-frame points; PhongQuery::flat is not reported.
+inline std::vector<std::optional<dg::PhongQuery>> sdf_queries(Runtime& rt, const Object& obj,
+                                                              std::span<const dg::Vec3> r, double radius,
+                                                              bool within) {
+  std::vector<double> p(3 * r.size()), out(8 * r.size());
+  for (std::size_t i = 0; i < r.size(); ++i) { p[3 * i] = r[i].x; p[3 * i + 1] = r[i].y; p[3 * i + 2] = r[i].z; }
+  detail::check(dgx_sdf_query_batch(rt.get(), obj.get(), static_cast<int32_t>(r.size()), p.data(), radius,
+                                    within ? 1 : 0, out.data(), 0));
+  std::vector<std::optional<dg::PhongQuery>> res(r.size());
+  for (std::size_t i = 0; i < r.size(); ++i) {
+    const double* o = out.data() + 8 * i;
+    if (o[7] == 0.0) continue;  // culled (nullopt)
+    dg::PhongQuery q;
+    q.rho = o[0];
+    q.grad = {o[1], o[2], o[3]};
+    q.smoothed_point = {o[4], o[5], o[6]};
+    q.sign = static_cast<int>(o[7]);
+    res[i] = q;
+  }
+  return res;
+}
+inline dg::PhongQuery dilated(Runtime& rt, const Object& obj, const dg::Vec3& r, double radius) {
+  return *sdf_queries(rt, obj, std::span<const dg::Vec3>(&r, 1), radius, false)[0];
+}
+// with the solver's cull margin (sim.hpp:213)
+inline std::optional<dg::PhongQuery> dilated_within(Runtime& rt, const Object& obj, const dg::Vec3& r, double radius) {
+  return sdf_queries(rt, obj, std::span<const dg::Vec3>(&r, 1), radius, true)[0];
+}
 
 // ---- reference signatures (batch of one) ------------------------------------
 

@@ -1,6 +1,9 @@
 """Measure BASELINE.json configs 1, 3, 4, 5 on one B200 (config 2 is bench.py's
 headline). Writes one JSON record per line to stdout.
 
+  config1_mesh  the same on the reference's own representation: the
+           make_icosphere(0.025, 3) triangle mesh, GPU mesh backend vs the
+           UNMODIFIED reference (real MeshSdf) on the CPU.
   config1  barrett3 on the analytic sphere (R 25 mm), 64 candidates, 200 iterations:
            FULL run on the GPU, grasps/s, plus the reference CPU full run on a
            16-candidate subset and a distribution comparison (final loss /
@@ -97,6 +100,52 @@ def config1():
                 mean_final_loss_gpu=float(eg[:, 0].mean()), mean_final_loss_ref=float(er[:, 0].mean()))
 
 
+def config1_mesh():
+    """Config 1's mesh cross-check: the paper's representation,
+    make_icosphere(0.025, 3) (1280 faces) through the UNMODIFIED reference
+    MeshSdf on the CPU vs the GPU mesh backend, same mesh (bit-identical
+    vertices), same hand, same initial configurations."""
+    from scipy.stats import ks_2samp
+    from oracle import ref
+    hd = model.HandDesc.asset("barrett3")
+    od = model.mesh_object(*model.icosphere_mesh(0.025, 3))
+    ctx = api.Context(0)
+    hand, obj = api.Hand(ctx, hd), api.GraspObject(ctx, od)
+    B, K = 64, 200
+    q0 = init.approach_init(od, hd, B, seed=1)
+    ms, qf, bad = timed_opt(ctx, [obj], hand, hd, [q0], K, 1, K)
+    ci_s = B * (K - 1) / (ms * 1e-3)
+    # throughput at a full-GPU batch
+    Bw = 2048
+    qw = init.approach_init(od, hd, Bw, seed=2)
+    msw, _, badw = timed_opt(ctx, [obj], hand, hd, [qw], 500, 1, 3)
+    rh = ref.RefHand.barrett3(variant="glibc")
+    ro = ref.RefObject.icosphere(0.025, 3, variant="glibc")
+    sub = 16
+    t0 = time.perf_counter()
+    r = ref.optimize(ro, rh, q0[:sub], ref.default_params(), iters=K)
+    cpu_s = time.perf_counter() - t0
+    proto = api.StabilityProtocol.standard()
+    eg, sg, _ = api.evaluate_losses(ctx, obj, hand, qf, proto, api.SimParams())
+    er, sr = [], []
+    for b in range(sub):
+        er.append(ref.evaluate_losses(ro, rh, r["q"][b], ref.default_params()))
+        sr.append([ref.sim_forward(ro, rh, r["q"][b], m, ref.default_params())[1] for m in range(7)])
+    er, sr = np.array(er), np.array(sr)
+    return dict(config="config1_mesh",
+                workload="barrett3 (N=1999) on make_icosphere(0.025, 3) mesh (1280 faces, alpha_phong 0.75), "
+                         "64 candidates, 200 iterations",
+                gpu_candidate_iterations_per_s=ci_s, gpu_full_run_s=ms * 1e-3 * K / (K - 1),
+                gpu_grasps_per_s=B / (ms * 1e-3 * K / (K - 1)), failed=bad,
+                gpu_candidate_iterations_per_s_B2048=Bw * 2 / (msw * 1e-3), failed_B2048=badw,
+                cpu_reference_candidate_iterations_per_s=sub * K / cpu_s, cpu_threads=os.cpu_count(),
+                cpu_subset=sub, cpu_reference="unmodified reference (glibc libm, real MeshSdf)",
+                ks_final_stable_loss_p=float(ks_2samp(eg[:, 0], er[:, 0]).pvalue),
+                ks_contacts_p=float(ks_2samp(sg[:, :, 0].sum(1), sr[:, :, 0].sum(1)).pvalue),
+                ks_penetration_p=float(ks_2samp(sg[:, :, 3].max(1), sr[:, :, 3].max(1)).pvalue),
+                mean_final_loss_gpu=float(eg[:, 0].mean()), mean_final_loss_ref=float(er[:, 0].mean()))
+
+
 def config3():
     hd = model.HandDesc.asset("shadow22_dense")
     od = model.blob_grid(seed=3, res=128)
@@ -139,7 +188,7 @@ def config5():
 
 
 def main():
-    which = sys.argv[1:] or ["config1", "config3", "config4", "config5"]
+    which = sys.argv[1:] or ["config1", "config1_mesh", "config3", "config4", "config5"]
     for w in which:
         t = time.time()
         rec = globals()[w]()

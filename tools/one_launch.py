@@ -10,8 +10,10 @@ from paper_2306_08132_b200 import api, init, model  # noqa: E402
 B = int(sys.argv[1]) if len(sys.argv) > 1 else 148
 dev = torch.device("cuda", 0)
 ctx = api.Context(0)
-hd = model.HandDesc.asset("allegro16")
-od = model.box_grid(res=64)
+hd = model.HandDesc.asset(sys.argv[2] if len(sys.argv) > 2 else "allegro16")
+OBJ = sys.argv[3] if len(sys.argv) > 3 else "boxgrid64"
+od = {"boxgrid64": lambda: model.box_grid(res=64),
+      "ico3": lambda: model.mesh_object(*model.icosphere_mesh(0.025, 3))}[OBJ]()
 hand, obj = api.Hand(ctx, hd), api.GraspObject(ctx, od)
 D = 6 + hd.num_joints
 q = torch.tensor(init.approach_init(od, hd, B, seed=17), device=dev)

@@ -13,6 +13,8 @@
  *                              + InertialData (rigid.hpp:8-13)
  *   dgx_sdf_query_batch        MeshSdf::dilated / dilated_within (sdf.hpp:41-45)
  *   dgx_mesh_inertia           dg::inertia_from_mesh (rigid.cpp:24-94)
+ *   dgx_drop_batch             dg::step_on_table (sim.cpp:14-94) + kinetic_energy
+ *                              (sim.cpp:8-12), iterated per scene
  *   dgx_forward_batch          HandModel::forward(const HandConfig&) (hand.hpp:86)
  *   dgx_loss_gradient_batch    dg::loss_gradient (losses.hpp:126-127, losses.cpp:20-66)
  *   dgx_evaluate_losses_batch  dg::evaluate_losses (losses.hpp:119-121, losses.cpp:7-18)
@@ -108,7 +110,24 @@ typedef struct {
   const double* vertex_normals;  /* [V,3] unit (TriMesh::set_vertex_normals), or NULL:
                                     area-weighted face normals (mesh.cpp:60-70) */
   double alpha_phong;            /* in [0,1] (sdf.cpp:19) */
+  double inertia_body[9];        /* InertialData::inertia_body (rigid.hpp:11); needed by
+                                    dgx_drop_batch (kinetic_energy, sim.cpp:8-12) only */
 } dgx_object_desc;
+
+/* scene drop (step_on_table, sim.cpp:14-94, iterated by a driver) */
+typedef struct {
+  double dt;               /* SimParams::dt */
+  double mu;               /* SimParams::mu */
+  int32_t gs_iters;        /* SimParams::gs_iters */
+  int32_t measure_residual;/* SolveStats::measure_residual: max table penetration */
+  double gravity[3];       /* SimParams::gravity (e.g. 0, 0, -9.81) */
+  int32_t max_steps;       /* step cap */
+  int32_t min_steps;       /* never stop before this many steps */
+  double ke_tol;           /* at rest: settle_steps consecutive contact steps with
+                              kinetic_energy < ke_tol (J) */
+  int32_t record_every;    /* > 0 with traj: state after every record_every-th step */
+  int32_t settle_steps;    /* >= 1 */
+} dgx_drop_params;
 
 typedef struct {
   double dt;               /* SimParams::dt (sim.hpp:34) */
@@ -205,6 +224,19 @@ int dgx_optimize_multi(dgx_ctx* ctx, const dgx_hand* hand, int32_t n_obj, const 
 int dgx_debug_sims(dgx_ctx* ctx, const dgx_hand* hand, const dgx_object* obj, int32_t B, const double* q,
                    const dgx_params* params, double* sim_res, double* sim_grads, double* point_grads,
                    int32_t* status, uint32_t flags);
+
+/* Batched scene drop: each row of state_in
+   [B,13] (dg::RigidState: x(3), theta w,x,y,z (4), xdot(3), thetadot(3)) of a
+   MESH object is advanced by step_on_table (sim.cpp:14-94) until settle_steps
+   consecutive steps with contact leave kinetic_energy (sim.cpp:8-12) below
+   ke_tol, or max_steps.
+   state_out [B,13], steps [B] (steps taken), ke [B] (final kinetic energy),
+   stats [B,4] (active_contacts, corrections, singular_skipped,
+   max_penetration) of one SolveStats shared by all steps (may be NULL), traj
+   [B, max_steps/record_every, 13] (may be NULL). */
+int dgx_drop_batch(dgx_ctx* ctx, const dgx_object* obj, int32_t B, const double* state_in,
+                   const dgx_drop_params* params, double* state_out, int32_t* steps, double* ke, double* stats,
+                   double* traj, uint32_t flags);
 
 /* Utility: measured FP64 FMA throughput of the device (TFLOP/s), the
    roofline denominator for the fused kernel. */

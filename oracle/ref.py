@@ -93,6 +93,8 @@ def lib(variant: str = "sm") -> C.CDLL:
     L.dgr_object_mesh_export.argtypes = [vp, _dp, _ip, _dp]
     L.dgr_object_bvh.argtypes = [vp, _dp, _ip, _ip, C.c_int]
     L.dgr_object_query_within.argtypes = [vp, _dp, C.c_double, _dp]
+    L.dgr_drop.argtypes = [vp, _dp, C.c_double, C.c_double, C.c_int, _dp, C.c_int, C.c_int, C.c_double, C.c_int,
+                           _dp, _ip, _dp, _dp, _dp, C.c_int, C.c_int]
     L.dgr_object_use_sphere.argtypes = [vp, C.c_double, C.c_double, C.c_double, C.c_double]
     L.dgr_object_use_box.argtypes = [vp, _dp, _dp]
     L.dgr_object_use_grid.argtypes = [vp, _ip, _dp, C.c_double, C.c_double, _fp]
@@ -383,3 +385,19 @@ def optimize(obj, hand, q, params, iters, k_begin=0, k_end=None, r0=0.02, lr=1e-
     if record:
         out.update(losses=tl, grads=tg)
     return out
+
+
+def drop(obj: RefObject, state, dt=1e-3, mu=1.0, gs=8, gravity=(0.0, 0.0, -9.81), max_steps=5000, min_steps=1,
+         ke_tol=1e-6, measure=False, record_every=0, settle=100):
+    """step_on_table (sim.cpp:14-94) iterated from one RigidState row [13] with
+    dgx_drop_batch's stopping rule -> (state [13], steps, ke, stats [4], traj)."""
+    L = obj.L
+    st = np.ascontiguousarray(state, np.float64)
+    g = np.ascontiguousarray(gravity, np.float64)
+    out, ke, stats = np.zeros(13), C.c_double(), np.zeros(4)
+    steps = np.zeros(1, np.int32)
+    rows = max_steps // record_every if record_every > 0 else 0
+    traj = np.zeros((max(rows, 1), 13))
+    _check(L, L.dgr_drop(obj.ptr, _d(st), dt, mu, gs, _d(g), max_steps, min_steps, ke_tol, int(measure), _d(out),
+                         _i(steps), C.byref(ke), _d(stats), _d(traj) if rows else None, record_every, settle))
+    return out, int(steps[0]), ke.value, stats, (traj[:rows] if rows else None)

@@ -391,6 +391,58 @@ int dgr_object_query_within(void* o, const double* r, double radius, double* out
   } catch (const std::exception& e) { return fail(e); }
 }
 
+// ---- scene drop -------------------------------------------
+// The reference's step_on_table (sim.cpp:14-94) iterated on one RigidState
+// with the driver rule of dgx_drop_batch: stop once settle consecutive steps
+// made contact (any correction) and left kinetic_energy (sim.cpp:8-12) <
+// ke_tol, never before min_steps, at most max_steps. One SolveStats shared by
+// all steps.
+int dgr_drop(void* o, const double* in, double dt, double mu, int gs, const double* gravity, int max_steps,
+             int min_steps, double ke_tol, int measure, double* out, int* steps, double* ke, double* stats,
+             double* traj, int record_every, int settle) {
+  try {
+    const auto& obj = *static_cast<GraspObject*>(o);
+    SimParams p;
+    p.dt = dt;
+    p.mu = mu;
+    p.gs_iters = gs;
+    p.gravity = Vec3{gravity[0], gravity[1], gravity[2]};
+    RigidState s;
+    s.x = {in[0], in[1], in[2]};
+    s.theta = {in[3], in[4], in[5], in[6]};
+    s.xdot = {in[7], in[8], in[9]};
+    s.thetadot = {in[10], in[11], in[12]};
+    SolveStats st;
+    st.measure_residual = measure != 0;
+    int k = 0, calm = 0;
+    double e = kinetic_energy(s, obj.inertial);
+    for (; k < max_steps;) {
+      const int corr_before = st.corrections;
+      s = step_on_table(s, obj.sdf.mesh(), obj.inertial, p, &st);
+      ++k;
+      if (traj && record_every > 0 && k % record_every == 0) {
+        double* t = traj + static_cast<std::size_t>(k / record_every - 1) * 13;
+        t[0] = s.x.x; t[1] = s.x.y; t[2] = s.x.z;
+        t[3] = s.theta.w; t[4] = s.theta.x; t[5] = s.theta.y; t[6] = s.theta.z;
+        t[7] = s.xdot.x; t[8] = s.xdot.y; t[9] = s.xdot.z;
+        t[10] = s.thetadot.x; t[11] = s.thetadot.y; t[12] = s.thetadot.z;
+      }
+      e = kinetic_energy(s, obj.inertial);
+      calm = (st.corrections > corr_before && e < ke_tol) ? calm + 1 : 0;
+      if (calm >= settle && k >= min_steps) break;
+    }
+    out[0] = s.x.x; out[1] = s.x.y; out[2] = s.x.z;
+    out[3] = s.theta.w; out[4] = s.theta.x; out[5] = s.theta.y; out[6] = s.theta.z;
+    out[7] = s.xdot.x; out[8] = s.xdot.y; out[9] = s.xdot.z;
+    out[10] = s.thetadot.x; out[11] = s.thetadot.y; out[12] = s.thetadot.z;
+    *steps = k;
+    *ke = e;
+    stats[0] = st.active_contacts; stats[1] = st.corrections; stats[2] = st.singular_skipped;
+    stats[3] = st.max_penetration;
+    return 0;
+  } catch (const std::exception& e) { return fail(e); }
+}
+
 // ---- objective ------------------------------------------------------------
 int dgr_loss_gradient(void* o, void* hp, const double* q, const Params* p, double* losses,
                       double* d_stable, double* d_qrange, double* d_qlimit) {

@@ -226,6 +226,60 @@ def sdf_query(ctx: Context, obj: GraspObject, points, radius: float = 0.0, withi
     return out
 
 
+@dataclass
+class DropParams:
+    """step_on_table's SimParams (sim.hpp:33-40) with gravity on, plus the
+    scene driver's stopping rule."""
+    dt: float = 1e-3
+    mu: float = 1.0
+    gs_iters: int = 8
+    gravity: tuple = (0.0, 0.0, -9.81)
+    max_steps: int = 5000
+    min_steps: int = 1
+    ke_tol: float = 1e-6
+    settle_steps: int = 100
+    measure_residual: bool = False
+
+    def c(self, record_every: int = 0) -> capi.DropParamsC:
+        p = capi.DropParamsC()
+        p.dt, p.mu, p.gs_iters = float(self.dt), float(self.mu), int(self.gs_iters)
+        p.measure_residual = int(bool(self.measure_residual))
+        p.gravity[:] = [float(v) for v in self.gravity]
+        p.max_steps, p.min_steps, p.ke_tol = int(self.max_steps), int(self.min_steps), float(self.ke_tol)
+        p.record_every = int(record_every)
+        p.settle_steps = int(self.settle_steps)
+        return p
+
+
+def drop(ctx: Context, obj: GraspObject, states, params: DropParams = DropParams(), record_every: int = 0,
+         flags: int | None = None):
+    """Batched scene drop of a mesh object: every RigidState row [13] (x, theta
+    w,x,y,z, xdot, thetadot) advanced by step_on_table (sim.cpp:14-94) until at
+    rest on the table z = 0 (settle_steps consecutive contact steps with kinetic
+    energy < ke_tol). Returns dict(state, steps, ke, stats[, traj])."""
+    dev = not isinstance(states, np.ndarray)
+    B = states.shape[0]
+    rows = params.max_steps // record_every if record_every > 0 else 0
+    if dev:
+        import torch
+        mk = lambda *shape, dt=torch.float64: torch.zeros(*shape, dtype=dt, device=states.device)  # noqa: E731
+        out, steps, ke, stats = mk(B, 13), mk(B, dt=torch.int32), mk(B), mk(B, 4)
+        traj = mk(B, rows, 13) if rows else None
+        fl = capi.DGX_DEVICE_PTRS if flags is None else flags
+    else:
+        states = _f64(states, (-1, 13))
+        out, steps, ke, stats = np.zeros((B, 13)), np.zeros(B, np.int32), np.zeros(B), np.zeros((B, 4))
+        traj = np.zeros((B, rows, 13)) if rows else None
+        fl = 0 if flags is None else flags
+    p = params.c(record_every)
+    capi.check(ctx.L.dgx_drop_batch(ctx.h, obj.h, B, capi.ptr(states), C.byref(p), capi.ptr(out), capi.ptr(steps),
+                                    capi.ptr(ke), capi.ptr(stats), capi.ptr(traj), fl))
+    res = dict(state=out, steps=steps, ke=ke, stats=stats)
+    if rows:
+        res["traj"] = traj
+    return res
+
+
 def mesh_bvh(vertices, faces):
     """Host-only: the BVH dgx_object_upload builds for a mesh (Bvh::build,
     bvh.cpp:148-163) as (boxes [n,6], links [n,4] left/right/first/count,

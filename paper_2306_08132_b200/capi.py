@@ -47,7 +47,15 @@ class ObjectDescC(C.Structure):
         ("spacing", C.c_double), ("inv_spacing", C.c_double), ("values", _fp), ("mass", C.c_double),
         ("com", C.c_double * 3), ("inertia_body_inv", C.c_double * 9),
         ("num_vertices", C.c_int32), ("num_faces", C.c_int32), ("vertices", _dp), ("faces", _ip),
-        ("vertex_normals", _dp), ("alpha_phong", C.c_double),
+        ("vertex_normals", _dp), ("alpha_phong", C.c_double), ("inertia_body", C.c_double * 9),
+    ]
+
+
+class DropParamsC(C.Structure):
+    _fields_ = [
+        ("dt", C.c_double), ("mu", C.c_double), ("gs_iters", C.c_int32), ("measure_residual", C.c_int32),
+        ("gravity", C.c_double * 3), ("max_steps", C.c_int32), ("min_steps", C.c_int32), ("ke_tol", C.c_double),
+        ("record_every", C.c_int32), ("settle_steps", C.c_int32),
     ]
 
 
@@ -74,7 +82,7 @@ EXPORTS = [
     "dgx_object_upload", "dgx_object_free", "dgx_forward_batch", "dgx_loss_gradient_batch",
     "dgx_evaluate_losses_batch", "dgx_apply_gradient_step_batch", "dgx_optimize_batch", "dgx_debug_sims",
     "dgx_fp64_peak", "dgx_optimize_multi", "dgx_sdf_query_batch", "dgx_mesh_inertia",
-    "dgx_mesh_bvh",
+    "dgx_mesh_bvh", "dgx_drop_batch",
 ]
 
 _lib: C.CDLL | None = None
@@ -120,6 +128,7 @@ def load() -> C.CDLL:
     L.dgx_sdf_query_batch.argtypes = [vp, vp, C.c_int32, vp, C.c_double, C.c_int32, vp, C.c_uint32]
     L.dgx_mesh_inertia.argtypes = [C.c_int32, vp, C.c_int32, vp, C.c_double, _dp, _dp, _dp, _dp]
     L.dgx_mesh_bvh.argtypes = [C.c_int32, vp, C.c_int32, vp, C.c_int32, vp, vp, vp, _ip]
+    L.dgx_drop_batch.argtypes = [vp, vp, C.c_int32, vp, C.POINTER(DropParamsC), vp, vp, vp, vp, vp, C.c_uint32]
     _lib = L
     return L
 
@@ -182,4 +191,5 @@ def object_desc_c(o) -> tuple[ObjectDescC, list]:
     d.mass = float(o.mass)
     d.com[:] = [float(v) for v in o.com]
     d.inertia_body_inv[:] = [float(v) for v in np.asarray(o.inertia_body_inv, np.float64).reshape(9)]
+    d.inertia_body[:] = [float(v) for v in np.asarray(o.inertia_body, np.float64).reshape(9)]
     return d, keep

@@ -14,6 +14,7 @@
 #include "../../include/dgx.h"
 #include "dgx_kernel.cuh"
 #include "dgx_mesh_host.h"
+#include "dgx_drop.cuh"
 
 using namespace dgx;
 
@@ -66,12 +67,13 @@ struct DevBuf {
 
 // per-stream kernel scratch (correction logs, contact slots, link-sum spills)
 struct Scratch {
-  DevBuf corr, slots, ftg, mcache;
+  DevBuf corr, slots, ftg, mcache, drop;
   void release() {
     corr.release();
     slots.release();
     ftg.release();
     mcache.release();
+    drop.release();
   }
 };
 
@@ -109,6 +111,11 @@ struct dgx_object {
   SdfSet sdf{};
   DevBuf vals;  // grid values, or the mesh block (nodes, faces, tri, vx, vn, MeshGeom)
   KObj k;
+  // mesh objects: device vertices + count (table-contact samples of the drop)
+  const double* mesh_vx = nullptr;
+  int mesh_nv = 0;
+  M3 inertia_body{};
+  bool has_inertia_body = false;
 };
 
 namespace {
@@ -416,6 +423,8 @@ int dgx_object_upload(dgx_ctx* c, const dgx_object_desc* d, dgx_object** out) {
         g.cull = 0.005;  // ContactSolver::kCullMargin (sim.hpp:213)
         g.nfaces = d->num_faces;
         o->sdf.mesh = MeshSdf{static_cast<const MeshGeom*>(put(&g, sizeof(MeshGeom), rnd(sizeof(MeshGeom))))};
+        o->mesh_vx = g.vx;
+        o->mesh_nv = d->num_vertices;
       } else {
         throw DgxError(DGX_E_UNSUPPORTED, "object: unknown SDF kind " + std::to_string(d->kind));
       }
@@ -423,6 +432,10 @@ int dgx_object_upload(dgx_ctx* c, const dgx_object_desc* d, dgx_object** out) {
       o->k.inv_mass = 1.0 / d->mass;
       o->k.com = V3{d->com[0], d->com[1], d->com[2]};
       for (int t = 0; t < 9; ++t) o->k.inertia_body_inv.m[t] = d->inertia_body_inv[t];
+      for (int t = 0; t < 9; ++t) {
+        o->inertia_body.m[t] = d->inertia_body[t];
+        o->has_inertia_body = o->has_inertia_body || d->inertia_body[t] != 0.0;
+      }
       // predict() from the canonical state (thetadot = 0, sim.hpp:74-83) and
       // world_inertia_inv (sim.hpp:96-100), same formulas as the kernel
       const Q4 pred_q = qnormalized(qmul(quat_exp(V3{0.0, 0.0, 0.0}), Q4{1.0, 0.0, 0.0, 0.0}));
@@ -490,6 +503,43 @@ int dgx_mesh_bvh(int32_t num_vertices, const double* vertices, int32_t num_faces
     }
     for (int i = 0; i < num_faces; ++i) face_order[i] = mh.faces[i].f;
     *n_nodes = n;
+  });
+}
+
+int dgx_drop_batch(dgx_ctx* c, const dgx_object* o, int32_t B, const double* state_in, const dgx_drop_params* p,
+                   double* state_out, int32_t* steps, double* ke, double* stats, double* traj, uint32_t flags) {
+  return guarded([&] {
+    if (!c || !o || !p || !steps || !ke) throw DgxError(DGX_E_INVALID, "NULL argument");
+    if (B < 0) throw DgxError(DGX_E_INVALID, "B < 0");
+    if (o->kind != DGX_SDF_MESH || !o->mesh_vx)
+      throw DgxError(DGX_E_UNSUPPORTED, "drop: needs a mesh object (its vertices are the table contacts, sim.cpp:28)");
+    if (!o->has_inertia_body) throw DgxError(DGX_E_INVALID, "drop: object descriptor lacks inertia_body");
+    if (!(p->dt > 0.0) || p->gs_iters < 0 || p->max_steps < 0)
+      throw DgxError(DGX_E_INVALID, "drop: dt > 0, gs_iters >= 0, max_steps >= 0 required");
+    if (traj && p->record_every <= 0) throw DgxError(DGX_E_INVALID, "drop: traj needs record_every > 0");
+    if (p->settle_steps < 1) throw DgxError(DGX_E_INVALID, "drop: settle_steps must be >= 1");
+    if (B == 0) return;
+    set_device(c);
+    DropObj O{o->mesh_vx, o->mesh_nv, o->k.mass, o->k.com, o->inertia_body, o->k.inertia_body_inv};
+    DropParams P{p->dt, p->mu, p->gs_iters, V3{p->gravity[0], p->gravity[1], p->gravity[2]}, p->max_steps,
+                 p->min_steps, p->ke_tol, p->record_every, p->settle_steps, p->measure_residual};
+    const int rows = traj ? p->max_steps / p->record_every : 0;
+    const bool dev = flags & DGX_DEVICE_PTRS;
+    Staging s(c, dev, bytes_round(104ull * B) * 2 + bytes_round(4ull * B) + bytes_round(8ull * B) +
+                          bytes_round(32ull * B) + bytes_round(104ull * B * rows));
+    const double* din = s.in(state_in, static_cast<size_t>(B) * 13);
+    double* dout = s.out(state_out, static_cast<size_t>(B) * 13);
+    int* dsteps = s.out(steps, static_cast<size_t>(B));
+    double* dke = s.out(ke, static_cast<size_t>(B));
+    double* dstats = s.out(stats, static_cast<size_t>(B) * 4);
+    double* dtraj = s.out(traj, static_cast<size_t>(B) * rows * 13);
+    const int warps = std::min(B, c->num_sms * 32);
+    c->scratch.drop.ensure(static_cast<size_t>(warps) * o->mesh_nv * sizeof(double));
+    cuda_check(launch_drop(O, P, B, din, dout, dsteps, dke, dstats, static_cast<double*>(c->scratch.drop.p), warps,
+                           dtraj, c->stream),
+               "drop_kernel");
+    ++c->launches;
+    s.finish(flags);
   });
 }
 

@@ -146,6 +146,56 @@ def config1_mesh():
                 mean_final_loss_gpu=float(eg[:, 0].mean()), mean_final_loss_ref=float(er[:, 0].mean()))
 
 
+def scene_drop():
+    """§8(f)-4 batched scene drop: scene-steps/s of step_on_table (sim.cpp:14-94)
+    on the GPU (one warp per scene) vs the reference's own step_on_table on all
+    host threads (oracle dgr_drop per scene, ctypes releases the GIL)."""
+    from concurrent.futures import ThreadPoolExecutor
+    from oracle import ref
+    from paper_2306_08132_b200 import pipeline
+    rows = []
+    meshes = {"box (8 vertices)": lambda: ref.RefObject.box_mesh(0.04, 0.05, 0.03, variant="glibc"),
+              "cylinder32 (66 vertices)": lambda: ref.RefObject.cylinder_mesh(0.0175, 0.07, 32, variant="glibc"),
+              "icosphere3 (642 vertices)": lambda: ref.RefObject.icosphere(0.025, 3, variant="glibc"),
+              "blob3 (642 vertices)": lambda: ref.RefObject.blob_mesh(0.021, 3, 0.5, 7, variant="glibc")}
+    ctx = api.Context(0)
+    stream = torch.cuda.Stream(DEV)
+    torch.cuda.set_stream(stream)
+    ctx.set_stream(stream.cuda_stream)
+    for name, mk in meshes.items():
+        ro = mk()
+        V, F, _ = ro.mesh_export()
+        od = model.mesh_object(V, F)
+        obj = api.GraspObject(ctx, od)
+        S, K = 8192, 2000
+        s0 = torch.tensor(pipeline.scene_states(od, np.arange(S)), device=DEV)
+        prm = api.DropParams(max_steps=K)
+        api.drop(ctx, obj, s0[:256], prm)
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        r = api.drop(ctx, obj, s0, prm)
+        e1.record(stream)
+        torch.cuda.synchronize()
+        ms = e0.elapsed_time(e1)
+        gsteps = float(r["steps"].sum().item())
+        # reference CPU on a subset, all host threads
+        sub = 64
+        s0h = s0[:sub].cpu().numpy()
+        t0 = time.perf_counter()
+        with ThreadPoolExecutor(os.cpu_count()) as ex:
+            res = list(ex.map(lambda b: ref.drop(ro, s0h[b], max_steps=K), range(sub)))
+        cpu_s = time.perf_counter() - t0
+        csteps = sum(x[1] for x in res)
+        rows.append(dict(mesh=name, scenes=S, max_steps=K, gpu_ms=ms, gpu_scene_steps_per_s=gsteps / (ms * 1e-3),
+                         gpu_scenes_per_s=S / (ms * 1e-3), mean_steps=gsteps / S,
+                         at_rest_frac=float((r["steps"] < K).float().mean().item()),
+                         cpu_reference_scene_steps_per_s=csteps / cpu_s, cpu_threads=os.cpu_count(), cpu_subset=sub))
+    ctx.set_stream(None)
+    return dict(config="scene_drop", workload="batched table drop, step_on_table until settled (100 calm steps) "
+                                              "or 2 s; 8192 random-orientation scenes per mesh", rows=rows)
+
+
 def config3():
     hd = model.HandDesc.asset("shadow22_dense")
     od = model.blob_grid(seed=3, res=128)
@@ -188,7 +238,7 @@ def config5():
 
 
 def main():
-    which = sys.argv[1:] or ["config1", "config1_mesh", "config3", "config4", "config5"]
+    which = sys.argv[1:] or ["config1", "config1_mesh", "config3", "config4", "config5", "scene_drop"]
     for w in which:
         t = time.time()
         rec = globals()[w]()

@@ -13,6 +13,8 @@
  *                              + InertialData (rigid.hpp:8-13)
  *   dgx_sdf_query_batch        MeshSdf::dilated / dilated_within (sdf.hpp:41-45)
  *   dgx_mesh_inertia           dg::inertia_from_mesh (rigid.cpp:24-94)
+ *   dgx_contacts_batch         SPEC metrics.generate_contacts / contact_area
+ *                              (not implemented by the reference)
  *   dgx_drop_batch             dg::step_on_table (sim.cpp:14-94) + kinetic_energy
  *                              (sim.cpp:8-12), iterated per scene
  *   dgx_forward_batch          HandModel::forward(const HandConfig&) (hand.hpp:86)
@@ -224,6 +226,20 @@ int dgx_optimize_multi(dgx_ctx* ctx, const dgx_hand* hand, int32_t n_obj, const 
 int dgx_debug_sims(dgx_ctx* ctx, const dgx_hand* hand, const dgx_object* obj, int32_t B, const double* q,
                    const dgx_params* params, double* sim_res, double* sim_grads, double* point_grads,
                    int32_t* status, uint32_t flags);
+
+/* Contact generation for grasp metrics (no
+   reference implementation): hand samples of q_b (forward order) queried
+   against the object at its canonical pose; a sample is a contact at
+   threshold t when |rho| <= t. thresholds [T] (host memory, ascending, T <=
+   16, >= 0). Outputs: contact_area [B,T] (m^2, sum of sample_area [N] over
+   contacts), contact_count [B,T], num_contacts [B] (at the largest
+   threshold, may exceed cap), contact_index [B,cap] (sample indices, ascending)
+   and contacts [B,cap,7] (rho, smoothed surface point (3), unit gradient (3))
+   for the first min(num_contacts, cap) contacts. */
+int dgx_contacts_batch(dgx_ctx* ctx, const dgx_hand* hand, const dgx_object* obj, int32_t B, const double* q,
+                       const double* sample_area, int32_t num_thresholds, const double* thresholds, int32_t cap,
+                       double* contact_area, int32_t* contact_count, int32_t* num_contacts,
+                       int32_t* contact_index, double* contacts, uint32_t flags);
 
 /* Batched scene drop: each row of state_in
    [B,13] (dg::RigidState: x(3), theta w,x,y,z (4), xdot(3), thetadot(3)) of a

@@ -78,6 +78,7 @@ def lib(variant: str = "sm") -> C.CDLL:
     L.dgr_hand_dims.argtypes = [vp, _ip]
     L.dgr_hand_export.argtypes = [vp, _ip, _ip, _ip, _ip, _dp, _dp, _dp, _dp, _dp, _dp, _ip]
     L.dgr_hand_forward.argtypes = [vp, _dp, _dp]
+    L.dgr_hand_sample_areas.argtypes = [vp, _dp]
     L.dgr_object_mesh.restype = vp
     L.dgr_object_mesh.argtypes = [_dp, C.c_int, _ip, C.c_int, C.c_double, C.c_double]
     L.dgr_object_icosphere.restype = vp
@@ -159,6 +160,8 @@ class RefHand:
         L.dgr_hand_export(ptr, _i(d["topo"]), _i(d["link_parent_joint"]), _i(d["joint_parent"]),
                           _i(d["joint_child"]), _d(d["axis"]), _d(d["origin_R"]), _d(d["origin_t"]),
                           _d(d["lower"]), _d(d["upper"]), _d(d["samples"]), _i(d["sample_link"]))
+        d["sample_area"] = np.zeros(N)
+        L.dgr_hand_sample_areas(ptr, _d(d["sample_area"]))
         h.desc = d
         return h
 

@@ -270,6 +270,13 @@ void dgr_hand_export(void* hp, int* topo, int* link_parent_joint, int* joint_par
     }
 }
 
+// per-sample surface area (HandModel::sample_areas, hand.hpp:77; link area /
+// link sample count, hand.cpp:199-207), forward() order
+void dgr_hand_sample_areas(void* hp, double* out) {
+  const auto& a = static_cast<HandModel*>(hp)->sample_areas();
+  for (std::size_t i = 0; i < a.size(); ++i) out[i] = a[i];
+}
+
 int dgr_hand_forward(void* hp, const double* q, double* out) {
   try {
     auto* h = static_cast<HandModel*>(hp);

@@ -82,7 +82,7 @@ EXPORTS = [
     "dgx_object_upload", "dgx_object_free", "dgx_forward_batch", "dgx_loss_gradient_batch",
     "dgx_evaluate_losses_batch", "dgx_apply_gradient_step_batch", "dgx_optimize_batch", "dgx_debug_sims",
     "dgx_fp64_peak", "dgx_optimize_multi", "dgx_sdf_query_batch", "dgx_mesh_inertia",
-    "dgx_mesh_bvh", "dgx_drop_batch",
+    "dgx_mesh_bvh", "dgx_drop_batch", "dgx_contacts_batch",
 ]
 
 _lib: C.CDLL | None = None
@@ -128,6 +128,8 @@ def load() -> C.CDLL:
     L.dgx_sdf_query_batch.argtypes = [vp, vp, C.c_int32, vp, C.c_double, C.c_int32, vp, C.c_uint32]
     L.dgx_mesh_inertia.argtypes = [C.c_int32, vp, C.c_int32, vp, C.c_double, _dp, _dp, _dp, _dp]
     L.dgx_mesh_bvh.argtypes = [C.c_int32, vp, C.c_int32, vp, C.c_int32, vp, vp, vp, _ip]
+    L.dgx_contacts_batch.argtypes = [vp, vp, vp, C.c_int32, vp, vp, C.c_int32, _dp, C.c_int32, vp, vp, vp, vp, vp,
+                                     C.c_uint32]
     L.dgx_drop_batch.argtypes = [vp, vp, C.c_int32, vp, C.POINTER(DropParamsC), vp, vp, vp, vp, vp, C.c_uint32]
     _lib = L
     return L

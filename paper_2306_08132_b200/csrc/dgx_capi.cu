@@ -67,8 +67,9 @@ struct DevBuf {
 
 // per-stream kernel scratch (correction logs, contact slots, link-sum spills)
 struct Scratch {
-  DevBuf corr, slots, ftg, mcache, drop;
+  DevBuf corr, slots, ftg, mcache, drop, thr;
   void release() {
+    thr.release();
     corr.release();
     slots.release();
     ftg.release();
@@ -503,6 +504,45 @@ int dgx_mesh_bvh(int32_t num_vertices, const double* vertices, int32_t num_faces
     }
     for (int i = 0; i < num_faces; ++i) face_order[i] = mh.faces[i].f;
     *n_nodes = n;
+  });
+}
+
+int dgx_contacts_batch(dgx_ctx* c, const dgx_hand* h, const dgx_object* o, int32_t B, const double* q,
+                       const double* sample_area, int32_t T, const double* thresholds, int32_t cap,
+                       double* contact_area, int32_t* contact_count, int32_t* num_contacts, int32_t* contact_index,
+                       double* contacts, uint32_t flags) {
+  return guarded([&] {
+    if (!c || !h || !o || !sample_area || !thresholds || !contact_area || !contact_count || !num_contacts)
+      throw DgxError(DGX_E_INVALID, "NULL argument");
+    if (B < 0 || cap < 0) throw DgxError(DGX_E_INVALID, "B < 0 or cap < 0");
+    if (T < 1 || T > 16) throw DgxError(DGX_E_INVALID, "contacts: 1..16 thresholds");
+    for (int t = 0; t < T; ++t)
+      if (!(thresholds[t] >= 0.0) || (t > 0 && thresholds[t] < thresholds[t - 1]))
+        throw std::invalid_argument("contacts: thresholds must be >= 0 and ascending");
+    if (cap > 0 && (!contact_index || !contacts)) throw DgxError(DGX_E_INVALID, "contacts: cap > 0 needs outputs");
+    if (B == 0) return;
+    set_device(c);
+    const bool dev = flags & DGX_DEVICE_PTRS;
+    const size_t N = h->N;
+    Staging s(c, dev, bytes_round(8ull * B * (7 + h->J)) + bytes_round(8ull * N) + bytes_round(8ull * B * T) +
+                          bytes_round(4ull * B * T) + bytes_round(4ull * B) + bytes_round(4ull * B * cap) +
+                          bytes_round(56ull * B * cap));
+    const double* dq = s.in(q, static_cast<size_t>(B) * (7 + h->J));
+    const double* da = s.in(sample_area, N);
+    double* dca = s.out(contact_area, static_cast<size_t>(B) * T);
+    int* dcnt = s.out(contact_count, static_cast<size_t>(B) * T);
+    int* dn = s.out(num_contacts, static_cast<size_t>(B));
+    int* dci = s.out(contact_index, static_cast<size_t>(B) * cap);
+    double* dcr = s.out(contacts, static_cast<size_t>(B) * cap * 7);
+    c->scratch.thr.ensure(16 * sizeof(double));
+    cuda_check(cudaMemcpyAsync(c->scratch.thr.p, thresholds, T * sizeof(double), cudaMemcpyHostToDevice, c->stream),
+               "H2D thresholds");
+    const int grid = std::min(B, c->num_sms * 8);
+    cuda_check(launch_contacts(h->k, o->sdf, B, dq, da, T, static_cast<const double*>(c->scratch.thr.p), cap, dca,
+                               dcnt, dn, dci, dcr, grid, c->stream),
+               "contacts_kernel");
+    ++c->launches;
+    s.finish(flags);
   });
 }
 

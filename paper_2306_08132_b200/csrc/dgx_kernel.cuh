@@ -160,5 +160,8 @@ cudaError_t fused_occupancy(int kind, int M, int smem, int* blocks_per_sm);
 cudaError_t launch_sdf_query(const SdfSet& sdf, int n, const double* r, double radius, int within, double* out,
                              cudaStream_t st);
 cudaError_t launch_forward(const KHand& H, const double* q, double* out, int B, int grid, cudaStream_t st);
+cudaError_t launch_contacts(const KHand& H, const SdfSet& sdf, int B, const double* q, const double* area, int T,
+                            const double* thr, int cap, double* ca, int* cnt, int* ncont, int* cidx, double* crec,
+                            int grid, cudaStream_t st);
 cudaError_t launch_step(int J, const double* q, const double* g, double lr, double* out, int B, cudaStream_t st);
 }  // namespace dgx

@@ -1462,6 +1462,133 @@ __global__ void __launch_bounds__(256) forward_kernel(KHand H, const double* q, 
   }
 }
 
+// Contact generation (the reference specifies but does not
+// implement it): per candidate, FK (hand.hpp:116-152), every hand sample
+// queried against the object at its canonical pose (object frame = world),
+// contact when |rho| <= threshold. Per threshold: contact count and contact
+// area (sum of HandModel::sample_areas over contacts) from fixed-
+// order reductions; the contacts at the largest threshold are compacted in
+// point order (ballot prefix sums) with (rho, smoothed point, unit gradient).
+constexpr int kMaxThresholds = 16;
+
+template <class Sdf>
+__global__ void __launch_bounds__(256) contacts_kernel(KHand H, Sdf sdf, int B, const double* __restrict__ q,
+                                                       const double* __restrict__ area, int T,
+                                                       const double* __restrict__ thr, int cap,
+                                                       double* __restrict__ ca, int* __restrict__ cnt,
+                                                       int* __restrict__ ncont, int* __restrict__ cidx,
+                                                       double* __restrict__ crec) {
+  extern __shared__ __align__(16) unsigned char smem[];
+  double* link = reinterpret_cast<double*>(smem);
+  double* sq = link + 12 * H.L;
+  double* red = sq + 48;                                  // [8 warps][T]
+  int* redc = reinterpret_cast<int*>(red + 8 * kMaxThresholds);  // [8 warps][T]
+  int* wtot = redc + 8 * kMaxThresholds;                  // [8]
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nwarp = blockDim.x >> 5;
+  const int Qd = 7 + H.J, N = H.N;
+  const double tmax = thr[T - 1];
+  for (int b = blockIdx.x; b < B; b += gridDim.x) {
+    if (tid < Qd) sq[tid] = q[static_cast<size_t>(b) * Qd + tid];
+    __syncthreads();
+    if (tid == 0) link_transforms(H, sq, false, link);
+    __syncthreads();
+    double acc[kMaxThresholds];
+    int ac[kMaxThresholds];
+#pragma unroll
+    for (int t = 0; t < kMaxThresholds; ++t) { acc[t] = 0.0; ac[t] = 0; }
+    int nbase = 0;
+    for (int c = 0; c < N; c += blockDim.x) {
+      const int i = c + tid;
+      bool con = false;
+      SdfQuery qq{};
+      if (i < N) {
+        const double* Rl = link + 12 * H.sample_link[i];
+        M3 R;
+        for (int m = 0; m < 9; ++m) R.m[m] = Rl[m];
+        const V3 p = mul(R, V3{H.samples[3 * i], H.samples[3 * i + 1], H.samples[3 * i + 2]}) + V3{Rl[9], Rl[10], Rl[11]};
+        qq = sdf.query(p);
+        const double ar = fabs(qq.rho);
+        const double ai = area[i];
+#pragma unroll
+        for (int t = 0; t < kMaxThresholds; ++t)
+          if (t < T && ar <= thr[t]) { acc[t] += ai; ++ac[t]; }
+        con = ar <= tmax;
+      }
+      const unsigned m = __ballot_sync(0xffffffffu, con);
+      if (lane == 0) wtot[warp] = __popc(m);
+      __syncthreads();
+      int off = nbase, tot = 0;
+      for (int w = 0; w < nwarp; ++w) {
+        if (w < warp) off += wtot[w];
+        tot += wtot[w];
+      }
+      off += __popc(m & ((1u << lane) - 1u));
+      if (con && off < cap) {
+        const size_t k = static_cast<size_t>(b) * cap + off;
+        cidx[k] = i;
+        double* r = crec + 7 * k;
+        r[0] = qq.rho;
+        r[1] = qq.proxy.x; r[2] = qq.proxy.y; r[3] = qq.proxy.z;
+        r[4] = qq.grad.x; r[5] = qq.grad.y; r[6] = qq.grad.z;
+      }
+      nbase += tot;
+      __syncthreads();
+    }
+    // fixed-order reductions: xor butterfly per warp, then warps in order
+#pragma unroll
+    for (int t = 0; t < kMaxThresholds; ++t) {
+      if (t >= T) break;
+      double v = acc[t];
+      int n = ac[t];
+      for (int o = 16; o > 0; o >>= 1) {
+        v += __shfl_xor_sync(0xffffffffu, v, o);
+        n += __shfl_xor_sync(0xffffffffu, n, o);
+      }
+      if (lane == 0) {
+        red[warp * kMaxThresholds + t] = v;
+        redc[warp * kMaxThresholds + t] = n;
+      }
+    }
+    __syncthreads();
+    if (tid < T) {
+      double v = 0.0;
+      int n = 0;
+      for (int w = 0; w < nwarp; ++w) {
+        v += red[w * kMaxThresholds + tid];
+        n += redc[w * kMaxThresholds + tid];
+      }
+      ca[static_cast<size_t>(b) * T + tid] = v;
+      cnt[static_cast<size_t>(b) * T + tid] = n;
+    }
+    if (tid == 0) ncont[b] = nbase;
+    __syncthreads();
+  }
+}
+
+cudaError_t launch_contacts(const KHand& H, const SdfSet& sdf, int B, const double* q, const double* area, int T,
+                            const double* thr, int cap, double* ca, int* cnt, int* ncont, int* cidx, double* crec,
+                            int grid, cudaStream_t st) {
+  if (B <= 0) return cudaSuccess;
+  const size_t smem = sizeof(double) * (12 * H.L + 48 + 8 * kMaxThresholds) + sizeof(int) * (8 * kMaxThresholds + 8);
+  switch (sdf.kind) {
+    case kSdfSphere:
+      contacts_kernel<<<grid, 256, smem, st>>>(H, sdf.sph, B, q, area, T, thr, cap, ca, cnt, ncont, cidx, crec);
+      break;
+    case kSdfBox:
+      contacts_kernel<<<grid, 256, smem, st>>>(H, sdf.box, B, q, area, T, thr, cap, ca, cnt, ncont, cidx, crec);
+      break;
+    case kSdfGrid:
+      contacts_kernel<<<grid, 256, smem, st>>>(H, sdf.grd, B, q, area, T, thr, cap, ca, cnt, ncont, cidx, crec);
+      break;
+    case kSdfMesh:
+      contacts_kernel<<<grid, 256, smem, st>>>(H, sdf.mesh, B, q, area, T, thr, cap, ca, cnt, ncont, cidx, crec);
+      break;
+    default:
+      return cudaErrorInvalidValue;
+  }
+  return cudaGetLastError();
+}
+
 __global__ void step_kernel(int J, const double* q, const double* g, double lr, double* out, int B) {
   const int b = blockIdx.x * blockDim.x + threadIdx.x;
   if (b >= B) return;

@@ -38,6 +38,7 @@ class HandDesc:
     upper: np.ndarray             # [J]
     samples: np.ndarray           # [N,3] link frame, forward() order
     sample_link: np.ndarray       # [N] int32
+    sample_area: np.ndarray | None = None  # [N] m^2, HandModel::sample_areas (hand.hpp:77)
 
     @property
     def num_links(self) -> int:
@@ -78,12 +79,15 @@ class HandDesc:
             upper=np.ascontiguousarray(d["upper"], np.float64),
             samples=np.ascontiguousarray(d["samples"], np.float64).reshape(-1, 3),
             sample_link=np.ascontiguousarray(d["sample_link"], np.int32),
+            sample_area=np.ascontiguousarray(d["sample_area"], np.float64) if "sample_area" in d else None,
         )
 
     def to_dict(self) -> dict:
-        return {k: getattr(self, k) for k in ("topo", "link_parent_joint", "joint_parent", "joint_child", "axis",
-                                               "origin_R", "origin_t", "lower", "upper", "samples",
-                                               "sample_link")}
+        d = {k: getattr(self, k) for k in ("topo", "link_parent_joint", "joint_parent", "joint_child", "axis",
+                                            "origin_R", "origin_t", "lower", "upper", "samples", "sample_link")}
+        if self.sample_area is not None:
+            d["sample_area"] = self.sample_area
+        return d
 
     def save(self, path: str) -> None:
         np.savez_compressed(path, name=np.array(self.name), **self.to_dict())

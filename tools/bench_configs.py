@@ -196,6 +196,45 @@ def scene_drop():
                                               "or 2 s; 8192 random-orientation scenes per mesh", rows=rows)
 
 
+def metrics_sweep():
+    """§8(f)-3: synthesis + grasp metrics. 256 barrett3 candidates on a 40 mm
+    box MESH, 200 iterations on the GPU; contact generation at 1..10 mm
+    (dgx_contacts_batch, one launch) and epsilon / GWS volume (host Qhull) for
+    the initial and final grasps (SPEC ACCEPTANCE 5-6 shape)."""
+    from paper_2306_08132_b200 import metrics
+    hd = model.HandDesc.asset("barrett3")
+    od = model.mesh_object(*model.box_mesh((0.04, 0.04, 0.04)))
+    ctx = api.Context(0)
+    hand, obj = api.Hand(ctx, hd), api.GraspObject(ctx, od)
+    B, K = 256, 200
+    q0 = init.approach_init(od, hd, B, seed=21)
+    ms, qf, bad = timed_opt(ctx, [obj], hand, hd, [q0], K, 1, K)
+    thr = tuple(float(t) for t in range(1, 11))
+    metrics.contacts(ctx, hand, obj, qf, thr)
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    for _ in range(5):
+        metrics.contacts(ctx, hand, obj, qf, thr)
+    t_con = (time.perf_counter() - t0) / 5
+    t0 = time.perf_counter()
+    rep0 = metrics.evaluate(ctx, hand, obj, q0, thr, hull_thresholds_mm=(2.0, 5.0, 10.0))
+    repf = metrics.evaluate(ctx, hand, obj, qf, thr, hull_thresholds_mm=(2.0, 5.0, 10.0))
+    t_eval = (time.perf_counter() - t0) / 2
+    s0, sf = metrics.threshold_sweep(rep0), metrics.threshold_sweep(repf)
+    top = metrics.top_k(repf, 10, threshold_index=4)
+    c5_0 = np.array([r[4]["contacts"] for r in rep0])
+    c5_f = np.array([r[4]["contacts"] for r in repf])
+    e5_f = np.array([r[4]["epsilon"] for r in repf])
+    return dict(config="metrics_sweep", workload="barrett3 on a 40 mm box mesh, 256 candidates x 200 iterations; "
+                                                 "metrics at 1..10 mm", opt_s=ms * 1e-3, failed=bad,
+                contacts_kernel_grasps_per_s_10_thresholds=B / t_con,
+                evaluate_s_per_grasp_hulls_at_3_thresholds=t_eval / B, hull_max_contacts=32,
+                frac_more_contacts_at_5mm=float(np.mean(c5_f > c5_0)), frac_eps_positive_at_5mm=float(np.mean(e5_f > 0)),
+                sweep_init=s0, sweep_final=sf,
+                top10_mean_eps_5mm=float(np.mean([repf[i][4]["epsilon"] for i in top])),
+                top10_mean_CA_cm2_5mm=float(np.mean([repf[i][4]["contact_area_cm2"] for i in top])))
+
+
 def config3():
     hd = model.HandDesc.asset("shadow22_dense")
     od = model.blob_grid(seed=3, res=128)
@@ -238,7 +277,7 @@ def config5():
 
 
 def main():
-    which = sys.argv[1:] or ["config1", "config1_mesh", "config3", "config4", "config5", "scene_drop"]
+    which = sys.argv[1:] or ["config1", "config1_mesh", "config3", "config4", "config5", "scene_drop", "metrics_sweep"]
     for w in which:
         t = time.time()
         rec = globals()[w]()

@@ -154,16 +154,20 @@ int prepare(dgx_ctx* c, Scratch& sc, const dgx_hand* h, const dgx_object* o, KSi
   const int M = S.M;
   // longest adjoint segment whose staging still fits one CTA's shared memory
   S.seg_max = 0;
-  // mesh objects: two resident CTAs per SM (dgx_kernels.cu CtasPerSm) need
-  // the shorter adjoint staging
-  int seg_cap = o->kind == DGX_SDF_MESH ? 4 : kSegMaxCap;
+  // Adjoint staging length (points per lane): the longest up to 12 whose
+  // shared memory stays within the 196 KB carve-out tier (1 KB is reserved per
+  // CTA), so >= 60 KB of L1 remain for the SDF data. Config 2 (allegro16,
+  // 40-step bench, candidate-iterations/s): seg 16 needs 197.5 KB -> the 228 KB
+  // tier, ~28 KB of L1 -> 71k; seg 12-14 -> 78-79k; seg 15 -> 77k; seg 8 ->
+  // 77k; seg 4 -> 72k. Larger hands fall back to the longest staging that fits
+  // at all. Mesh objects run two CTAs per SM (dgx_kernels.cu CtasPerSm) and
+  // cap it at 4.
+  int seg_cap = o->kind == DGX_SDF_MESH ? 4 : 12;
   if (const char* ev = std::getenv("DGX_SEGMAX")) seg_cap = std::max(1, std::min(kSegMaxCap, std::atoi(ev)));
-  for (int seg : {kSegMaxCap, 8, 4, 2, 1}) {
-    if (seg > seg_cap) continue;
-    if (SmemLayout(h->N, h->L, M, seg).total <= 227 * 1024) {
-      S.seg_max = seg;
-      break;
-    }
+  for (int limit : {195 * 1024, 227 * 1024}) {
+    for (int seg = seg_cap; seg >= 1 && S.seg_max == 0; --seg)
+      if (SmemLayout(h->N, h->L, M, seg).total <= limit) S.seg_max = seg;
+    if (S.seg_max) break;
   }
   if (S.seg_max == 0)
     throw DgxError(DGX_E_UNSUPPORTED, "hand too large for one CTA's shared memory (N=" + std::to_string(h->N) + ")");

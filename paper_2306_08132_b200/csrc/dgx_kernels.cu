@@ -822,7 +822,7 @@ __device__ double run_sim(const Sdf& sdf, SimEnv& e, V3 v_m, bool record, bool m
   // remaining sweeps are skipped (and the adjoint folds them, run_sim below).
   int f_last = -1, singular_since = 0;
   while (sweep < e.gs) {
-#ifdef DGX_QUIET  // exact, but measured slower under the CTA barrier
+#if defined(DGX_QUIET) || defined(DGX_QUIET_FWD)  // exact
     if (sweep * N + pos - f_last - 1 >= N && singular_since == 0) break;
 #endif
     int cls[2];

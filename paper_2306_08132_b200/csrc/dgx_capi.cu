@@ -389,11 +389,29 @@ int dgx_object_upload(dgx_ctx* c, const dgx_object_desc* d, dgx_object** out) {
       } else if (d->kind == DGX_SDF_GRID) {
         if (d->dims[0] < 2 || d->dims[1] < 2 || d->dims[2] < 2 || !d->values)
           throw DgxError(DGX_E_INVALID, "grid: dims must be >= 2 and values non-NULL");
-        size_t n = static_cast<size_t>(d->dims[0]) * d->dims[1] * d->dims[2];
-        o->vals.ensure(n * sizeof(float));
+        const int nx = d->dims[0], ny = d->dims[1], nz = d->dims[2];
+        const size_t n = static_cast<size_t>(nx) * ny * nz;
+        const size_t nc = static_cast<size_t>(nx - 1) * (ny - 1) * (nz - 1);
+        // node values (host-layout copy) + the corner-packed cells the kernels read
+        const size_t vbytes = (n * sizeof(float) + 255) & ~size_t(255);
+        o->vals.ensure(vbytes + nc * 8 * sizeof(float));
         cuda_check(cudaMemcpy(o->vals.p, d->values, n * sizeof(float), cudaMemcpyHostToDevice), "grid upload");
-        o->sdf.grd = GridSdf{d->dims[0], d->dims[1], d->dims[2], V3{d->origin[0], d->origin[1], d->origin[2]},
-                             d->spacing, d->inv_spacing, static_cast<const float*>(o->vals.p)};
+        std::vector<float> packed(nc * 8);
+        const float* v = d->values;
+        auto at = [&](int i, int j, int k) { return v[(static_cast<size_t>(k) * ny + j) * nx + i]; };
+        for (int k = 0; k < nz - 1; ++k)
+          for (int j = 0; j < ny - 1; ++j)
+            for (int i = 0; i < nx - 1; ++i) {
+              float* c = packed.data() + 8 * ((static_cast<size_t>(k) * (ny - 1) + j) * (nx - 1) + i);
+              c[0] = at(i, j, k); c[1] = at(i + 1, j, k); c[2] = at(i, j + 1, k); c[3] = at(i + 1, j + 1, k);
+              c[4] = at(i, j, k + 1); c[5] = at(i + 1, j, k + 1); c[6] = at(i, j + 1, k + 1);
+              c[7] = at(i + 1, j + 1, k + 1);
+            }
+        float* dcells = reinterpret_cast<float*>(static_cast<char*>(o->vals.p) + vbytes);
+        cuda_check(cudaMemcpy(dcells, packed.data(), packed.size() * sizeof(float), cudaMemcpyHostToDevice),
+                   "grid cells upload");
+        o->sdf.grd = GridSdf{nx, ny, nz, V3{d->origin[0], d->origin[1], d->origin[2]}, d->spacing, d->inv_spacing,
+                             static_cast<const float*>(o->vals.p), dcells};
       } else if (d->kind == DGX_SDF_MESH) {
         // MeshSdf(TriMesh, alpha_phong) (sdf.cpp:17-20): validate, BVH, upload
         if (!(d->alpha_phong >= 0.0 && d->alpha_phong <= 1.0))

@@ -261,6 +261,10 @@ struct GridSdf {
   V3 origin;
   double h, inv_h;
   const float* vals;
+  // device only (may be null): corner-packed copy, the 8 node values of cell
+  // (i,j,k) at cells[8 * ((k*(ny-1) + j)*(nx-1) + i)] in the order
+  // c000 c100 c010 c110 c001 c101 c011 c111 (one 32 B sector per lookup)
+  const float* cells;
 
   DGX_GHD double at(int i, int j, int k) const {
 #if defined(__CUDA_ARCH__)
@@ -287,10 +291,22 @@ struct GridSdf {
       t[a] = v - static_cast<double>(i);
       u[a] = v;
     }
-    const double c000 = at(ci[0], ci[1], ci[2]), c100 = at(ci[0] + 1, ci[1], ci[2]);
-    const double c010 = at(ci[0], ci[1] + 1, ci[2]), c110 = at(ci[0] + 1, ci[1] + 1, ci[2]);
-    const double c001 = at(ci[0], ci[1], ci[2] + 1), c101 = at(ci[0] + 1, ci[1], ci[2] + 1);
-    const double c011 = at(ci[0], ci[1] + 1, ci[2] + 1), c111 = at(ci[0] + 1, ci[1] + 1, ci[2] + 1);
+    double c000, c100, c010, c110, c001, c101, c011, c111;
+#if defined(__CUDA_ARCH__)
+    if (cells) {
+      const float4* cp = reinterpret_cast<const float4*>(
+          cells + 8 * ((static_cast<long long>(ci[2]) * (ny - 1) + ci[1]) * (nx - 1) + ci[0]));
+      const float4 lo = __ldg(cp), hi = __ldg(cp + 1);
+      c000 = lo.x; c100 = lo.y; c010 = lo.z; c110 = lo.w;
+      c001 = hi.x; c101 = hi.y; c011 = hi.z; c111 = hi.w;
+    } else
+#endif
+    {
+      c000 = at(ci[0], ci[1], ci[2]); c100 = at(ci[0] + 1, ci[1], ci[2]);
+      c010 = at(ci[0], ci[1] + 1, ci[2]); c110 = at(ci[0] + 1, ci[1] + 1, ci[2]);
+      c001 = at(ci[0], ci[1], ci[2] + 1); c101 = at(ci[0] + 1, ci[1], ci[2] + 1);
+      c011 = at(ci[0], ci[1] + 1, ci[2] + 1); c111 = at(ci[0] + 1, ci[1] + 1, ci[2] + 1);
+    }
     const double tx = t[0], ty = t[1], tz = t[2];
     double c00 = c000 + (c100 - c000) * tx, c10 = c010 + (c110 - c010) * tx;
     double c01 = c001 + (c101 - c001) * tx, c11 = c011 + (c111 - c011) * tx;

@@ -189,9 +189,18 @@ int prepare(dgx_ctx* c, Scratch& sc, const dgx_hand* h, const dgx_object* o, KSi
   sc.ftg.ensure(nws * 6 * static_cast<size_t>(h->L) * sizeof(double));
   buf.ft_global = static_cast<double*>(sc.ftg.p);
   buf.mesh_cache = nullptr;
-  if (o->kind == DGX_SDF_MESH) {  // per point-sweep (face, sign) of the forward, read by the adjoint
-    sc.mcache.ensure(per * static_cast<size_t>(std::max(S.gs, 1)) * sizeof(int));
-    buf.mesh_cache = static_cast<int*>(sc.mcache.p);
+  buf.mesh_cert = nullptr;
+  buf.mesh_cf = nullptr;
+  if (o->kind == DGX_SDF_MESH) {
+    // per point-sweep (face, sign) of the forward, read by the adjoint; per
+    // point nearest-face certificates (4 doubles + 1 + kCertFaces ints)
+    const size_t b_cache = (per * static_cast<size_t>(std::max(S.gs, 1)) * sizeof(int) + 255) & ~size_t(255);
+    const size_t b_cert = (per * 4 * sizeof(double) + 255) & ~size_t(255);
+    sc.mcache.ensure(b_cache + b_cert + per * (kCertFaces + 1) * sizeof(int));
+    char* base = static_cast<char*>(sc.mcache.p);
+    buf.mesh_cache = reinterpret_cast<int*>(base);
+    buf.mesh_cert = reinterpret_cast<double*>(base + b_cache);
+    buf.mesh_cf = reinterpret_cast<int*>(base + b_cache + b_cert);
   }
   buf.cap_corr = c->cap_corr;
   buf.B = B;
@@ -421,7 +430,8 @@ int dgx_object_upload(dgx_ctx* c, const dgx_object_desc* d, dgx_object** out) {
         auto rnd = [](size_t x) { return (x + 255) & ~size_t(255); };
         const size_t b_nodes = rnd(mh.nodes.size() * sizeof(MeshNode)), b_faces = rnd(mh.faces.size() * sizeof(MeshFace));
         const size_t b_tri = rnd(mh.tri.size() * sizeof(int)), b_v = rnd(mh.vx.size() * sizeof(double));
-        const size_t total = b_nodes + b_faces + b_tri + 2 * b_v + rnd(sizeof(MeshGeom));
+        const size_t b_vfo = rnd(mh.vf_off.size() * sizeof(int)), b_vfi = rnd(mh.vf_idx.size() * sizeof(int));
+        const size_t total = b_nodes + b_faces + b_tri + 2 * b_v + b_vfo + b_vfi + rnd(sizeof(MeshGeom));
         o->vals.ensure(total);
         char* base = static_cast<char*>(o->vals.p);
         MeshGeom g{};
@@ -437,6 +447,8 @@ int dgx_object_upload(dgx_ctx* c, const dgx_object_desc* d, dgx_object** out) {
         g.tri = static_cast<const int*>(put(mh.tri.data(), mh.tri.size() * sizeof(int), b_tri));
         g.vx = static_cast<const double*>(put(mh.vx.data(), mh.vx.size() * sizeof(double), b_v));
         g.vn = static_cast<const double*>(put(mh.vn.data(), mh.vn.size() * sizeof(double), b_v));
+        g.vf_off = static_cast<const int*>(put(mh.vf_off.data(), mh.vf_off.size() * sizeof(int), b_vfo));
+        g.vf_idx = static_cast<const int*>(put(mh.vf_idx.data(), mh.vf_idx.size() * sizeof(int), b_vfi));
         for (int k = 0; k < 3; ++k) {
           g.blo[k] = mh.blo[k];
           g.bhi[k] = mh.bhi[k];

@@ -110,6 +110,8 @@ struct KBuf {
   int* fric_order;      // [grid, M, N]
   double* ft_global;    // [grid, M, L*6] adjoint link-sum spill buffers
   int* mesh_cache;      // [grid, M, gs*N] mesh objects: forward (face << 1 | inside) per point-sweep
+  double* mesh_cert;    // [grid, M, N, 4] mesh objects: nearest-face certificate centre + radius
+  int* mesh_cf;         // [grid, M, N, 1 + kCertFaces] certificate face sets
   int cap_corr;
   int B;
 };

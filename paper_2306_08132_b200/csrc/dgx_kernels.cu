@@ -94,6 +94,8 @@ struct SimEnv {
   double radius, alpha, mu, dt;
   double* point_grads;    // debug, may be null
   int* mcache;            // mesh: [gs*N] packed (face, sign) of the forward's query per point-sweep
+  double* mcert;          // mesh: [N,4] nearest-face certificates (reset per sim)
+  int* mcf;               // mesh: [N, 1 + kCertFaces]
 };
 
 // Classification of flattened position fpos (sweep*N + i) at r (FMA-built
@@ -111,8 +113,9 @@ __device__ __forceinline__ FastEval classify_bwd(const Sdf& sdf, const SimEnv& e
 }
 __device__ __forceinline__ FastEval classify_fwd(const MeshSdf& m, const SimEnv& e, int fpos, V3 r) {
   const int hint = fpos >= e.N ? (e.mcache[fpos - e.N] >> 1) : -1;
+  const int i = fpos % e.N;
   int packed;
-  const SdfQuery q = m.query_ws(r, hint, packed);
+  const SdfQuery q = m.query_cert(r, hint, packed, e.mcert + 4 * i, e.mcf + (kCertFaces + 1) * i);
   e.mcache[fpos] = packed;
   return classify_query(q, r, e.radius);
 }
@@ -805,6 +808,8 @@ __device__ double run_sim(const Sdf& sdf, SimEnv& e, V3 v_m, bool record, bool m
   bool touched = false;
   const int nwords = (N + 31) / 32;
   for (int w = lane; w < nwords; w += 32) e.bitmap[w] = 0u;
+  if (e.mcert)  // nearest-face certificates are per sim
+    for (int i = lane; i < N; i += 32) e.mcert[4 * i + 3] = -1.0;
   __syncwarp();
 
   PROF_T(tfwd);
@@ -1238,6 +1243,8 @@ __global__ void __launch_bounds__(224, CtasPerSm<Sdf>::value) fused_kernel(KHand
   e.dt = S.dt;
   e.point_grads = nullptr;
   e.mcache = buf.mesh_cache ? buf.mesh_cache + wslot * static_cast<size_t>(S.gs) * N : nullptr;
+  e.mcert = buf.mesh_cert ? buf.mesh_cert + wslot * 4 * static_cast<size_t>(N) : nullptr;
+  e.mcf = buf.mesh_cf ? buf.mesh_cf + wslot * static_cast<size_t>(kCertFaces + 1) * N : nullptr;
 
   const int k0 = mode == kModeOpt ? P.k_begin : 0;
   const int k1 = mode == kModeOpt ? P.k_end : 1;

@@ -28,6 +28,8 @@
 namespace dgx {
 
 constexpr int kMeshStack = 48;  // traversal stack; the builder rejects deeper trees (bvh.cpp uses 128)
+constexpr int kCertFaces = 24;  // nearest-face certificate: candidate set size cap
+constexpr double kCertReach = 5e-3;  // certificate gap search bound (m)
 constexpr double kInf = __builtin_huge_val();
 
 #if !defined(DGX_MESH_CNT) || !defined(__CUDA_ARCH__)
@@ -195,6 +197,8 @@ struct MeshGeom {
   double dir[3][3];      // ray directions kRayDir0, kRayDir1, third fixed direction (bvh.cpp:143-144, 250)
   double inv[3][3];      // 1 / dir, per component (bvh.cpp:219)
   double cull;           // ContactSolver::kCullMargin (sim.hpp:213)
+  const int* vf_off;     // [V+1] vertex -> incident faces (CSR), for certificates
+  const int* vf_idx;
   int nfaces;
 
   DGX_GHD MeshNode node(int i) const { return load_node(nodes + i); }
@@ -411,6 +415,121 @@ struct MeshGeom {
     return phong(r, fl);
   }
 
+  // Faces incident to any vertex of face f, sorted; -1 if more than cap.
+  DGX_GHD int ring_faces(int f, int* out, int cap) const {
+    int n = 0;
+    for (int k = 0; k < 3; ++k) {
+      const int v = load_i(tri + 3 * f + k);
+      const int b = load_i(vf_off + v), e = load_i(vf_off + v + 1);
+      for (int j = b; j < e; ++j) {
+        const int g = load_i(vf_idx + j);
+        bool seen = false;
+        for (int t = 0; t < n; ++t) seen = seen || out[t] == g;
+        if (seen) continue;
+        if (n == cap) return -1;
+        int t = n++;
+        while (t > 0 && out[t - 1] > g) { out[t] = out[t - 1]; --t; }
+        out[t] = g;
+      }
+    }
+    return n;
+  }
+
+  // Smallest squared distance from r over faces NOT in the sorted set C (n),
+  // or lim2 when none is closer (box-pruned traversal)
+  DGX_GHD double nearest_excluding(V3 r, const int* C, int n, double lim2) const {
+    double best2 = lim2;
+    int stack[kMeshStack];
+    double sb[kMeshStack];
+    int top = 0;
+    stack[top] = 0;
+    sb[top++] = node_lb2(nodes, r);
+    while (top > 0) {
+      --top;
+      if (sb[top] > best2) continue;
+      int left, right, first, count;
+      node_links(nodes + stack[top], left, right, first, count);
+      if (left < 0) {
+        for (int i = first; i < first + count; ++i) {
+          const FaceV F = load_face(faces + i);
+          int lo = 0, hi = n;  // binary search in C
+          while (lo < hi) {
+            const int mid = (lo + hi) >> 1;
+            if (C[mid] < F.f) lo = mid + 1; else hi = mid;
+          }
+          if (lo < n && C[lo] == F.f) continue;
+          FlatPoint sp;
+          closest_on_triangle(r, F.a, F.b, F.c, sp);
+          if (sp.dist2 < best2) best2 = sp.dist2;
+        }
+      } else {
+        const double dl = node_lb2(nodes + left, r), dr = node_lb2(nodes + right, r);
+        if (dl <= dr) {
+          if (dr <= best2) { stack[top] = right; sb[top++] = dr; }
+          if (dl <= best2) { stack[top] = left; sb[top++] = dl; }
+        } else {
+          if (dl <= best2) { stack[top] = left; sb[top++] = dl; }
+          if (dr <= best2) { stack[top] = right; sb[top++] = dr; }
+        }
+      }
+    }
+    return best2;
+  }
+
+  // Solver forward with a per-point nearest-face certificate (cert: rc.x,
+  // rc.y, rc.z, rad; cf: n then n sorted face ids). Valid while |r - rc| <
+  // rad: every face outside the set is then strictly farther than the
+  // certified nearest face, so the argmin (dist2, lowest id) over the set IS
+  // the global one. Otherwise the point is re-certified: warm-started nearest
+  // search, the set = faces around the nearest face's vertices, g = nearest
+  // distance outside the set (searched up to d + kCertReach), rad = (g - d)/2
+  // less a rounding allowance. The sign always comes from the ray cast.
+  DGX_GHD SdfQuery query_cert(V3 r, int hint, int& packed, double* cert, int* cf) const {
+    FlatPoint fl;
+    fl.face = -1;
+    const double rad = cert[3];
+    if (rad > 0.0) {
+      const V3 dv = V3{r.x - cert[0], r.y - cert[1], r.z - cert[2]};
+      if (dot(dv, dv) < rad * rad) {
+        DGX_MESH_CNT(28, 1);
+        const int n = cf[0];
+        double best2 = kInf;
+        int bf = -1;
+        for (int t = 0; t < n; ++t) {
+          const int f = cf[1 + t];  // ascending ids: a tie keeps the lower id
+          FlatPoint sp;
+          face_closest(r, f, sp);
+          if (sp.dist2 < best2) {
+            best2 = sp.dist2;
+            bf = f;
+            fl = sp;
+          }
+        }
+        (void)bf;
+      }
+    }
+    if (fl.face < 0) {
+      nearest_ws(r, hint, fl);
+      int C[kCertFaces];
+      const int n = ring_faces(fl.face, C, kCertFaces);
+      cert[3] = -1.0;
+      if (n > 0) {
+        const double d = dsqrt(fl.dist2);
+        const double lim = d + kCertReach;
+        const double g = dsqrt(nearest_excluding(r, C, n, lim * lim));
+        const double rr = 0.5 * (g - d) - (1e-12 + 1e-9 * (g + d));
+        if (rr > 0.0) {
+          cert[0] = r.x; cert[1] = r.y; cert[2] = r.z; cert[3] = rr;
+          cf[0] = n;
+          for (int t = 0; t < n; ++t) cf[1 + t] = C[t];
+        }
+      }
+    }
+    const SdfQuery q = phong(r, fl);
+    packed = (fl.face << 1) | (q.sign < 0 ? 1 : 0);
+    return q;
+  }
+
   // solver forward: query via nearest_ws; *packed = face << 1 | (sign < 0)
   DGX_GHD SdfQuery query_ws(V3 r, int hint, int& packed) const {
     DGX_MESH_CNT(27, 1);
@@ -447,6 +566,7 @@ struct MeshSdf {
   __device__ bool culled(V3 r, double radius) const;
   __device__ SdfQuery query_ws(V3 r, int hint, int& packed) const;
   __device__ SdfQuery query_packed(V3 r, int packed) const;
+  __device__ SdfQuery query_cert(V3 r, int hint, int& packed, double* cert, int* cf) const;
 #endif
 };
 
@@ -460,6 +580,13 @@ static __device__ __noinline__ SdfQuery mesh_query_ws(const MeshGeom* __restrict
 }
 static __device__ __noinline__ SdfQuery mesh_query_packed(const MeshGeom* __restrict__ g, V3 r, int packed) {
   return g->query_packed(r, packed);
+}
+static __device__ __noinline__ SdfQuery mesh_query_cert(const MeshGeom* __restrict__ g, V3 r, int hint, int* packed,
+                                                       double* cert, int* cf) {
+  return g->query_cert(r, hint, *packed, cert, cf);
+}
+__device__ __forceinline__ SdfQuery MeshSdf::query_cert(V3 r, int hint, int& packed, double* cert, int* cf) const {
+  return mesh_query_cert(g, r, hint, &packed, cert, cf);
 }
 __device__ __forceinline__ SdfQuery MeshSdf::query(V3 r) const { return mesh_query(g, r); }
 __device__ __forceinline__ SdfQuery MeshSdf::query_ws(V3 r, int hint, int& packed) const {

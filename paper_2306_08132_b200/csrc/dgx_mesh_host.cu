@@ -185,6 +185,15 @@ void mesh_prepare(int nv, const double* V, int nf, const int32_t* F, const doubl
   bd.build(0, nf, 0);
   out.depth = bd.depth;
   if (out.depth + 2 > kMeshStack) throw std::runtime_error("mesh: BVH too deep for the device traversal stack");
+  out.vf_off.assign(nv + 1, 0);
+  for (int i = 0; i < 3 * nf; ++i) ++out.vf_off[F[i] + 1];
+  for (int v = 0; v < nv; ++v) out.vf_off[v + 1] += out.vf_off[v];
+  out.vf_idx.assign(3 * static_cast<size_t>(nf), 0);
+  {
+    std::vector<int> fill(out.vf_off.begin(), out.vf_off.end() - 1);
+    for (int f = 0; f < nf; ++f)
+      for (int k = 0; k < 3; ++k) out.vf_idx[fill[F[3 * f + k]]++] = f;
+  }
   out.faces.resize(nf);
   for (int i = 0; i < nf; ++i) {
     const int f = bd.order[i];

@@ -13,6 +13,7 @@ struct MeshHost {
   std::vector<MeshFace> faces;  // leaf order
   std::vector<int> tri;         // [F,3]
   std::vector<double> vx, vn;   // [V,3]
+  std::vector<int> vf_off, vf_idx;  // vertex -> incident faces (CSR)
   double blo[3], bhi[3];
   int depth = 0;
 };

@@ -22,7 +22,8 @@ NAMES = {0: "forward sweeps (incl. corrections)", 1: "  apply_correction", 2: "f
 COUNTS = {16: "forward chunk iterations", 17: "forward candidate lanes", 18: "adjoint blocks", 19: "runs",
           20: "forward corrections tried", 21: "frictions applied", 22: "sims",
           23: "mesh nearest queries (lane 0)", 24: "mesh nearest node pops (lane 0)",
-          25: "mesh ray casts (lane 0)", 26: "mesh ray node pops (lane 0)", 27: "mesh exact queries (lane 0)"}
+          25: "mesh ray casts (lane 0)", 26: "mesh ray node pops (lane 0)", 27: "mesh exact queries (lane 0)",
+          28: "mesh certified queries (lane 0)"}
 
 
 def main():

@@ -420,7 +420,9 @@ int dgx_object_upload(dgx_ctx* c, const dgx_object_desc* d, dgx_object** out) {
         cuda_check(cudaMemcpy(dcells, packed.data(), packed.size() * sizeof(float), cudaMemcpyHostToDevice),
                    "grid cells upload");
         o->sdf.grd = GridSdf{nx, ny, nz, V3{d->origin[0], d->origin[1], d->origin[2]}, d->spacing, d->inv_spacing,
-                             static_cast<const float*>(o->vals.p), dcells};
+                             static_cast<const float*>(o->vals.p), dcells, static_cast<float>(d->origin[0]),
+                             static_cast<float>(d->origin[1]), static_cast<float>(d->origin[2]),
+                             static_cast<float>(d->spacing), static_cast<float>(d->inv_spacing)};
       } else if (d->kind == DGX_SDF_MESH) {
         // MeshSdf(TriMesh, alpha_phong) (sdf.cpp:17-20): validate, BVH, upload
         if (!(d->alpha_phong >= 0.0 && d->alpha_phong <= 1.0))

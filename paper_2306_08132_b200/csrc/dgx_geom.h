@@ -265,6 +265,8 @@ struct GridSdf {
   // (i,j,k) at cells[8 * ((k*(ny-1) + j)*(nx-1) + i)] in the order
   // c000 c100 c010 c110 c001 c101 c011 c111 (one 32 B sector per lookup)
   const float* cells;
+  // FP32 copies of origin / h / 1/h for the forward's FP32 pre-filter
+  float ofx, ofy, ofz, hf, inv_hf;
 
   DGX_GHD double at(int i, int j, int k) const {
 #if defined(__CUDA_ARCH__)

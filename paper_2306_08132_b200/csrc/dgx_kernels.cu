@@ -98,6 +98,13 @@ struct SimEnv {
   int* mcf;               // mesh: [N, 1 + kCertFaces]
 };
 
+// Forward classification of grids through the FP32 pre-filter (see
+// grid_inactive_f32); the other backends classify in FP64.
+template <class Sdf>
+constexpr bool kF32Prefilter = false;
+template <>
+constexpr bool kF32Prefilter<GridSdf> = true;
+
 // Classification of flattened position fpos (sweep*N + i) at r (FMA-built
 // r_local). Mesh objects: the forward's exact query is warm-started from the
 // point's face one sweep earlier and its (face, sign) recorded; the adjoint
@@ -805,6 +812,9 @@ __device__ double run_sim(const Sdf& sdf, SimEnv& e, V3 v_m, bool record, bool m
   V3 x = pred_x;
   Q4 q = pred_q;
   M3 R = rotation_matrix(q);
+  PoseF Pf{};  // FP32 copy of the pose for the grid pre-filter
+  const float radf = static_cast<float>(e.radius);
+  if constexpr (kF32Prefilter<Sdf>) Pf = pose_f32(x, R, e.O->com);
   bool touched = false;
   const int nwords = (N + 31) / 32;
   for (int w = lane; w < nwords; w += 32) e.bitmap[w] = 0u;
@@ -835,9 +845,14 @@ __device__ double run_sim(const Sdf& sdf, SimEnv& e, V3 v_m, bool record, bool m
     for (int h = 0; h < 2; ++h) {
       const int i = pos + 32 * h + lane;
       const int ic = i < N ? i : N - 1;
-      const V3 p{e.px[ic], e.py[ic], e.pz[ic]};
-      const V3 rl = ftmul(R, p - x) + e.O->com;
-      cls[h] = i < N ? classify_fwd(sdf, e, sweep * N + i, rl).cls : 1;
+      if constexpr (kF32Prefilter<Sdf>) {
+        // grids: FP32 "certainly inactive" test; everything else -> exact query
+        cls[h] = (i >= N || grid_inactive_f32(sdf, Pf, e.px[ic], e.py[ic], e.pz[ic], radf)) ? 1 : 0;
+      } else {
+        const V3 p{e.px[ic], e.py[ic], e.pz[ic]};
+        const V3 rl = ftmul(R, p - x) + e.O->com;
+        cls[h] = i < N ? classify_fwd(sdf, e, sweep * N + i, rl).cls : 1;
+      }
     }
     const unsigned cand0 = __ballot_sync(kFull, cls[0] <= 0);
     const unsigned cand1 = __ballot_sync(kFull, cls[1] <= 0);
@@ -890,6 +905,7 @@ __device__ double run_sim(const Sdf& sdf, SimEnv& e, V3 v_m, bool record, bool m
       x = co.x;
       q = co.q;
       R = rotation_matrix(q);
+      if constexpr (kF32Prefilter<Sdf>) Pf = pose_f32(x, R, e.O->com);
       touched = true;
       f_last = sweep * N + ij;
       singular_since = 0;

@@ -12,8 +12,8 @@ headline). Writes one JSON record per line to stdout.
            4096 candidates: candidate-iterations/s over a few iterations.
   config4  barrett3 x 64 procedural blob objects (64^3) x 1024 candidates
            (65,536 candidates, object-major, dgx_optimize_multi).
-  config5  sweep: 3 hands x SDF resolution {32,64,128}^3 x candidates
-           {256, 1024, 4096, 16384} (one GPU; multi-GPU runs shard candidates
+  config5  sweep: 3 hands x SDF resolution {32,64,128,256}^3 x candidates
+           {256, 1024, 4096, 16384} (1024 / 16384 at 256^3) (one GPU; multi-GPU runs shard candidates
            with no collective, so aggregate = per-GPU x N).
 
 usage: python tools/bench_configs.py [config1 config3 config4 config5]
@@ -266,10 +266,10 @@ def config5():
     for hname in ("barrett3", "allegro16", "shadow22"):
         hd = model.HandDesc.asset(hname)
         hand = api.Hand(ctx, hd)
-        for res in (32, 64, 128):
+        for res in (32, 64, 128, 256):
             od = model.blob_grid(seed=11, res=res)
             obj = api.GraspObject(ctx, od)
-            for B in (256, 1024, 4096, 16384):
+            for B in ((256, 1024, 4096, 16384) if res < 256 else (1024, 16384)):
                 q0 = init.approach_init(od, hd, B, seed=5)
                 ms, _, bad = timed_opt(ctx, [obj], hand, hd, [q0], 500, 1, 2)
                 out.append(dict(hand=hname, sdf_res=res, candidates=B, cand_iter_per_s=B / (ms * 1e-3), failed=bad))

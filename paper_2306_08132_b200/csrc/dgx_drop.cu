@@ -54,7 +54,7 @@ __device__ __forceinline__ V3 vtx(const DropObj& O, int i) {
 
 }  // namespace
 
-__global__ void __launch_bounds__(128) drop_kernel(const __grid_constant__ DropObj O, DropParams P, int B,
+__global__ void __launch_bounds__(128, 6) drop_kernel(const __grid_constant__ DropObj O, DropParams P, int B,
                                                    const double* __restrict__ in, double* __restrict__ out,
                                                    int* __restrict__ steps_out, double* __restrict__ ke_out,
                                                    double* __restrict__ stats_out, double* __restrict__ lam_all,

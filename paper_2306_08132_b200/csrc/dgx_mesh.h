@@ -494,18 +494,15 @@ struct MeshGeom {
         DGX_MESH_CNT(28, 1);
         const int n = cf[0];
         double best2 = kInf;
-        int bf = -1;
         for (int t = 0; t < n; ++t) {
           const int f = cf[1 + t];  // ascending ids: a tie keeps the lower id
           FlatPoint sp;
           face_closest(r, f, sp);
           if (sp.dist2 < best2) {
             best2 = sp.dist2;
-            bf = f;
             fl = sp;
           }
         }
-        (void)bf;
       }
     }
     if (fl.face < 0) {

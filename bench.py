@@ -271,8 +271,19 @@ def run_dgx(args, rank, world, local_rank):
     cand_total = args.candidates * world
     value = cand_total * args.steps / (max_ms * 1e-3)
 
-    # ---- end to end through the public host API (numpy in / out, synchronous) ----
-    host = dict(q=st["q"].cpu().numpy(), m=st["m"].cpu().numpy(), v=st["v"].cpu().numpy())
+    # ---- end to end through the public host API (host arrays in / out, synchronous) ----
+    # The step's inputs live in pinned host memory; the library copies them in,
+    # runs the fused iteration and copies q / m / v / status / the iterate's
+    # losses + gradient record back, every step.
+    def pinned(a):
+        t = torch.empty(a.shape, dtype=a.dtype, pin_memory=True)
+        t.copy_(a)
+        return t.numpy()
+
+    host = dict(q=pinned(st["q"].cpu()), m=pinned(st["m"].cpu()), v=pinned(st["v"].cpu()))
+    Bt = host["q"].shape[0]
+    status_h = pinned(torch.zeros(Bt, dtype=torch.int32))
+    traj_h = pinned(torch.zeros((Bt, 1, 3 + host["m"].shape[1]), dtype=torch.float64))
     ctx.set_stream(None)
     k0 = args.warmup + args.steps
     h2d = d2h = 0
@@ -282,8 +293,8 @@ def run_dgx(args, rank, world, local_rank):
     t0 = time.perf_counter()
     for s in range(args.steps):
         out = api.optimize_multi(ctx, objs, hand, host["q"], counts, proto, params, weights, opt, k_begin=k0 + s,
-                                 k_end=k0 + s + 1, adam_m=host["m"], adam_v=host["v"], record=True)
-        host.update(q=out["q"], m=out["m"], v=out["v"])
+                                 k_end=k0 + s + 1, adam_m=host["m"], adam_v=host["v"], record=True,
+                                 status=status_h, traj=traj_h, inplace=True)
         nb = host["q"].nbytes + host["m"].nbytes + host["v"].nbytes
         h2d += nb + out["status"].nbytes
         d2h += nb + out["traj"].nbytes + out["status"].nbytes
@@ -311,7 +322,9 @@ def run_dgx(args, rank, world, local_rank):
             "config": config_dict(args.candidates, world),
             "grasps_per_sec": value / ITERS,
             "e2e": {"value": e2e_value, "unit": "candidate-iterations/s",
-                    "h2d_bytes_per_step": h2d // args.steps, "d2h_bytes_per_step": d2h // args.steps},
+                    "h2d_bytes_per_step": h2d // args.steps, "d2h_bytes_per_step": d2h // args.steps,
+                    "path": "api.optimize_multi -> dgx_optimize_multi with pinned host arrays (q, adam m/v in; "
+                            "q, m, v, status, iterate losses + gradient out), synchronous, wall clock"},
             "gpu_launches": launches,
             "roofline": {"bound": "fp64", "achieved": achieved, "peak": pk.value, "unit": "TFLOP/s",
                          "frac": achieved / pk.value, "traffic": traffic,

@@ -355,14 +355,27 @@ def optimize(ctx: Context, obj: GraspObject, hand: Hand, q, protocol: StabilityP
 def optimize_multi(ctx: Context, objs: list, hand: Hand, q, counts, protocol: StabilityProtocol,
                    params: SimParams, weights: LossWeights, opt: OptConfig, k_begin: int = 0,
                    k_end: int | None = None, adam_m=None, adam_v=None, record: bool = False, flags: int | None = None,
-                   status=None):
+                   status=None, traj=None, inplace: bool = False):
     """Multi-object fused synthesis (dgx_optimize_multi): candidates object-major,
-    counts[i] for objs[i]; objects run concurrently on side streams."""
+    counts[i] for objs[i]; objects run concurrently on side streams.
+    Host arrays are copied unless inplace=True: then q / adam_m / adam_v (and
+    status / traj when given) must be C-contiguous (e.g. pinned) arrays of the
+    right dtype and are updated in place."""
     k_end = opt.iterations if k_end is None else k_end
     D = 6 + hand.J
     counts = np.ascontiguousarray(counts, np.int32)
     host = isinstance(q, np.ndarray) or not hasattr(q, "data_ptr")
-    if host:
+    if host and inplace:
+        for a, dt in ((q, np.float64), (adam_m, np.float64), (adam_v, np.float64)):
+            if not (isinstance(a, np.ndarray) and a.dtype == dt and a.flags["C_CONTIGUOUS"]):
+                raise ValueError("inplace: q, adam_m, adam_v must be C-contiguous float64 numpy arrays")
+        B = q.shape[0]
+        status = np.zeros(B, np.int32) if status is None else status
+        if record and traj is None:
+            traj = np.zeros((B, k_end - k_begin, 3 + D))
+        if not record:
+            traj = None
+    elif host:
         q = np.array(q, np.float64, copy=True, order="C").reshape(-1, 7 + hand.J)
         B = q.shape[0]
         adam_m = np.zeros((B, D)) if adam_m is None else np.array(adam_m, np.float64, copy=True, order="C")

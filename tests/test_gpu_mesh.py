@@ -72,3 +72,22 @@ def test_mesh_query_explicit_normals(ctx, oracle):
     b = api.GraspObject(ctx, model.mesh_object(V, F, vertex_normals=VN))
     P = samples(V, F, np.random.default_rng(3), 500)
     assert np.array_equal(api.sdf_query(ctx, a, P), api.sdf_query(ctx, b, P))
+
+
+@pytest.mark.parametrize("obj_name", ["sphere25", "box40", "boxgrid32"])
+def test_non_mesh_sdf_query_bit_exact(ctx, oracle, obj_name):
+    """dgx_sdf_query_batch on the analytic / grid backends vs the oracle's
+    AnySdf query (the shared definitions in csrc/dgx_geom.h evaluated on the
+    CPU): bit-exact; within=True never culls for these backends."""
+    from paper_2306_08132_b200 import api, model
+    od = {"sphere25": lambda: model.sphere(0.025), "box40": lambda: model.box((0.04, 0.04, 0.04)),
+          "boxgrid32": lambda: model.box_grid(res=32)}[obj_name]()
+    ro = oracle.RefObject.from_desc(od)
+    obj = api.GraspObject(ctx, od)
+    rng = np.random.default_rng(5)
+    P = np.concatenate([rng.uniform(-0.06, 0.06, size=(2000, 3)), rng.normal(size=(200, 3)) * 0.02])
+    for radius in (0.0, 0.003):
+        got = api.sdf_query(ctx, obj, P, radius)
+        want = np.array([ro.query(p, radius) for p in P])
+        assert np.array_equal(got, want), (obj_name, radius, np.flatnonzero(np.any(got != want, axis=1))[:5])
+        assert np.array_equal(api.sdf_query(ctx, obj, P, radius, within=True), got)

@@ -110,3 +110,26 @@ def test_multi_object_launch_matches_per_object(ctx):
         assert np.array_equal(one["m"], multi["m"][off:off + n])
         assert np.array_equal(one["traj"], multi["traj"][off:off + n])
         off += n
+
+
+def test_optimize_multi_inplace_host_path(ctx):
+    """The pinned / in-place host path of optimize_multi (bench e2e) equals the
+    copying host path and the device path."""
+    import torch
+    from paper_2306_08132_b200 import api, init, model
+    hd = model.HandDesc.asset("barrett3")
+    od = model.sphere(0.025)
+    hand, obj = api.Hand(ctx, hd), api.GraspObject(ctx, od)
+    q0 = init.approach_init(od, hd, 12, seed=9)
+    proto, params, w, opt = api.StabilityProtocol.standard(), api.SimParams(), api.LossWeights(), api.OptConfig(50)
+    counts = np.array([12], np.int32)
+    a = api.optimize_multi(ctx, [obj], hand, q0, counts, proto, params, w, opt, k_begin=0, k_end=3, record=True)
+    pin = lambda x: torch.tensor(x).pin_memory().numpy()  # noqa: E731
+    q, m, v = pin(q0), pin(np.zeros((12, 6 + hd.num_joints))), pin(np.zeros((12, 6 + hd.num_joints)))
+    b = api.optimize_multi(ctx, [obj], hand, q, counts, proto, params, w, opt, k_begin=0, k_end=3, adam_m=m,
+                           adam_v=v, record=True, inplace=True)
+    assert b["q"] is q and np.array_equal(q, a["q"]) and np.array_equal(m, a["m"]) and np.array_equal(v, a["v"])
+    assert np.array_equal(b["traj"], a["traj"]) and not np.any(b["status"])
+    with pytest.raises(ValueError):
+        api.optimize_multi(ctx, [obj], hand, q0.astype(np.float32), counts, proto, params, w, opt, k_begin=0,
+                           k_end=1, adam_m=m, adam_v=v, inplace=True)

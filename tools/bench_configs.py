@@ -235,6 +235,27 @@ def metrics_sweep():
                 top10_mean_CA_cm2_5mm=float(np.mean([repf[i][4]["contact_area_cm2"] for i in top])))
 
 
+def mesh_scaling():
+    """SPEC ACCEPTANCE 7's BVH check on the GPU mesh backend: per-iteration
+    cost vs face count (icospheres of 1280 / 5120 / 20480 faces, barrett3,
+    2048 candidates)."""
+    hd = model.HandDesc.asset("barrett3")
+    ctx = api.Context(0)
+    hand = api.Hand(ctx, hd)
+    rows = []
+    for sub in (3, 4, 5):
+        V, F = model.icosphere_mesh(0.025, sub)
+        od = model.mesh_object(V, F)
+        obj = api.GraspObject(ctx, od)
+        B = 2048
+        q0 = init.approach_init(od, hd, B, seed=1)
+        ms, _, bad = timed_opt(ctx, [obj], hand, hd, [q0], 500, 1, 3)
+        rows.append(dict(faces=int(F.shape[0]), cand_iter_per_s=B * 2 / (ms * 1e-3), ms_per_iteration=ms / 2,
+                         failed=bad))
+    return dict(config="mesh_scaling", workload="barrett3 on icosphere meshes, 2048 candidates, 2 iterations",
+                rows=rows)
+
+
 def config3():
     hd = model.HandDesc.asset("shadow22_dense")
     od = model.blob_grid(seed=3, res=128)
@@ -277,7 +298,8 @@ def config5():
 
 
 def main():
-    which = sys.argv[1:] or ["config1", "config1_mesh", "config3", "config4", "config5", "scene_drop", "metrics_sweep"]
+    which = sys.argv[1:] or ["config1", "config1_mesh", "config3", "config4", "config5", "scene_drop", "metrics_sweep",
+                                 "mesh_scaling"]
     for w in which:
         t = time.time()
         rec = globals()[w]()

@@ -235,3 +235,31 @@ def test_invalid_arguments(ctx, oracle):
                                           api.SimParams(dilation_radius=0.01))
     rl, ds, dr, dl = oracle.loss_gradient(c.ro, c.rh, bad[0], oracle.default_params(dilation_radius=0.01))
     assert np.array_equal(losses[0], rl) and np.array_equal(grads[0, 0], ds)
+
+
+def test_nonfinite_adjoint_matches_reference(ctx, oracle):
+    """Error behaviour: at an iterate (tests/golden/errors, from
+    tools/make_nonfinite_fixture.py) where the reference's tape throws
+    "non-finite adjoint" (tape.cpp:35-38) on a procedural blob mesh, the GPU
+    reports DGX_E_NONFINITE_GRAD for that candidate; the forward-only objective
+    still matches bit-exactly."""
+    from paper_2306_08132_b200 import api, capi, model
+    z = np.load(os.path.join(ROOT, "tests", "golden", "errors", "nonfinite_adjoint_blob.npz"))
+    rad, sub, amp, seed = z["blob"]
+    ro_mesh = oracle.RefObject.blob_mesh(float(rad), int(sub), float(amp), int(seed))
+    od = model.mesh_object(*ro_mesh.mesh_export()[:2])
+    ro = oracle.RefObject.from_desc(od)
+    rh = oracle.RefHand.barrett3()
+    hd = model.HandDesc.from_dict("barrett3", rh.desc)
+    hand, obj = api.Hand(ctx, hd), api.GraspObject(ctx, od)
+    r = float(z["radius"])
+    with pytest.raises(oracle.RefError, match="non-finite adjoint"):
+        oracle.loss_gradient(ro, rh, z["q"], oracle.default_params(dilation_radius=r))
+    losses, grads, st = api.loss_gradient(ctx, obj, hand, z["q"][None, :], api.StabilityProtocol.standard(),
+                                          api.SimParams(dilation_radius=r))
+    assert capi.STATUS_NAMES[int(st[0])] == "tape: non-finite adjoint"
+    # the forward-only objective is unaffected and bit-exact
+    el, _, st2 = api.evaluate_losses(ctx, obj, hand, z["q"][None, :], api.StabilityProtocol.standard(),
+                                     api.SimParams(dilation_radius=r))
+    assert not np.any(st2)
+    assert np.array_equal(el[0], oracle.evaluate_losses(ro, rh, z["q"], oracle.default_params(dilation_radius=r)))

@@ -235,6 +235,41 @@ def metrics_sweep():
                 top10_mean_CA_cm2_5mm=float(np.mean([repf[i][4]["contact_area_cm2"] for i in top])))
 
 
+def acceptance5():
+    """SPEC ACCEPTANCE 5 on the GPU path: 20 seeds x 3 desk-scale MESH objects
+    (cube, cylinder, blob) with the 3-finger hand, 200 iterations. Fraction of
+    runs ending with (a) more 5 mm contacts than the initialization, (b)
+    L_stable reduced >= 50%, (c) epsilon > 0 at 5 mm; the spec asks >= 70%."""
+    from oracle import ref
+    from paper_2306_08132_b200 import metrics
+    hd = model.HandDesc.asset("barrett3")
+    ctx = api.Context(0)
+    hand = api.Hand(ctx, hd)
+    objs = {"cube40": model.mesh_object(*model.box_mesh((0.04, 0.04, 0.04))),
+            "cylinder": model.mesh_object(*ref.RefObject.cylinder_mesh(0.0175, 0.07, 32).mesh_export()[:2]),
+            "blob": model.mesh_object(*ref.RefObject.blob_mesh(0.021, 3, 0.5, 7).mesh_export()[:2])}
+    rows = []
+    proto, params = api.StabilityProtocol.standard(), api.SimParams()
+    for name, od in objs.items():
+        obj = api.GraspObject(ctx, od)
+        B, K = 20, 200
+        q0 = init.approach_init(od, hd, B, seed=5)
+        ms, qf, bad = timed_opt(ctx, [obj], hand, hd, [q0], K, 1, K)
+        l0, _, _ = api.evaluate_losses(ctx, obj, hand, q0, proto, params)
+        lf, _, _ = api.evaluate_losses(ctx, obj, hand, qf, proto, params)
+        r0 = metrics.evaluate(ctx, hand, obj, q0, (5.0,))
+        rf = metrics.evaluate(ctx, hand, obj, qf, (5.0,))
+        a = np.array([rf[b][0]["contacts"] > r0[b][0]["contacts"] for b in range(B)])
+        bb = lf[:, 0] <= 0.5 * l0[:, 0]
+        c = np.array([rf[b][0]["epsilon"] > 0 for b in range(B)])
+        rows.append(dict(object=name, runs=B, more_contacts=float(a.mean()), stable_halved=float(bb.mean()),
+                         eps_positive=float(c.mean()), all_three=float((a & bb & c).mean()),
+                         mean_stable_init=float(l0[:, 0].mean()), mean_stable_final=float(lf[:, 0].mean()),
+                         gpu_s=ms * 1e-3, failed=bad))
+    return dict(config="acceptance5", workload="barrett3, 20 seeds x {cube, cylinder, blob} meshes, 200 iterations",
+                rows=rows)
+
+
 def mesh_scaling():
     """SPEC ACCEPTANCE 7's BVH check on the GPU mesh backend: per-iteration
     cost vs face count (icospheres of 1280 / 5120 / 20480 faces, barrett3,

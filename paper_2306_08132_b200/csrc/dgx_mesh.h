@@ -35,6 +35,11 @@ constexpr double kInf = __builtin_huge_val();
 #if !defined(DGX_MESH_CNT) || !defined(__CUDA_ARCH__)
 #undef DGX_MESH_CNT
 #define DGX_MESH_CNT(r, n)
+#define DGX_MESH_T(v)
+#define DGX_MESH_CYC(r, v)
+#else
+#define DGX_MESH_T(v) const long long v = clock64()
+#define DGX_MESH_CYC(r, v) DGX_MESH_CNT(r, clock64() - (v))
 #endif
 
 struct alignas(16) MeshNode {    // 64 B
@@ -488,6 +493,7 @@ struct MeshGeom {
     FlatPoint fl;
     fl.face = -1;
     const double rad = cert[3];
+    DGX_MESH_T(tq0);
     if (rad > 0.0) {
       const V3 dv = V3{r.x - cert[0], r.y - cert[1], r.z - cert[2]};
       if (dot(dv, dv) < rad * rad) {
@@ -505,6 +511,8 @@ struct MeshGeom {
         }
       }
     }
+    DGX_MESH_CYC(29, tq0);
+    DGX_MESH_T(tq1);
     if (fl.face < 0) {
       nearest_ws(r, hint, fl);
       int C[kCertFaces];
@@ -522,7 +530,10 @@ struct MeshGeom {
         }
       }
     }
+    DGX_MESH_CYC(30, tq1);
+    DGX_MESH_T(tq2);
     const SdfQuery q = phong(r, fl);
+    DGX_MESH_CYC(31, tq2);
     packed = (fl.face << 1) | (q.sign < 0 ? 1 : 0);
     return q;
   }

@@ -23,7 +23,8 @@ COUNTS = {16: "forward chunk iterations", 17: "forward candidate lanes", 18: "ad
           20: "forward corrections tried", 21: "frictions applied", 22: "sims",
           23: "mesh nearest queries (lane 0)", 24: "mesh nearest node pops (lane 0)",
           25: "mesh ray casts (lane 0)", 26: "mesh ray node pops (lane 0)", 27: "mesh exact queries (lane 0)",
-          28: "mesh certified queries (lane 0)"}
+          28: "mesh certified queries (lane 0)", 29: "mesh cycles: certified argmin (lane 0)",
+          30: "mesh cycles: re-certification (lane 0)", 31: "mesh cycles: phong + ray-cast sign (lane 0)"}
 
 
 def main():

@@ -133,3 +133,23 @@ def test_optimize_multi_inplace_host_path(ctx):
     with pytest.raises(ValueError):
         api.optimize_multi(ctx, [obj], hand, q0.astype(np.float32), counts, proto, params, w, opt, k_begin=0,
                            k_end=1, adam_m=m, adam_v=v, inplace=True)
+
+
+def test_optimize_multi_mixed_backends(ctx):
+    """One dgx_optimize_multi call over a mesh, a grid and an analytic object
+    (each on its own side stream with its own scratch, including the mesh
+    caches) equals separate single-object runs bit-for-bit."""
+    from paper_2306_08132_b200 import api, init, model
+    hd = model.HandDesc.asset("barrett3")
+    hand = api.Hand(ctx, hd)
+    ods = [model.mesh_object(*model.icosphere_mesh(0.025, 2)), model.box_grid(res=32), model.sphere(0.025)]
+    objs = [api.GraspObject(ctx, o) for o in ods]
+    qs = [init.approach_init(o, hd, 5, seed=31 + i) for i, o in enumerate(ods)]
+    proto, params, w, opt = api.StabilityProtocol.standard(), api.SimParams(), api.LossWeights(), api.OptConfig(50)
+    multi = api.optimize_multi(ctx, objs, hand, np.concatenate(qs), np.array([5, 5, 5], np.int32), proto, params, w,
+                               opt, k_begin=0, k_end=3)
+    assert not np.any(multi["status"])
+    for i, (o, q) in enumerate(zip(objs, qs)):
+        one = api.optimize(ctx, o, hand, q, proto, params, w, opt, k_begin=0, k_end=3)
+        assert np.array_equal(multi["q"][5 * i:5 * i + 5], one["q"]), i
+        assert np.array_equal(multi["m"][5 * i:5 * i + 5], one["m"]), i

@@ -401,6 +401,8 @@ int dgx_object_upload(dgx_ctx* c, const dgx_object_desc* d, dgx_object** out) {
         const int nx = d->dims[0], ny = d->dims[1], nz = d->dims[2];
         const size_t n = static_cast<size_t>(nx) * ny * nz;
         const size_t nc = static_cast<size_t>(nx - 1) * (ny - 1) * (nz - 1);
+        if (8 * nc >= (size_t(1) << 31) || n >= (size_t(1) << 31))
+          throw DgxError(DGX_E_UNSUPPORTED, "grid: more than 2^28 cells (32-bit cell offsets)");
         // node values (host-layout copy) + the corner-packed cells the kernels read
         const size_t vbytes = (n * sizeof(float) + 255) & ~size_t(255);
         o->vals.ensure(vbytes + nc * 8 * sizeof(float));
@@ -427,6 +429,8 @@ int dgx_object_upload(dgx_ctx* c, const dgx_object_desc* d, dgx_object** out) {
         // MeshSdf(TriMesh, alpha_phong) (sdf.cpp:17-20): validate, BVH, upload
         if (!(d->alpha_phong >= 0.0 && d->alpha_phong <= 1.0))
           throw std::invalid_argument("alpha_phong must be in [0,1]");
+        if (d->num_faces >= (1 << 30))
+          throw DgxError(DGX_E_UNSUPPORTED, "mesh: more than 2^30 faces (packed face ids)");
         MeshHost mh;
         mesh_prepare(d->num_vertices, d->vertices, d->num_faces, d->faces, d->vertex_normals, mh);
         auto rnd = [](size_t x) { return (x + 255) & ~size_t(255); };

@@ -148,9 +148,8 @@ KSim make_sim(const dgx_params* p, bool eval) {
   return s;
 }
 
-// grid of persistent CTAs and the scratch it needs
-int prepare(dgx_ctx* c, Scratch& sc, const dgx_hand* h, const dgx_object* o, KSim& S, int B, KBuf& buf,
-            int& smem) {
+// adjoint staging length S.seg_max; returns the adjoint kernel's shared memory
+int choose_staging(const dgx_hand* h, const dgx_object* o, KSim& S) {
   const int M = S.M;
   // longest adjoint segment whose staging still fits one CTA's shared memory
   S.seg_max = 0;
@@ -171,9 +170,16 @@ int prepare(dgx_ctx* c, Scratch& sc, const dgx_hand* h, const dgx_object* o, KSi
   }
   if (S.seg_max == 0)
     throw DgxError(DGX_E_UNSUPPORTED, "hand too large for one CTA's shared memory (N=" + std::to_string(h->N) + ")");
-  smem = SmemLayout(h->N, h->L, M, S.seg_max).total;
+  return SmemLayout(h->N, h->L, M, S.seg_max).total;
+}
+
+// grid of persistent CTAs and the scratch it needs (fused execution)
+int prepare(dgx_ctx* c, Scratch& sc, const dgx_hand* h, const dgx_object* o, KSim& S, int B, KBuf& buf,
+            int& smem) {
+  const int M = S.M;
+  smem = choose_staging(h, o, S);
   int per_sm = 0;
-  cuda_check(fused_occupancy(o->kind, M, smem, &per_sm), "occupancy");
+  cuda_check(fused_occupancy(o->kind, M, smem, kPhaseFused, &per_sm), "occupancy");
   if (per_sm < 1) throw DgxError(DGX_E_UNSUPPORTED, "fused kernel cannot be resident (registers/smem)");
   int grid = c->num_sms * per_sm;
   if (grid > B) grid = B;
@@ -186,6 +192,8 @@ int prepare(dgx_ctx* c, Scratch& sc, const dgx_hand* h, const dgx_object* o, KSi
   buf.slots = static_cast<SlotRec*>(sc.slots.p);
   buf.slot_of_point = reinterpret_cast<int*>(buf.slots + per);
   buf.fric_order = buf.slot_of_point + per;
+  buf.slot_stride = h->N;
+  buf.fwd = nullptr;
   sc.ftg.ensure(nws * 6 * static_cast<size_t>(h->L) * sizeof(double));
   buf.ft_global = static_cast<double*>(sc.ftg.p);
   buf.mesh_cache = nullptr;
@@ -205,6 +213,109 @@ int prepare(dgx_ctx* c, Scratch& sc, const dgx_hand* h, const dgx_object* o, KSi
   buf.cap_corr = c->cap_corr;
   buf.B = B;
   return grid;
+}
+
+// Split execution for the analytic and grid backends: per
+// chunk of candidates the forward kernel (kFwdCtasPerSm CTAs per SM: its
+// register budget is not set by the adjoint) and then the adjoint kernel,
+// handing over through FwdRec and per-(candidate, sim) logs. Mesh objects run
+// fused. DGX_FUSED=1 forces the fused kernel everywhere (A/B measurements).
+bool use_split(const dgx_object* o) {
+  static const bool fused_env = std::getenv("DGX_FUSED") != nullptr;
+  return split_capable(o->kind) && !fused_env;
+}
+
+struct SplitGrid {
+  int chunk, grid_f, grid_a, smem_f, smem_a;
+};
+
+SplitGrid prepare_split(dgx_ctx* c, Scratch& sc, const dgx_hand* h, const dgx_object* o, KSim& S, int B,
+                        bool record, KBuf& buf) {
+  const int M = S.M, N = h->N;
+  SplitGrid g{};
+  g.smem_a = choose_staging(h, o, S);
+  g.smem_f = SmemLayout(N, h->L, M, 0).total;
+  int per_f = 0, per_a = 1;
+  cuda_check(fused_occupancy(o->kind, M, g.smem_f, kPhaseFwd, &per_f), "occupancy");
+  if (record) cuda_check(fused_occupancy(o->kind, M, g.smem_a, kPhaseAdj, &per_a), "occupancy");
+  if (per_f < 1 || per_a < 1) throw DgxError(DGX_E_UNSUPPORTED, "split kernels cannot be resident (registers/smem)");
+  g.grid_f = c->num_sms * per_f;
+  g.grid_a = c->num_sms * per_a;
+  // logs live per (candidate, sim) for one chunk: ~(cap_corr + 1) x 372 B + 8 N B per sim
+  g.chunk = std::max(1, std::min(B, 4 * std::max(g.grid_f, g.grid_a)));
+  g.grid_f = std::min(g.grid_f, g.chunk);
+  g.grid_a = std::min(g.grid_a, g.chunk);
+  const size_t nws = static_cast<size_t>(g.chunk) * M;
+  const size_t cap = static_cast<size_t>(c->cap_corr), ss = cap + 1;  // nslot <= ncorr <= cap_corr
+  sc.corr.ensure(nws * cap * sizeof(CorrRec));
+  sc.slots.ensure(nws * (ss * sizeof(SlotRec) + sizeof(FwdRec) + (ss + N) * sizeof(int)));
+  char* base = static_cast<char*>(sc.slots.p);
+  buf.corr = static_cast<CorrRec*>(sc.corr.p);
+  buf.slots = reinterpret_cast<SlotRec*>(base);
+  buf.fwd = reinterpret_cast<FwdRec*>(base + nws * ss * sizeof(SlotRec));
+  buf.slot_of_point = reinterpret_cast<int*>(buf.fwd + nws);
+  buf.fric_order = buf.slot_of_point + nws * N;
+  buf.slot_stride = static_cast<int>(ss);
+  sc.ftg.ensure(static_cast<size_t>(g.grid_a) * M * 6 * static_cast<size_t>(h->L) * sizeof(double));
+  buf.ft_global = static_cast<double*>(sc.ftg.p);
+  buf.mesh_cache = nullptr;
+  buf.mesh_cert = nullptr;
+  buf.mesh_cf = nullptr;
+  buf.cap_corr = c->cap_corr;
+  return g;
+}
+
+// Every launch for B candidates whose per-candidate arrays start at buf's
+// pointers, on stream st with scratch sc.
+void launch_range(dgx_ctx* c, Scratch& sc, const dgx_hand* h, const dgx_object* o, KSim S, KOpt P, KBuf buf,
+                  int B, int mode, cudaStream_t st) {
+  const int M = S.M, D = 6 + h->J, Qd = 7 + h->J, N = h->N;
+  if (mode == kModeOpt) {
+    P.traj_k0 = P.k_begin;
+    P.traj_rows = P.k_end - P.k_begin;
+  }
+  if (!use_split(o) || (mode == kModeOpt && P.k_end == P.k_begin)) {
+    int smem = 0;
+    const int grid = prepare(c, sc, h, o, S, B, buf, smem);
+    cuda_check(launch_fused(h->k, o->k, o->sdf, S, P, buf, mode, kPhaseFused, grid, smem, st), "fused_kernel");
+    ++c->launches;
+    return;
+  }
+  const bool record = mode != kModeEval;
+  const SplitGrid g = prepare_split(c, sc, h, o, S, B, record, buf);
+  const int k0 = mode == kModeOpt ? P.k_begin : 0, k1 = mode == kModeOpt ? P.k_end : 1;
+  for (int b0 = 0; b0 < B; b0 += g.chunk) {
+    const int nb = std::min(g.chunk, B - b0);
+    const size_t o0 = static_cast<size_t>(b0);
+    auto off = [&](auto* p, size_t per) { return p ? p + o0 * per : p; };
+    KBuf cb = buf;
+    cb.B = nb;
+    cb.q = off(buf.q, Qd);
+    cb.adam_m = off(buf.adam_m, D);
+    cb.adam_v = off(buf.adam_v, D);
+    cb.losses = off(buf.losses, 3);
+    cb.grads = off(buf.grads, 3 * static_cast<size_t>(D));
+    cb.stats = off(buf.stats, static_cast<size_t>(M) * 5);
+    cb.sim_res = off(buf.sim_res, M);
+    cb.sim_grads = off(buf.sim_grads, static_cast<size_t>(M) * D);
+    cb.point_grads = off(buf.point_grads, static_cast<size_t>(M) * N * 3);
+    cb.traj = off(buf.traj, static_cast<size_t>(P.traj_rows) * (3 + D));
+    cb.status = off(buf.status, 1);
+    for (int k = k0; k < k1; ++k) {
+      KOpt Pk = P;
+      if (mode == kModeOpt) {
+        Pk.k_begin = k;
+        Pk.k_end = k + 1;
+      }
+      cuda_check(launch_fused(h->k, o->k, o->sdf, S, Pk, cb, mode, kPhaseFwd, std::min(g.grid_f, nb), g.smem_f, st),
+                 "forward kernel");
+      ++c->launches;
+      if (!record) continue;
+      cuda_check(launch_fused(h->k, o->k, o->sdf, S, Pk, cb, mode, kPhaseAdj, std::min(g.grid_a, nb), g.smem_a, st),
+                 "adjoint kernel");
+      ++c->launches;
+    }
+  }
 }
 
 // host <-> device staging for non-device-pointer calls
@@ -673,11 +784,7 @@ static void run_fused(dgx_ctx* c, const dgx_hand* h, const dgx_object* o, int32_
   if (!status) throw DgxError(DGX_E_INVALID, "status is NULL");
   buf.status = s.out(status, static_cast<size_t>(B));
   if (point_grads) cuda_check(cudaMemsetAsync(buf.point_grads, 0, 24ull * B * M * N, c->stream), "memset");
-  int smem = 0;
-  int grid = prepare(c, c->scratch, h, o, S, B, buf, smem);
-  cuda_check(launch_fused(h->k, o->k, o->sdf, S, P, buf, mode, grid, smem, c->stream),
-             "fused_kernel");
-  ++c->launches;
+  launch_range(c, c->scratch, h, o, S, P, buf, B, mode, c->stream);
   s.finish(flags);
 }
 
@@ -778,11 +885,7 @@ int dgx_optimize_multi(dgx_ctx* c, const dgx_hand* h, int32_t n_obj, const dgx_o
       buf.adam_v = dv + off * D;
       buf.traj = dt ? dt + off * steps * (3 + D) : nullptr;
       buf.status = ds + off;
-      int smem = 0;
-      const int grid = prepare(c, sub.scratch, h, objs[i], S, Bi, buf, smem);
-      cuda_check(launch_fused(h->k, objs[i]->k, objs[i]->sdf, S, P, buf, kModeOpt, grid, smem, sub.stream),
-                 "fused_kernel");
-      ++c->launches;
+      launch_range(c, sub.scratch, h, objs[i], S, P, buf, Bi, kModeOpt, sub.stream);
       off += Bi;
     }
     for (int k = 0; k < P_streams; ++k) {

@@ -12,6 +12,13 @@ constexpr int kSegMaxCap = 16;    // max points per lane segment in the adjoint
 
 enum Mode : int { kModeGrad = 0, kModeEval = 1, kModeOpt = 2 };
 
+// Execution phases of one candidate-iteration (DESIGN.md §3 "split
+// execution"): the fused kernel runs both halves in one warp per sim; the
+// split pair runs the forward sweep at a higher occupancy (its register
+// budget is not set by the adjoint) and hands over through FwdRec + the
+// per-(candidate, sim) logs.
+enum Phase : int { kPhaseFused = 0, kPhaseFwd = 1, kPhaseAdj = 2 };
+
 enum Status : int {
   kOk = 0,
   kNonFiniteLoss = 1,
@@ -57,6 +64,15 @@ struct SlotRec {
   int pad;
 };
 
+// Forward state handed from the forward kernel to the adjoint kernel, per
+// (candidate, sim): the state after the solve (sim.hpp:188-196) and log sizes.
+struct FwdRec {
+  double x[3];
+  double q[4];
+  double residual;
+  int ncorr, nslot, nfric, touched, status, pad;
+};
+
 struct KHand {
   int L, J, N;
   const int* topo;
@@ -90,6 +106,7 @@ struct KSim {
 struct KOpt {
   int iters, k_begin, k_end, record;
   double r0, lr, beta1, beta2, eps;
+  int traj_k0, traj_rows;  // traj row of iterate k: b * traj_rows + (k - traj_k0)
 };
 
 struct KBuf {
@@ -108,6 +125,8 @@ struct KBuf {
   SlotRec* slots;       // [grid, M, N]  contact slots (one per hand point at most)
   int* slot_of_point;   // [grid, M, N]
   int* fric_order;      // [grid, M, N]
+  FwdRec* fwd;          // [B, M] split execution only
+  int slot_stride;      // slots / fric_order entries per sim (N fused, cap_corr + 1 split)
   double* ft_global;    // [grid, M, L*6] adjoint link-sum spill buffers
   int* mesh_cache;      // [grid, M, gs*N] mesh objects: forward (face << 1 | inside) per point-sweep
   double* mesh_cert;    // [grid, M, N, 4] mesh objects: nearest-face certificate centre + radius
@@ -153,9 +172,12 @@ struct SdfSet {
   GridSdf grd;
   MeshSdf mesh;
 };
+// phase: kPhaseFused (any backend) or kPhaseFwd / kPhaseAdj (analytic and grid
+// backends; see split_capable)
 cudaError_t launch_fused(const KHand& H, const KObj& O, const SdfSet& sdf, const KSim& S, const KOpt& P,
-                         const KBuf& buf, int mode, int grid, int smem, cudaStream_t st);
-cudaError_t fused_occupancy(int kind, int M, int smem, int* blocks_per_sm);
+                         const KBuf& buf, int mode, int phase, int grid, int smem, cudaStream_t st);
+cudaError_t fused_occupancy(int kind, int M, int smem, int phase, int* blocks_per_sm);
+inline bool split_capable(int kind) { return kind != kSdfMesh; }
 // out[n, 8] = rho - radius, grad (3), proxy (3), sign per point (MeshSdf::dilated,
 // sdf.cpp:62-67); within != 0: dilated_within (sdf.cpp:69-81), culled points
 // report sign 0 and rho = +inf

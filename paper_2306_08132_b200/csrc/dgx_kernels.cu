@@ -27,6 +27,7 @@
 // Built with --fmad=false: every forward value is the same IEEE op sequence
 // as the reference, so activations / corrections are bit-exact. Adjoint code
 // uses explicit fma().
+#include <type_traits>
 #include <cuda_runtime.h>
 
 #include <cstdint>
@@ -795,9 +796,14 @@ __device__ __forceinline__ CorrAdj correction_adjoint(const Sdf& sdf, const SimE
 
 // One perturbation simulation (losses.hpp:47-57 with T = 1), forward and,
 // when `record`, its adjoint. Returns the residual; status via `status`.
-template <class Sdf>
+//
+// Phase (split execution): kPhaseFused runs forward and adjoint
+// in the same warp; kPhaseFwd runs the forward only and stores the state the
+// adjoint needs in *rec (its logs stay in the per-(candidate, sim) scratch);
+// kPhaseAdj skips the forward, reloads *rec and runs the adjoint.
+template <int Phase, class Sdf>
 __device__ double run_sim(const Sdf& sdf, SimEnv& e, V3 v_m, bool record, bool measure_residual, SimStats& st,
-                          int& status, FtAcc& acc) {
+                          int& status, FtAcc& acc, FwdRec* rec) {
   const int lane = e.lane, N = e.N;
   // canonical_state (rigid.hpp:29-33) with xdot = v_m; predict (sim.hpp:74-83)
   const V3 prev_x = e.O->com;
@@ -811,159 +817,168 @@ __device__ double run_sim(const Sdf& sdf, SimEnv& e, V3 v_m, bool record, bool m
   // state has thetadot = 0, so every perturbation predicts the same pose)
   V3 x = pred_x;
   Q4 q = pred_q;
-  M3 R = rotation_matrix(q);
-  PoseF Pf{};  // FP32 copy of the pose for the grid pre-filter
-  const float radf = static_cast<float>(e.radius);
-  if constexpr (kF32Prefilter<Sdf>) Pf = pose_f32(x, R, e.O->com);
   bool touched = false;
+  int ncorr = 0, nslot = 0, nfric = 0;
   const int nwords = (N + 31) / 32;
-  for (int w = lane; w < nwords; w += 32) e.bitmap[w] = 0u;
-  if (e.mcert)  // nearest-face certificates are per sim
-    for (int i = lane; i < N; i += 32) e.mcert[4 * i + 3] = -1.0;
-  __syncwarp();
+  if constexpr (Phase == kPhaseAdj) {
+    x = V3{rec->x[0], rec->x[1], rec->x[2]};
+    q = Q4{rec->q[0], rec->q[1], rec->q[2], rec->q[3]};
+    touched = rec->touched != 0;
+    ncorr = rec->ncorr;
+    nslot = rec->nslot;
+    nfric = rec->nfric;
+    status = rec->status;
+    if (status != kOk) return rec->residual;
+  } else {
+    M3 R = rotation_matrix(q);
+    PoseF Pf{};  // FP32 copy of the pose for the grid pre-filter
+    const float radf = static_cast<float>(e.radius);
+    if constexpr (kF32Prefilter<Sdf>) Pf = pose_f32(x, R, e.O->com);
+    for (int w = lane; w < nwords; w += 32) e.bitmap[w] = 0u;
+    if (e.mcert)  // nearest-face certificates are per sim
+      for (int i = lane; i < N; i += 32) e.mcert[4 * i + 3] = -1.0;
+    __syncwarp();
 
-  PROF_T(tfwd);
-  // ---- Gauss-Seidel sweeps (sim.hpp:157-186) -------------------------------
-  // Two chunks of 32 consecutive points are classified against the current
-  // state (independent straight-line work: ILP); only candidates near /
-  // inside the dilated surface run the exact query; the first exact-active
-  // point is applied and evaluation restarts right after it. Inactive points
-  // change no forward value (sim.hpp:105-125), so this is the sequential sweep.
-  int ncorr = 0, nslot = 0;
-  int pos = 0, sweep = 0;
-  // Quiet window: once N consecutive positions pass with no applied
-  // correction (and no singular skip, to keep SolveStats exact), every later
-  // position repeats an earlier inactive decision under the same state: the
-  // remaining sweeps are skipped (and the adjoint folds them, run_sim below).
-  int f_last = -1, singular_since = 0;
-  while (sweep < e.gs) {
-#if defined(DGX_QUIET) || defined(DGX_QUIET_FWD)  // exact
-    if (sweep * N + pos - f_last - 1 >= N && singular_since == 0) break;
-#endif
-    int cls[2];
-#pragma unroll
-    for (int h = 0; h < 2; ++h) {
-      const int i = pos + 32 * h + lane;
-      const int ic = i < N ? i : N - 1;
-      if constexpr (kF32Prefilter<Sdf>) {
-        // grids: FP32 "certainly inactive" test; everything else -> exact query
-        cls[h] = (i >= N || grid_inactive_f32(sdf, Pf, e.px[ic], e.py[ic], e.pz[ic], radf)) ? 1 : 0;
-      } else {
-        const V3 p{e.px[ic], e.py[ic], e.pz[ic]};
-        const V3 rl = ftmul(R, p - x) + e.O->com;
-        cls[h] = i < N ? classify_fwd(sdf, e, sweep * N + i, rl).cls : 1;
-      }
-    }
-    const unsigned cand0 = __ballot_sync(kFull, cls[0] <= 0);
-    const unsigned cand1 = __ballot_sync(kFull, cls[1] <= 0);
-    PROF_CNT(16, 1);
-    PROF_CNT(17, __popc(cand0) + __popc(cand1));
-    if ((cand0 | cand1) == 0u) {
-      pos += 64;
-      if (pos >= N) { pos = 0; ++sweep; }
-      continue;
-    }
-    PointEval pe;
-    int hsel = -1;
-    unsigned mask = 0u;
-#pragma unroll 1
-    for (int h = 0; h < 2; ++h) {
-      if ((h ? cand1 : cand0) == 0u) continue;
-      const int i = pos + 32 * h + lane;
-      bool act = false;
-      if ((h ? cls[1] : cls[0]) <= 0) {
-        eval_point(sdf, e, i, x, R, record, pe);
-        act = record ? (pe.rho_d < 0.0) : !(pe.rho_d >= 0.0);
-      }
-      mask = __ballot_sync(kFull, act);
-      if (mask != 0u) {
-        hsel = h;
-        break;
-      }
-    }
-    if (hsel < 0) {
-      pos += 64;
-      if (pos >= N) { pos = 0; ++sweep; }
-      continue;
-    }
-    const int j = __ffs(mask) - 1;
-    const int ij = pos + 32 * hsel + j;
-    const V3 rel = shfl(pe.rel, j);
-    const V3 g = shfl(pe.q.grad, j);
-    const V3 pj = shfl(pe.p, j);
-    const double C = -shfl(pe.rho_d, j);
-    const V3 dxj = shfl(pe.rl - pe.q.proxy, j);
-    const int sgj = __shfl_sync(kFull, pe.q.sign, j);
-    const int fbj = __shfl_sync(kFull, pe.fb ? 1 : 0, j);
-    // apply_contact (sim.hpp:215-245), out of line (rare path)
-    PROF_T(tc);
-    const CorrOut co = apply_correction(e, CorrIn{x, q, rel, g, pj, dxj, C, ij, sweep * N + ij, ncorr, nslot, sgj, fbj});
-    PROF_ACC(1, tc);
-    PROF_CNT(20, 1);
-    if (co.status != kOk) { status = co.status; return 0.0; }
-    if (co.applied) {
-      x = co.x;
-      q = co.q;
-      R = rotation_matrix(q);
-      if constexpr (kF32Prefilter<Sdf>) Pf = pose_f32(x, R, e.O->com);
-      touched = true;
-      f_last = sweep * N + ij;
-      singular_since = 0;
-      ++ncorr;
-      nslot = co.nslot;
-      ++st.corrections;
-      st.active += co.new_contact;
-    } else {
-      ++st.singular;
-      ++singular_since;
-    }
-    pos = ij + 1;
-    if (pos >= N) { pos = 0; ++sweep; }
-  }
-
-  __syncwarp();  // order the forward's mesh-cache stores before the adjoint's loads
-  PROF_ACC(0, tfwd);
-  PROF_T(tfr);
-  // ---- friction (sim.hpp:188-196), active slots in point order -------------
-  int nfric = 0;
-  if (e.mu > 0.0) {
-    for (int wd = 0; wd < nwords; ++wd) {
-      unsigned bits = e.bitmap[wd];
-      while (bits) {
-        const int b = __ffs(bits) - 1;
-        bits &= bits - 1u;
-        const int pt = wd * 32 + b;
-        const int slot = e.slot_of_point[pt];
-        const SlotRec& s = e.slots[slot];
-        const double lambda_n = s.lambda_n;
-        if (lambda_n <= 0.0) continue;
-        const V3 x_in = x;
-        const Q4 q_in = q;
-        Q4 fE{1.0, 0.0, 0.0, 0.0};
-        double fsin = 0.0;
-        const bool applied =
-            friction_fwd(e, prev_x, prev_q, x, q, V3{s.rb[0], s.rb[1], s.rb[2]}, V3{s.n[0], s.n[1], s.n[2]},
-                         lambda_n, st, fE, fsin);
-        if (applied) {
-          touched = true;
-          if (lane == 0) {
-            SlotRec& sw = e.slots[slot];
-            sw.fx[0] = x_in.x; sw.fx[1] = x_in.y; sw.fx[2] = x_in.z;
-            sw.fq[0] = q_in.w; sw.fq[1] = q_in.x; sw.fq[2] = q_in.y; sw.fq[3] = q_in.z;
-            sw.fE[0] = fE.w; sw.fE[1] = fE.x; sw.fE[2] = fE.y; sw.fE[3] = fE.z;
-            sw.fsin = fsin;
-            sw.fric = 1;
-            e.fric_order[nfric] = slot;
-          }
-          ++nfric;
+    PROF_T(tfwd);
+    // ---- Gauss-Seidel sweeps (sim.hpp:157-186) -------------------------------
+    // Two chunks of 32 consecutive points are classified against the current
+    // state (independent straight-line work: ILP); only candidates near /
+    // inside the dilated surface run the exact query; the first exact-active
+    // point is applied and evaluation restarts right after it. Inactive points
+    // change no forward value (sim.hpp:105-125), so this is the sequential sweep.
+    int pos = 0, sweep = 0;
+    // Quiet window: once N consecutive positions pass with no applied
+    // correction (and no singular skip, to keep SolveStats exact), every later
+    // position repeats an earlier inactive decision under the same state: the
+    // remaining sweeps are skipped (and the adjoint folds them, run_sim below).
+    int f_last = -1, singular_since = 0;
+    while (sweep < e.gs) {
+  #if defined(DGX_QUIET) || defined(DGX_QUIET_FWD)  // exact
+      if (sweep * N + pos - f_last - 1 >= N && singular_since == 0) break;
+  #endif
+      int cls[2];
+  #pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const int i = pos + 32 * h + lane;
+        const int ic = i < N ? i : N - 1;
+        if constexpr (kF32Prefilter<Sdf>) {
+          // grids: FP32 "certainly inactive" test; everything else -> exact query
+          cls[h] = (i >= N || grid_inactive_f32(sdf, Pf, e.px[ic], e.py[ic], e.pz[ic], radf)) ? 1 : 0;
+        } else {
+          const V3 p{e.px[ic], e.py[ic], e.pz[ic]};
+          const V3 rl = ftmul(R, p - x) + e.O->com;
+          cls[h] = i < N ? classify_fwd(sdf, e, sweep * N + i, rl).cls : 1;
         }
-        __syncwarp();
+      }
+      const unsigned cand0 = __ballot_sync(kFull, cls[0] <= 0);
+      const unsigned cand1 = __ballot_sync(kFull, cls[1] <= 0);
+      PROF_CNT(16, 1);
+      PROF_CNT(17, __popc(cand0) + __popc(cand1));
+      if ((cand0 | cand1) == 0u) {
+        pos += 64;
+        if (pos >= N) { pos = 0; ++sweep; }
+        continue;
+      }
+      PointEval pe;
+      int hsel = -1;
+      unsigned mask = 0u;
+  #pragma unroll 1
+      for (int h = 0; h < 2; ++h) {
+        if ((h ? cand1 : cand0) == 0u) continue;
+        const int i = pos + 32 * h + lane;
+        bool act = false;
+        if ((h ? cls[1] : cls[0]) <= 0) {
+          eval_point(sdf, e, i, x, R, record, pe);
+          act = record ? (pe.rho_d < 0.0) : !(pe.rho_d >= 0.0);
+        }
+        mask = __ballot_sync(kFull, act);
+        if (mask != 0u) {
+          hsel = h;
+          break;
+        }
+      }
+      if (hsel < 0) {
+        pos += 64;
+        if (pos >= N) { pos = 0; ++sweep; }
+        continue;
+      }
+      const int j = __ffs(mask) - 1;
+      const int ij = pos + 32 * hsel + j;
+      const V3 rel = shfl(pe.rel, j);
+      const V3 g = shfl(pe.q.grad, j);
+      const V3 pj = shfl(pe.p, j);
+      const double C = -shfl(pe.rho_d, j);
+      const V3 dxj = shfl(pe.rl - pe.q.proxy, j);
+      const int sgj = __shfl_sync(kFull, pe.q.sign, j);
+      const int fbj = __shfl_sync(kFull, pe.fb ? 1 : 0, j);
+      // apply_contact (sim.hpp:215-245), out of line (rare path)
+      PROF_T(tc);
+      const CorrOut co = apply_correction(e, CorrIn{x, q, rel, g, pj, dxj, C, ij, sweep * N + ij, ncorr, nslot, sgj, fbj});
+      PROF_ACC(1, tc);
+      PROF_CNT(20, 1);
+      if (co.status != kOk) { status = co.status; return 0.0; }
+      if (co.applied) {
+        x = co.x;
+        q = co.q;
+        R = rotation_matrix(q);
+        if constexpr (kF32Prefilter<Sdf>) Pf = pose_f32(x, R, e.O->com);
+        touched = true;
+        f_last = sweep * N + ij;
+        singular_since = 0;
+        ++ncorr;
+        nslot = co.nslot;
+        ++st.corrections;
+        st.active += co.new_contact;
+      } else {
+        ++st.singular;
+        ++singular_since;
+      }
+      pos = ij + 1;
+      if (pos >= N) { pos = 0; ++sweep; }
+    }
+
+    __syncwarp();  // order the forward's mesh-cache stores before the adjoint's loads
+    PROF_ACC(0, tfwd);
+    PROF_T(tfr);
+    // ---- friction (sim.hpp:188-196), active slots in point order -------------
+    if (e.mu > 0.0) {
+      for (int wd = 0; wd < nwords; ++wd) {
+        unsigned bits = e.bitmap[wd];
+        while (bits) {
+          const int b = __ffs(bits) - 1;
+          bits &= bits - 1u;
+          const int pt = wd * 32 + b;
+          const int slot = e.slot_of_point[pt];
+          const SlotRec& s = e.slots[slot];
+          const double lambda_n = s.lambda_n;
+          if (lambda_n <= 0.0) continue;
+          const V3 x_in = x;
+          const Q4 q_in = q;
+          Q4 fE{1.0, 0.0, 0.0, 0.0};
+          double fsin = 0.0;
+          const bool applied =
+              friction_fwd(e, prev_x, prev_q, x, q, V3{s.rb[0], s.rb[1], s.rb[2]}, V3{s.n[0], s.n[1], s.n[2]},
+                           lambda_n, st, fE, fsin);
+          if (applied) {
+            touched = true;
+            if (lane == 0) {
+              SlotRec& sw = e.slots[slot];
+              sw.fx[0] = x_in.x; sw.fx[1] = x_in.y; sw.fx[2] = x_in.z;
+              sw.fq[0] = q_in.w; sw.fq[1] = q_in.x; sw.fq[2] = q_in.y; sw.fq[3] = q_in.z;
+              sw.fE[0] = fE.w; sw.fE[1] = fE.x; sw.fE[2] = fE.y; sw.fE[3] = fE.z;
+              sw.fsin = fsin;
+              sw.fric = 1;
+              e.fric_order[nfric] = slot;
+            }
+            ++nfric;
+          }
+          __syncwarp();
+        }
       }
     }
-  }
-
-  PROF_ACC(2, tfr);
-  PROF_CNT(21, nfric);
+    PROF_ACC(2, tfr);
+    PROF_CNT(21, nfric);
+  }  // forward
   PROF_CNT(22, 1);
   // ---- finalize_velocities (sim.hpp:276-287) and residual ------------------
   V3 xdot, thd;
@@ -992,6 +1007,17 @@ __device__ double run_sim(const Sdf& sdf, SimEnv& e, V3 v_m, bool record, bool m
       if (rho < 0.0) mp = mp < -rho ? -rho : mp;
     }
     st.max_pen = warp_max(mp);
+  }
+  if constexpr (Phase == kPhaseFwd) {  // the adjoint kernel resumes from here
+    if (lane == 0) {
+      rec->x[0] = x.x; rec->x[1] = x.y; rec->x[2] = x.z;
+      rec->q[0] = q.w; rec->q[1] = q.x; rec->q[2] = q.y; rec->q[3] = q.z;
+      rec->touched = touched ? 1 : 0;
+      rec->ncorr = ncorr;
+      rec->nslot = nslot;
+      rec->nfric = nfric;
+    }
+    return residual;
   }
   if (!record || !touched) return residual;  // untouched: constant loss, zero gradient
 
@@ -1212,10 +1238,15 @@ struct CtasPerSm<MeshSdf> {
   static constexpr int value = 2;
 };
 
-template <class Sdf>
-__global__ void __launch_bounds__(224, CtasPerSm<Sdf>::value) fused_kernel(KHand H, const __grid_constant__ KObj O, Sdf sdf, KSim S, KOpt P, KBuf buf, int mode) {
+// Split-execution forward kernel: 2 CTAs per SM (128 registers; the adjoint
+// is compiled out of this instance). Config 2: 2 CTAs/SM 101k cand-iter/s,
+// 3 CTAs/SM (80 registers, 1 KB of spills) 96k, fused 86k.
+constexpr int kFwdCtasPerSm = 2;
+
+template <class Sdf, int Occ = CtasPerSm<Sdf>::value, int Phase = kPhaseFused>
+__global__ void __launch_bounds__(224, Occ) fused_kernel(KHand H, const __grid_constant__ KObj O, Sdf sdf, KSim S, KOpt P, KBuf buf, int mode) {
   extern __shared__ __align__(16) unsigned char smem[];
-  const SmemLayout lay(H.N, H.L, S.M, S.seg_max);
+  const SmemLayout lay(H.N, H.L, S.M, Phase == kPhaseFwd ? 0 : S.seg_max);  // the forward stages nothing
   double* px = reinterpret_cast<double*>(smem + lay.off_px);
   double* py = reinterpret_cast<double*>(smem + lay.off_py);
   double* pz = reinterpret_cast<double*>(smem + lay.off_pz);
@@ -1245,13 +1276,19 @@ __global__ void __launch_bounds__(224, CtasPerSm<Sdf>::value) fused_kernel(KHand
   e.stage = stage_all + warp * lay.stage_per_warp;
   e.seg_max = S.seg_max;
   e.ft = ft_all + warp * 6 * L;
-  const size_t wslot = static_cast<size_t>(blockIdx.x) * M + (warp < M ? warp : 0);
-  e.corr = buf.corr + wslot * buf.cap_corr;
-  e.slots = buf.slots + wslot * N;
+  const int wm = warp < M ? warp : 0;
+  const size_t wslot = static_cast<size_t>(blockIdx.x) * M + wm;
+  // logs: per resident (CTA, warp) when fused; per (candidate, sim) when split
+  // (bound per candidate below)
+  auto bind_logs = [&](size_t ws) {
+    e.corr = buf.corr + ws * buf.cap_corr;
+    e.slots = buf.slots + ws * buf.slot_stride;
+    e.slot_of_point = buf.slot_of_point + ws * N;
+    e.fric_order = buf.fric_order + ws * buf.slot_stride;
+  };
+  bind_logs(wslot);
   e.gft = buf.ft_global + wslot * 6 * L;
   e.L = L;
-  e.slot_of_point = buf.slot_of_point + wslot * N;
-  e.fric_order = buf.fric_order + wslot * N;
   e.cap_corr = buf.cap_corr;
   e.O = &O;
   e.alpha = S.alpha;
@@ -1266,6 +1303,12 @@ __global__ void __launch_bounds__(224, CtasPerSm<Sdf>::value) fused_kernel(KHand
   const int k1 = mode == kModeOpt ? P.k_end : 1;
 
   for (int b = blockIdx.x; b < buf.B; b += gridDim.x) {
+    if constexpr (Phase != kPhaseFused) {
+      bind_logs(static_cast<size_t>(b) * M + wm);
+      // a candidate that failed at an earlier iterate of this call stays
+      // there (the fused kernel's loop stops at its first failure)
+      if (mode == kModeOpt && P.k_begin > P.traj_k0 && buf.status[b] != kOk) continue;
+    }
     // Adam state in registers of lanes < D of warp 0
     double am = 0.0, av = 0.0;
     double b1t = 1.0, b2t = 1.0;
@@ -1310,8 +1353,15 @@ __global__ void __launch_bounds__(224, CtasPerSm<Sdf>::value) fused_kernel(KHand
         const V3 vm{S.vel[warp][0], S.vel[warp][1], S.vel[warp][2]};
         const bool meas = mode == kModeEval && S.measure_residual;
         PROF_T(tsim);
-        const double res = run_sim(sdf, e, vm, record, meas, st, status, acc);
+        FwdRec* rec = Phase != kPhaseFused ? buf.fwd + static_cast<size_t>(b) * M + warp : nullptr;
+        const double res = run_sim<Phase>(sdf, e, vm, record, meas, st, status, acc, rec);
         PROF_ACC(12, tsim);
+        if constexpr (Phase == kPhaseFwd) {
+          if (lane == 0) {
+            rec->residual = res;
+            rec->status = status;
+          }
+        }
         ft_flush_warp(acc, e.ft, lane);
         __syncwarp();
         if (lane == 0) {
@@ -1323,7 +1373,7 @@ __global__ void __launch_bounds__(224, CtasPerSm<Sdf>::value) fused_kernel(KHand
             so[0] = st.active; so[1] = st.corrections; so[2] = st.singular; so[3] = st.max_pen; so[4] = st.max_fric;
           }
         }
-        if (buf.sim_grads && record) {  // debug: per-perturbation gradient via the FK adjoint
+        if (Phase != kPhaseFwd && buf.sim_grads && record) {  // debug: per-perturbation gradient via the FK adjoint
           __syncwarp();
           if (lane == 0) {
             double gtmp[kMaxDim];
@@ -1336,6 +1386,9 @@ __global__ void __launch_bounds__(224, CtasPerSm<Sdf>::value) fused_kernel(KHand
         }
       }
       __syncthreads();
+      if constexpr (Phase == kPhaseFwd) {
+        if (record) continue;  // losses / gradient / step: the adjoint kernel
+      }
 
       // 4. losses, gradient, optimizer (warp 0)
       if (warp == 0) {
@@ -1406,7 +1459,7 @@ __global__ void __launch_bounds__(224, CtasPerSm<Sdf>::value) fused_kernel(KHand
           const bool bad = __any_sync(kFull, lane < D && !isfinite(gw));
           if (bad && cand_status == kOk) cand_status = kNonFiniteGrad;
           if (buf.traj) {
-            double* tr = buf.traj + (static_cast<size_t>(b) * (P.k_end - P.k_begin) + (k - P.k_begin)) * (3 + D);
+            double* tr = buf.traj + (static_cast<size_t>(b) * P.traj_rows + (k - P.traj_k0)) * (3 + D);
             if (lane == 0) { tr[0] = stable; tr[1] = qr; tr[2] = ql; }
             if (lane < D) tr[3 + lane] = gw;
           }
@@ -1441,6 +1494,12 @@ __global__ void __launch_bounds__(224, CtasPerSm<Sdf>::value) fused_kernel(KHand
       __syncthreads();
       cand_status = sflag[15];
       if (cand_status != kOk) break;
+    }
+    if constexpr (Phase == kPhaseFwd) {
+      if (record) {
+        __syncthreads();
+        continue;
+      }
     }
     // write back
     if (mode == kModeOpt) {
@@ -1628,43 +1687,79 @@ __global__ void step_kernel(int J, const double* q, const double* g, double lr, 
   for (int j = 0; j < J; ++j) o[7 + j] = qi[7 + j] - lr * gi[6 + j];
 }
 
+template <class Sdf, int Occ, int Phase>
+static cudaError_t allow_smem() {
+  static bool configured = false;
+  if (configured) return cudaSuccess;
+  cudaError_t e =
+      cudaFuncSetAttribute(fused_kernel<Sdf, Occ, Phase>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+  if (e == cudaSuccess) configured = true;
+  return e;
+}
+
+// the split pair exists for the analytic and grid backends; mesh objects run
+// fused (their forward and adjoint share the per-point-sweep face cache)
+template <class Sdf>
+constexpr bool kSplitCapable = !std::is_same<Sdf, MeshSdf>::value;
+
 template <class Sdf>
 static cudaError_t launch_fused_t(const KHand& H, const KObj& O, const Sdf& sdf, const KSim& S, const KOpt& P,
-                                  const KBuf& buf, int mode, int grid, int smem, cudaStream_t st) {
-  static bool configured = false;
-  if (!configured) {
-    cudaError_t e = cudaFuncSetAttribute(fused_kernel<Sdf>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
-    if (e != cudaSuccess) return e;
-    configured = true;
+                                  const KBuf& buf, int mode, int phase, int grid, int smem, cudaStream_t st) {
+  constexpr int occ = CtasPerSm<Sdf>::value;
+  cudaError_t e = cudaSuccess;
+  if constexpr (kSplitCapable<Sdf>) {
+    if (phase == kPhaseFwd) {
+      if ((e = allow_smem<Sdf, kFwdCtasPerSm, kPhaseFwd>()) != cudaSuccess) return e;
+      fused_kernel<Sdf, kFwdCtasPerSm, kPhaseFwd><<<grid, 32 * S.M, smem, st>>>(H, O, sdf, S, P, buf, mode);
+      return cudaGetLastError();
+    }
+    if (phase == kPhaseAdj) {
+      if ((e = allow_smem<Sdf, occ, kPhaseAdj>()) != cudaSuccess) return e;
+      fused_kernel<Sdf, occ, kPhaseAdj><<<grid, 32 * S.M, smem, st>>>(H, O, sdf, S, P, buf, mode);
+      return cudaGetLastError();
+    }
   }
-  fused_kernel<Sdf><<<grid, 32 * S.M, smem, st>>>(H, O, sdf, S, P, buf, mode);
+  if (phase != kPhaseFused) return cudaErrorInvalidValue;
+  if ((e = allow_smem<Sdf, occ, kPhaseFused>()) != cudaSuccess) return e;
+  fused_kernel<Sdf, occ, kPhaseFused><<<grid, 32 * S.M, smem, st>>>(H, O, sdf, S, P, buf, mode);
   return cudaGetLastError();
 }
 
 cudaError_t launch_fused(const KHand& H, const KObj& O, const SdfSet& sdf, const KSim& S, const KOpt& P,
-                         const KBuf& buf, int mode, int grid, int smem, cudaStream_t st) {
+                         const KBuf& buf, int mode, int phase, int grid, int smem, cudaStream_t st) {
   switch (sdf.kind) {
-    case kSdfSphere: return launch_fused_t(H, O, sdf.sph, S, P, buf, mode, grid, smem, st);
-    case kSdfBox: return launch_fused_t(H, O, sdf.box, S, P, buf, mode, grid, smem, st);
-    case kSdfGrid: return launch_fused_t(H, O, sdf.grd, S, P, buf, mode, grid, smem, st);
-    case kSdfMesh: return launch_fused_t(H, O, sdf.mesh, S, P, buf, mode, grid, smem, st);
+    case kSdfSphere: return launch_fused_t(H, O, sdf.sph, S, P, buf, mode, phase, grid, smem, st);
+    case kSdfBox: return launch_fused_t(H, O, sdf.box, S, P, buf, mode, phase, grid, smem, st);
+    case kSdfGrid: return launch_fused_t(H, O, sdf.grd, S, P, buf, mode, phase, grid, smem, st);
+    case kSdfMesh: return launch_fused_t(H, O, sdf.mesh, S, P, buf, mode, phase, grid, smem, st);
     default: return cudaErrorInvalidValue;
   }
 }
 
-template <class Sdf>
-static cudaError_t occupancy_t(int M, int smem, int* blocks_per_sm) {
-  cudaError_t e = cudaFuncSetAttribute(fused_kernel<Sdf>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+template <class Sdf, int Occ, int Phase>
+static cudaError_t occupancy_i(int M, int smem, int* blocks_per_sm) {
+  cudaError_t e = allow_smem<Sdf, Occ, Phase>();
   if (e != cudaSuccess) return e;
-  return cudaOccupancyMaxActiveBlocksPerMultiprocessor(blocks_per_sm, fused_kernel<Sdf>, 32 * M, smem);
+  return cudaOccupancyMaxActiveBlocksPerMultiprocessor(blocks_per_sm, fused_kernel<Sdf, Occ, Phase>, 32 * M, smem);
 }
 
-cudaError_t fused_occupancy(int kind, int M, int smem, int* blocks_per_sm) {
+template <class Sdf>
+static cudaError_t occupancy_t(int M, int smem, int phase, int* blocks_per_sm) {
+  constexpr int occ = CtasPerSm<Sdf>::value;
+  if constexpr (kSplitCapable<Sdf>) {
+    if (phase == kPhaseFwd) return occupancy_i<Sdf, kFwdCtasPerSm, kPhaseFwd>(M, smem, blocks_per_sm);
+    if (phase == kPhaseAdj) return occupancy_i<Sdf, occ, kPhaseAdj>(M, smem, blocks_per_sm);
+  }
+  if (phase != kPhaseFused) return cudaErrorInvalidValue;
+  return occupancy_i<Sdf, occ, kPhaseFused>(M, smem, blocks_per_sm);
+}
+
+cudaError_t fused_occupancy(int kind, int M, int smem, int phase, int* blocks_per_sm) {
   switch (kind) {
-    case kSdfSphere: return occupancy_t<SphereSdf>(M, smem, blocks_per_sm);
-    case kSdfBox: return occupancy_t<BoxSdf>(M, smem, blocks_per_sm);
-    case kSdfGrid: return occupancy_t<GridSdf>(M, smem, blocks_per_sm);
-    case kSdfMesh: return occupancy_t<MeshSdf>(M, smem, blocks_per_sm);
+    case kSdfSphere: return occupancy_t<SphereSdf>(M, smem, phase, blocks_per_sm);
+    case kSdfBox: return occupancy_t<BoxSdf>(M, smem, phase, blocks_per_sm);
+    case kSdfGrid: return occupancy_t<GridSdf>(M, smem, phase, blocks_per_sm);
+    case kSdfMesh: return occupancy_t<MeshSdf>(M, smem, phase, blocks_per_sm);
     default: return cudaErrorInvalidValue;
   }
 }

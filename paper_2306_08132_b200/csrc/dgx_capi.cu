@@ -4,6 +4,7 @@
 #include <algorithm>
 #include <climits>
 #include <cmath>
+#include <cstdint>
 #include <cstdio>
 #include <cstring>
 #include <cstdlib>
@@ -194,6 +195,7 @@ int prepare(dgx_ctx* c, Scratch& sc, const dgx_hand* h, const dgx_object* o, KSi
   buf.fric_order = buf.slot_of_point + per;
   buf.slot_stride = h->N;
   buf.fwd = nullptr;
+  buf.fk = nullptr;
   sc.ftg.ensure(nws * 6 * static_cast<size_t>(h->L) * sizeof(double));
   buf.ft_global = static_cast<double*>(sc.ftg.p);
   buf.mesh_cache = nullptr;
@@ -248,13 +250,17 @@ SplitGrid prepare_split(dgx_ctx* c, Scratch& sc, const dgx_hand* h, const dgx_ob
   const size_t nws = static_cast<size_t>(g.chunk) * M;
   const size_t cap = static_cast<size_t>(c->cap_corr), ss = cap + 1;  // nslot <= ncorr <= cap_corr
   sc.corr.ensure(nws * cap * sizeof(CorrRec));
-  sc.slots.ensure(nws * (ss * sizeof(SlotRec) + sizeof(FwdRec) + (ss + N) * sizeof(int)));
+  const size_t fk_per = 12 * static_cast<size_t>(h->L) + 3 * static_cast<size_t>(N);
+  sc.slots.ensure(nws * (ss * sizeof(SlotRec) + sizeof(FwdRec) + (ss + N) * sizeof(int)) +
+                  static_cast<size_t>(g.chunk) * fk_per * sizeof(double) + 256);
   char* base = static_cast<char*>(sc.slots.p);
   buf.corr = static_cast<CorrRec*>(sc.corr.p);
   buf.slots = reinterpret_cast<SlotRec*>(base);
   buf.fwd = reinterpret_cast<FwdRec*>(base + nws * ss * sizeof(SlotRec));
   buf.slot_of_point = reinterpret_cast<int*>(buf.fwd + nws);
   buf.fric_order = buf.slot_of_point + nws * N;
+  buf.fk = reinterpret_cast<double*>(
+      (reinterpret_cast<uintptr_t>(buf.fric_order + nws * ss) + 255) & ~static_cast<uintptr_t>(255));
   buf.slot_stride = static_cast<int>(ss);
   sc.ftg.ensure(static_cast<size_t>(g.grid_a) * M * 6 * static_cast<size_t>(h->L) * sizeof(double));
   buf.ft_global = static_cast<double*>(sc.ftg.p);

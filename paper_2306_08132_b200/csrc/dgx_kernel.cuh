@@ -126,6 +126,7 @@ struct KBuf {
   int* slot_of_point;   // [grid, M, N]
   int* fric_order;      // [grid, M, N]
   FwdRec* fwd;          // [B, M] split execution only
+  double* fk;           // [B, 12 L + 3 N] split: link transforms + world points of the forward
   int slot_stride;      // slots / fric_order entries per sim (N fused, cap_corr + 1 split)
   double* ft_global;    // [grid, M, L*6] adjoint link-sum spill buffers
   int* mesh_cache;      // [grid, M, gs*N] mesh objects: forward (face << 1 | inside) per point-sweep

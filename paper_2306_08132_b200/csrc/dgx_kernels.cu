@@ -1238,13 +1238,14 @@ struct CtasPerSm<MeshSdf> {
   static constexpr int value = 2;
 };
 
-// Split-execution forward kernel: 2 CTAs per SM (128 registers; the adjoint
-// is compiled out of this instance). Config 2: 2 CTAs/SM 101k cand-iter/s,
-// 3 CTAs/SM (80 registers, 1 KB of spills) 96k, fused 86k.
+// Split-execution forward kernel: 2 CTAs per SM (the adjoint is compiled out
+// of this instance). Config 2: 2 CTAs/SM 101k cand-iter/s, 3 CTAs/SM (80
+// registers, 1 KB of spills) 96k, fused 86k.
 constexpr int kFwdCtasPerSm = 2;
 
-template <class Sdf, int Occ = CtasPerSm<Sdf>::value, int Phase = kPhaseFused>
-__global__ void __launch_bounds__(224, Occ) fused_kernel(KHand H, const __grid_constant__ KObj O, Sdf sdf, KSim S, KOpt P, KBuf buf, int mode) {
+template <class Sdf, int Phase>
+__device__ __forceinline__ void kernel_body(const KHand& H, const KObj& O, const Sdf& sdf, const KSim& S,
+                                            const KOpt& P, const KBuf& buf, int mode) {
   extern __shared__ __align__(16) unsigned char smem[];
   const SmemLayout lay(H.N, H.L, S.M, Phase == kPhaseFwd ? 0 : S.seg_max);  // the forward stages nothing
   double* px = reinterpret_cast<double*>(smem + lay.off_px);
@@ -1327,21 +1328,40 @@ __global__ void __launch_bounds__(224, Occ) fused_kernel(KHand H, const __grid_c
       double radius = S.radius;
       if (mode == kModeOpt)
         radius = P.iters > 1 ? P.r0 * (1.0 - static_cast<double>(k) / static_cast<double>(P.iters - 1)) : 0.0;
-      // 1. FK
-      if (tid == 0) link_transforms(H, sq, record, link);
+      // 1. FK. Split execution: the forward kernel stores the link transforms
+      // and world points per candidate; the adjoint kernel reloads them.
+      double* fkb = Phase != kPhaseFused && record ? buf.fk + static_cast<size_t>(b) * (12 * L + 3 * N) : nullptr;
       for (int t = tid; t < 6 * L * M; t += blockDim.x) ft_all[t] = 0.0;
       if (tid < 16) sflag[tid] = kOk;
-      __syncthreads();
-      for (int i = tid; i < N; i += blockDim.x) {
-        const int li = H.sample_link[i];
-        const double* Rl = link + 12 * li;
-        M3 R;
-        for (int m = 0; m < 9; ++m) R.m[m] = Rl[m];
-        const V3 s{H.samples[3 * i], H.samples[3 * i + 1], H.samples[3 * i + 2]};
-        const V3 p = mul(R, s) + V3{Rl[9], Rl[10], Rl[11]};
-        px[i] = p.x; py[i] = p.y; pz[i] = p.z;
+      if constexpr (Phase == kPhaseAdj) {
+        for (int t = tid; t < 12 * L; t += blockDim.x) link[t] = __ldcg(fkb + t);
+        for (int i = tid; i < N; i += blockDim.x) {
+          px[i] = __ldcg(fkb + 12 * L + i);
+          py[i] = __ldcg(fkb + 12 * L + N + i);
+          pz[i] = __ldcg(fkb + 12 * L + 2 * N + i);
+        }
+        __syncthreads();
+      } else {
+        if (tid == 0) link_transforms(H, sq, record, link);
+        __syncthreads();
+        for (int i = tid; i < N; i += blockDim.x) {
+          const int li = H.sample_link[i];
+          const double* Rl = link + 12 * li;
+          M3 R;
+          for (int m = 0; m < 9; ++m) R.m[m] = Rl[m];
+          const V3 s{H.samples[3 * i], H.samples[3 * i + 1], H.samples[3 * i + 2]};
+          const V3 p = mul(R, s) + V3{Rl[9], Rl[10], Rl[11]};
+          px[i] = p.x; py[i] = p.y; pz[i] = p.z;
+          if (fkb) {
+            __stcg(fkb + 12 * L + i, p.x);
+            __stcg(fkb + 12 * L + N + i, p.y);
+            __stcg(fkb + 12 * L + 2 * N + i, p.z);
+          }
+        }
+        if (fkb)
+          for (int t = tid; t < 12 * L; t += blockDim.x) __stcg(fkb + t, link[t]);
+        __syncthreads();
       }
-      __syncthreads();
 
       // 2-3. perturbation sims, one per warp
       if (warp < M) {
@@ -1514,6 +1534,23 @@ __global__ void __launch_bounds__(224, Occ) fused_kernel(KHand H, const __grid_c
   }
 }
 
+
+// fused / adjoint instances: the register budget follows CTAs per SM
+template <class Sdf, int Occ = CtasPerSm<Sdf>::value, int Phase = kPhaseFused>
+__global__ void __launch_bounds__(224, Occ) fused_kernel(KHand H, const __grid_constant__ KObj O, Sdf sdf, KSim S,
+                                                         KOpt P, KBuf buf, int mode) {
+  kernel_body<Sdf, Phase>(H, O, sdf, S, P, buf, mode);
+}
+
+// forward instance of split execution: kFwdCtasPerSm CTAs per SM. The
+// register file is split per SM sub-partition (16384 each), so 14 warps on 4
+// sub-partitions allow 4096 / 32 = 128 registers per thread; __maxnreg__(144)
+// leaves one CTA per SM (90k vs 101k cand-iter/s)
+template <class Sdf>
+__global__ void __launch_bounds__(224, kFwdCtasPerSm) fwd_kernel(KHand H, const __grid_constant__ KObj O, Sdf sdf,
+                                                                 KSim S, KOpt P, KBuf buf, int mode) {
+  kernel_body<Sdf, kPhaseFwd>(H, O, sdf, S, P, buf, mode);
+}
 }  // namespace dgx
 
 // ---------------------------------------------------------------------------
@@ -1697,6 +1734,15 @@ static cudaError_t allow_smem() {
   return e;
 }
 
+template <class Sdf>
+static cudaError_t allow_smem_fwd() {
+  static bool configured = false;
+  if (configured) return cudaSuccess;
+  cudaError_t e = cudaFuncSetAttribute(fwd_kernel<Sdf>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+  if (e == cudaSuccess) configured = true;
+  return e;
+}
+
 // the split pair exists for the analytic and grid backends; mesh objects run
 // fused (their forward and adjoint share the per-point-sweep face cache)
 template <class Sdf>
@@ -1709,8 +1755,8 @@ static cudaError_t launch_fused_t(const KHand& H, const KObj& O, const Sdf& sdf,
   cudaError_t e = cudaSuccess;
   if constexpr (kSplitCapable<Sdf>) {
     if (phase == kPhaseFwd) {
-      if ((e = allow_smem<Sdf, kFwdCtasPerSm, kPhaseFwd>()) != cudaSuccess) return e;
-      fused_kernel<Sdf, kFwdCtasPerSm, kPhaseFwd><<<grid, 32 * S.M, smem, st>>>(H, O, sdf, S, P, buf, mode);
+      if ((e = allow_smem_fwd<Sdf>()) != cudaSuccess) return e;
+      fwd_kernel<Sdf><<<grid, 32 * S.M, smem, st>>>(H, O, sdf, S, P, buf, mode);
       return cudaGetLastError();
     }
     if (phase == kPhaseAdj) {
@@ -1747,7 +1793,11 @@ template <class Sdf>
 static cudaError_t occupancy_t(int M, int smem, int phase, int* blocks_per_sm) {
   constexpr int occ = CtasPerSm<Sdf>::value;
   if constexpr (kSplitCapable<Sdf>) {
-    if (phase == kPhaseFwd) return occupancy_i<Sdf, kFwdCtasPerSm, kPhaseFwd>(M, smem, blocks_per_sm);
+    if (phase == kPhaseFwd) {
+      cudaError_t e = allow_smem_fwd<Sdf>();
+      if (e != cudaSuccess) return e;
+      return cudaOccupancyMaxActiveBlocksPerMultiprocessor(blocks_per_sm, fwd_kernel<Sdf>, 32 * M, smem);
+    }
     if (phase == kPhaseAdj) return occupancy_i<Sdf, occ, kPhaseAdj>(M, smem, blocks_per_sm);
   }
   if (phase != kPhaseFused) return cudaErrorInvalidValue;

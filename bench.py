@@ -45,6 +45,9 @@ HAND = "allegro16"
 # algorithmic FLOP per point-sweep: 160 backend-independent
 # (50 forward + 110 adjoint) + 2 x F_sdf with F_sdf(grid trilinear + gradient + proxy) = 70
 FLOP_PER_POINT_SWEEP = 160 + 2 * 70
+# SURVEY §8(d) split by kernel: forward 50 + one grid query (70); adjoint 110 + one recompute (70)
+FLOP_FWD_PER_POINT_SWEEP = 50 + 70
+FLOP_ADJ_PER_POINT_SWEEP = 110 + 70
 M_SIMS, GS = 7, 8
 
 
@@ -304,6 +307,24 @@ def run_dgx(args, rank, world, local_rank):
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
     e2e_value = cand_total * args.steps / float(t.item())
 
+    # ---- per-kernel launch durations (roofline of the dominant kernel) ----
+    # One object's 512-candidate launches on one stream, CUDA events around
+    # every launch on that stream (dgx_ctx_set_kernel_timing), L2 flushed
+    # between steps; the same launches the ncu launch list shows serialised.
+    ctx.set_stream(stream.cuda_stream)
+    n0 = int(counts[0])
+    sub = {k: st[k][:n0] for k in ("q", "m", "v", "status")}
+    ktimes = None
+    for phase in ("warm", "timed"):
+        ctx.set_kernel_timing(phase == "timed")
+        for s in range(3 if phase == "warm" else args.steps):
+            flush.zero_()
+            api.optimize(ctx, objs[0], hand, sub["q"], proto, params, weights, opt, k_begin=k0 + s, k_end=k0 + s + 1,
+                         adam_m=sub["m"], adam_v=sub["v"], status=sub["status"], flags=flags)
+        torch.cuda.synchronize()
+    ktimes = ctx.kernel_times()
+    ctx.set_kernel_timing(False)
+
     if rank == 0:
         L = capi.load()
         import ctypes as C
@@ -311,8 +332,21 @@ def run_dgx(args, rank, world, local_rank):
         capi.check(L.dgx_fp64_peak(local_rank, C.byref(pk), C.byref(pms)))
         n_pts = hand_d.num_samples
         flop_cand_iter = M_SIMS * GS * n_pts * FLOP_PER_POINT_SWEEP
-        avg_step_s = statistics.mean(step_ms) * 1e-3
-        achieved = flop_cand_iter * args.candidates / avg_step_s / 1e12
+        pts_sweeps = M_SIMS * GS * n_pts
+        kern = {}
+        for kind, per_ps in (("forward", FLOP_FWD_PER_POINT_SWEEP), ("adjoint", FLOP_ADJ_PER_POINT_SWEEP),
+                             ("fused", FLOP_PER_POINT_SWEEP)):
+            ms_tot, cnt = ktimes[kind]
+            if cnt:
+                ms = ms_tot / cnt
+                kern[kind] = {"avg_launch_ms": ms, "launches": cnt, "candidates_per_launch": n0,
+                              "flop_per_candidate_iteration": pts_sweeps * per_ps,
+                              "achieved_tflops": pts_sweeps * per_ps * n0 / (ms * 1e-3) / 1e12}
+        dom = max(kern, key=lambda k: kern[k]["avg_launch_ms"])
+        step_kernel_ms = sum(v["avg_launch_ms"] for v in kern.values())
+        for v in kern.values():
+            v["share_of_serialised_step"] = v["avg_launch_ms"] / step_kernel_ms
+        achieved = kern[dom]["achieved_tflops"]
         traffic = traffic_from_profiles()
         result = {
             "metric": "candidate-iterations/sec", "value": value, "unit": "candidate-iterations/s",
@@ -327,11 +361,15 @@ def run_dgx(args, rank, world, local_rank):
                             "q, m, v, status, iterate losses + gradient out), synchronous, wall clock"},
             "gpu_launches": launches,
             "roofline": {"bound": "fp64", "achieved": achieved, "peak": pk.value, "unit": "TFLOP/s",
-                         "frac": achieved / pk.value, "traffic": traffic,
+                         "frac": achieved / pk.value, "traffic": traffic, "kernel": dom,
                          "peak_source": "measured DFMA microbenchmark (dgx_fp64_peak, csrc/dgx_peak.cu)",
                          "flop_per_candidate_iteration": flop_cand_iter,
-                         "timing": "per step: one dgx_optimize_multi call = two concurrent fused launches (one per "
-                                   "object) on side streams; achieved = FLOP_alg x candidates / step time",
+                         "timing": "dominant kernel: FLOP_alg of its half (SURVEY 8(d): adjoint 110 + 70 per "
+                                   "point-sweep, forward 50 + 70) x candidates per launch / its mean launch "
+                                   "duration, CUDA events on its stream, one object's launches, L2 flushed",
+                         "kernels": kern,
+                         "step_achieved_tflops": flop_cand_iter * args.candidates / (statistics.mean(step_ms) * 1e-3)
+                         / 1e12,
                          "avg_step_ms": statistics.mean(step_ms)},
             "clocks": clk.summary(),
             "failed_candidates": status_bad,

@@ -162,6 +162,13 @@ int dgx_ctx_set_stream(dgx_ctx* ctx, void* cuda_stream);
 int dgx_ctx_set_correction_capacity(dgx_ctx* ctx, int32_t cap);
 /* number of kernels this context has launched */
 int64_t dgx_ctx_launch_count(const dgx_ctx* ctx);
+/* Per-kernel timing (measurement only; no reference counterpart): while
+ * enabled, every grasp-search launch is bracketed by CUDA events on the stream
+ * it runs on. dgx_ctx_kernel_times synchronizes and returns, per kernel kind
+ * (0 fused, 1 split forward, 2 split adjoint), the summed milliseconds and the
+ * launch count since the last enable; ms / count may be NULL. */
+int dgx_ctx_set_kernel_timing(dgx_ctx* ctx, int enable);
+int dgx_ctx_kernel_times(dgx_ctx* ctx, double ms[3], int64_t count[3]);
 
 int dgx_hand_upload(dgx_ctx* ctx, const dgx_hand_desc* desc, dgx_hand** out);
 int dgx_hand_free(dgx_hand* hand);

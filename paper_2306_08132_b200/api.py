@@ -108,6 +108,19 @@ class Context:
     def launches(self) -> int:
         return int(self.L.dgx_ctx_launch_count(self.h))
 
+    def set_kernel_timing(self, enable: bool) -> None:
+        """Bracket every grasp-search launch with CUDA events on its stream
+        (resets the record)."""
+        capi.check(self.L.dgx_ctx_set_kernel_timing(self.h, int(enable)))
+
+    def kernel_times(self) -> dict:
+        """{kind: (total ms, launches)} for kinds fused / forward / adjoint since
+        set_kernel_timing(True); synchronizes on the recorded events."""
+        ms = (C.c_double * 3)()
+        n = (C.c_int64 * 3)()
+        capi.check(self.L.dgx_ctx_kernel_times(self.h, ms, n))
+        return {k: (ms[i], n[i]) for i, k in enumerate(("fused", "forward", "adjoint"))}
+
     def close(self) -> None:
         if getattr(self, "h", None):
             self.L.dgx_ctx_destroy(self.h)

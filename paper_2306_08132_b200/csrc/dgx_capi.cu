@@ -94,6 +94,10 @@ struct dgx_ctx {
   cudaEvent_t fork = nullptr;
   int cap_corr = 1024;
   int64_t launches = 0;
+  // kernel timing (dgx_ctx_set_kernel_timing): event pairs per launch
+  bool timing = false;
+  std::vector<std::pair<int, std::pair<cudaEvent_t, cudaEvent_t>>> timed;  // kind, (start, stop)
+  std::vector<cudaEvent_t> event_pool;
   Scratch scratch;
   DevBuf io;
   std::vector<SubStream> subs;
@@ -271,6 +275,34 @@ SplitGrid prepare_split(dgx_ctx* c, Scratch& sc, const dgx_hand* h, const dgx_ob
   return g;
 }
 
+cudaEvent_t pool_event(dgx_ctx* c) {
+  if (!c->event_pool.empty()) {
+    cudaEvent_t e = c->event_pool.back();
+    c->event_pool.pop_back();
+    return e;
+  }
+  cudaEvent_t e;
+  cuda_check(cudaEventCreate(&e), "cudaEventCreate");
+  return e;
+}
+
+// one grasp-search launch of kind `phase` on st (counted; timed when enabled)
+template <class F>
+void counted_launch(dgx_ctx* c, int phase, cudaStream_t st, const char* what, F&& launch) {
+  cudaEvent_t e0 = nullptr, e1 = nullptr;
+  if (c->timing) {
+    e0 = pool_event(c);
+    e1 = pool_event(c);
+    cuda_check(cudaEventRecord(e0, st), "cudaEventRecord");
+  }
+  cuda_check(launch(), what);
+  ++c->launches;
+  if (c->timing) {
+    cuda_check(cudaEventRecord(e1, st), "cudaEventRecord");
+    c->timed.push_back({phase, {e0, e1}});
+  }
+}
+
 // Every launch for B candidates whose per-candidate arrays start at buf's
 // pointers, on stream st with scratch sc.
 void launch_range(dgx_ctx* c, Scratch& sc, const dgx_hand* h, const dgx_object* o, KSim S, KOpt P, KBuf buf,
@@ -283,8 +315,8 @@ void launch_range(dgx_ctx* c, Scratch& sc, const dgx_hand* h, const dgx_object* 
   if (!use_split(o) || (mode == kModeOpt && P.k_end == P.k_begin)) {
     int smem = 0;
     const int grid = prepare(c, sc, h, o, S, B, buf, smem);
-    cuda_check(launch_fused(h->k, o->k, o->sdf, S, P, buf, mode, kPhaseFused, grid, smem, st), "fused_kernel");
-    ++c->launches;
+    counted_launch(c, kPhaseFused, st, "fused_kernel",
+                   [&] { return launch_fused(h->k, o->k, o->sdf, S, P, buf, mode, kPhaseFused, grid, smem, st); });
     return;
   }
   const bool record = mode != kModeEval;
@@ -313,13 +345,13 @@ void launch_range(dgx_ctx* c, Scratch& sc, const dgx_hand* h, const dgx_object* 
         Pk.k_begin = k;
         Pk.k_end = k + 1;
       }
-      cuda_check(launch_fused(h->k, o->k, o->sdf, S, Pk, cb, mode, kPhaseFwd, std::min(g.grid_f, nb), g.smem_f, st),
-                 "forward kernel");
-      ++c->launches;
+      counted_launch(c, kPhaseFwd, st, "forward kernel", [&] {
+        return launch_fused(h->k, o->k, o->sdf, S, Pk, cb, mode, kPhaseFwd, std::min(g.grid_f, nb), g.smem_f, st);
+      });
       if (!record) continue;
-      cuda_check(launch_fused(h->k, o->k, o->sdf, S, Pk, cb, mode, kPhaseAdj, std::min(g.grid_a, nb), g.smem_a, st),
-                 "adjoint kernel");
-      ++c->launches;
+      counted_launch(c, kPhaseAdj, st, "adjoint kernel", [&] {
+        return launch_fused(h->k, o->k, o->sdf, S, Pk, cb, mode, kPhaseAdj, std::min(g.grid_a, nb), g.smem_a, st);
+      });
     }
   }
 }
@@ -399,6 +431,11 @@ int dgx_ctx_destroy(dgx_ctx* c) {
       if (sub.done) cudaEventDestroy(sub.done);
       if (sub.stream) cudaStreamDestroy(sub.stream);
     }
+    for (auto& t : c->timed) {
+      cudaEventDestroy(t.second.first);
+      cudaEventDestroy(t.second.second);
+    }
+    for (auto e : c->event_pool) cudaEventDestroy(e);
     if (c->fork) cudaEventDestroy(c->fork);
     if (c->own) cudaStreamDestroy(c->own);
     delete c;
@@ -417,6 +454,39 @@ int dgx_ctx_set_correction_capacity(dgx_ctx* c, int32_t cap) {
 }
 
 int64_t dgx_ctx_launch_count(const dgx_ctx* c) { return c ? c->launches : 0; }
+
+int dgx_ctx_set_kernel_timing(dgx_ctx* c, int enable) {
+  return guarded([&] {
+    if (!c) throw DgxError(DGX_E_INVALID, "NULL context");
+    set_device(c);
+    for (auto& t : c->timed) {
+      c->event_pool.push_back(t.second.first);
+      c->event_pool.push_back(t.second.second);
+    }
+    c->timed.clear();
+    c->timing = enable != 0;
+  });
+}
+
+int dgx_ctx_kernel_times(dgx_ctx* c, double ms[3], int64_t count[3]) {
+  return guarded([&] {
+    if (!c) throw DgxError(DGX_E_INVALID, "NULL context");
+    set_device(c);
+    double acc[3] = {0.0, 0.0, 0.0};
+    int64_t n[3] = {0, 0, 0};
+    for (auto& t : c->timed) {
+      cuda_check(cudaEventSynchronize(t.second.second), "cudaEventSynchronize");
+      float e = 0.0f;
+      cuda_check(cudaEventElapsedTime(&e, t.second.first, t.second.second), "cudaEventElapsedTime");
+      acc[t.first] += e;
+      ++n[t.first];
+    }
+    for (int k = 0; k < 3; ++k) {
+      if (ms) ms[k] = acc[k];
+      if (count) count[k] = n[k];
+    }
+  });
+}
 
 int dgx_hand_upload(dgx_ctx* c, const dgx_hand_desc* d, dgx_hand** out) {
   return guarded([&] {

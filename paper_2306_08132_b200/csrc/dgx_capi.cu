@@ -231,6 +231,9 @@ bool use_split(const dgx_object* o) {
   return split_capable(o->kind) && !fused_env;
 }
 
+constexpr size_t kSplitScratchBytes = size_t(8) << 30;  // per stream
+constexpr int kSplitMaxFwdSmem = 96 * 1024;
+
 struct SplitGrid {
   int chunk, grid_f, grid_a, smem_f, smem_a;
 };
@@ -247,8 +250,19 @@ SplitGrid prepare_split(dgx_ctx* c, Scratch& sc, const dgx_hand* h, const dgx_ob
   if (per_f < 1 || per_a < 1) throw DgxError(DGX_E_UNSUPPORTED, "split kernels cannot be resident (registers/smem)");
   g.grid_f = c->num_sms * per_f;
   g.grid_a = c->num_sms * per_a;
-  // logs live per (candidate, sim) for one chunk: ~(cap_corr + 1) x 372 B + 8 N B per sim
-  g.chunk = std::max(1, std::min(B, 4 * std::max(g.grid_f, g.grid_a)));
+  // logs live per (candidate, sim) for one chunk: ~(cap_corr + 1) x 372 B + 8 N B per sim. Chunks
+  // are as large as kSplitScratchBytes allows (each chunk boundary drains both kernels' tails);
+  // DGX_SPLIT_SCRATCH_MB lowers the budget, down to 4 waves of the larger grid per chunk.
+  const size_t per_cand = static_cast<size_t>(M) * ((static_cast<size_t>(c->cap_corr) + 1) *
+                                                        (sizeof(CorrRec) + sizeof(SlotRec) + sizeof(int)) +
+                                                    sizeof(FwdRec) + static_cast<size_t>(N) * sizeof(int)) +
+                          (12 * static_cast<size_t>(h->L) + 3 * static_cast<size_t>(N)) * sizeof(double);
+  size_t budget = kSplitScratchBytes;
+  if (const char* ev = std::getenv("DGX_SPLIT_SCRATCH_MB"))  // tests: force several chunks
+    budget = static_cast<size_t>(std::max(1, std::atoi(ev))) << 20;
+  const size_t by_mem = std::max<size_t>(1, budget / per_cand);
+  g.chunk = static_cast<int>(std::max<size_t>(
+      1, std::min<size_t>(B, std::max<size_t>(4 * static_cast<size_t>(std::max(g.grid_f, g.grid_a)), by_mem))));
   g.grid_f = std::min(g.grid_f, g.chunk);
   g.grid_a = std::min(g.grid_a, g.chunk);
   const size_t nws = static_cast<size_t>(g.chunk) * M;
@@ -312,7 +326,14 @@ void launch_range(dgx_ctx* c, Scratch& sc, const dgx_hand* h, const dgx_object* 
     P.traj_k0 = P.k_begin;
     P.traj_rows = P.k_end - P.k_begin;
   }
-  if (!use_split(o) || (mode == kModeOpt && P.k_end == P.k_begin)) {
+  // Fused instead of split when the split cannot gain (measured):
+  // * B <= #SMs: every candidate has an SM to itself in the fused kernel, and
+  //   the split's per-iterate launches only cost (config 1: 61.5k vs 69.4k);
+  // * forward shared memory > kSplitMaxFwdSmem (N >~ 3000 points): two forward
+  //   CTAs leave too little L1 for the SDF cells (config 3, N = 4093: 42.9k vs 45.8k).
+  const bool split = use_split(o) && B > c->num_sms && SmemLayout(N, h->L, M, 0).total <= kSplitMaxFwdSmem &&
+                     !(mode == kModeOpt && P.k_end == P.k_begin);
+  if (!split) {
     int smem = 0;
     const int grid = prepare(c, sc, h, o, S, B, buf, smem);
     counted_launch(c, kPhaseFused, st, "fused_kernel",

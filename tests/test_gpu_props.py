@@ -175,13 +175,16 @@ def test_split_execution_equals_fused(tmp_path):
         assert np.array_equal(a[k], b[k], equal_nan=True), k
 
 
-def test_split_chunks_equal_single_rows(ctx):
-    """More candidates than one split chunk (4 x the resident CTAs): every
-    chunk's rows equal the same candidates run alone."""
+def test_split_chunks_equal_single_rows(ctx, monkeypatch):
+    """More candidates than one split chunk (the scratch budget lowered so a
+    chunk is 4 x the resident CTAs = 1184): every chunk's rows equal the same
+    candidates run alone."""
     from paper_2306_08132_b200 import api
     hd, od, hand, obj, q = setup(ctx, B=1300, seed=23)
     proto, params = api.StabilityProtocol.standard(), api.SimParams(dilation_radius=0.015)
+    monkeypatch.setenv("DGX_SPLIT_SCRATCH_MB", "1")
     l1, g1, s1 = api.loss_gradient(ctx, obj, hand, q, proto, params)
+    monkeypatch.delenv("DGX_SPLIT_SCRATCH_MB")
     assert not np.any(s1)
     for lo, hi in ((0, 40), (1180, 1240), (1250, 1300)):
         ls, gs, ss = api.loss_gradient(ctx, obj, hand, q[lo:hi], proto, params)

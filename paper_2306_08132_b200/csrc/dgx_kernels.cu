@@ -1031,19 +1031,71 @@ __device__ double run_sim(const Sdf& sdf, SimEnv& e, V3 v_m, bool record, bool m
 
   PROF_T(tfa);
   // ---- friction, reverse --------------------------------------------------
-  for (int k = nfric - 1; k >= 0; --k) {
-    const int slot = e.fric_order[k];
-    SlotRec s = e.slots[slot];
-    double a_lam = s.a_lam;
-    V3 a_n{s.a_n[0], s.a_n[1], s.a_n[2]};
-    friction_adj(e, prev_x, prev_q, s, aX, aQ, a_lam, a_n);
-    __syncwarp();
-    if (lane == 0) {
-      SlotRec& sw = e.slots[slot];
-      sw.a_lam = a_lam;
-      sw.a_n[0] = a_n.x; sw.a_n[1] = a_n.y; sw.a_n[2] = a_n.z;
+  // Each friction's reverse step is linear in v = (aX, aQ) given its logged
+  // forward values: v <- A_k v, a_lam_k = l_k . v, a_n_k = N_k v (11 x 7).
+  // Batches of frictions get their matrices in parallel (one lane per
+  // friction, friction_adj on the 7 basis vectors, staged in shared memory);
+  // the serial chain is then one 11 x 7 mat-vec per friction (lanes = rows)
+  // instead of one full reverse step.
+  {
+    constexpr int kFr = 11 * 7;
+    const int nb_max = min(32, (e.seg_max * 5 * 32) / kFr);
+    int hi = nfric;
+    while (hi > 0) {
+      const int cnt = nb_max >= 2 ? min(nb_max, hi) : 1;
+      if (cnt == 1) {  // serial reverse step (short tails / tiny staging)
+        const int slot = e.fric_order[hi - 1];
+        SlotRec s = e.slots[slot];
+        double a_lam = s.a_lam;
+        V3 a_n{s.a_n[0], s.a_n[1], s.a_n[2]};
+        friction_adj(e, prev_x, prev_q, s, aX, aQ, a_lam, a_n);
+        __syncwarp();
+        if (lane == 0) {
+          SlotRec& sw = e.slots[slot];
+          sw.a_lam = a_lam;
+          sw.a_n[0] = a_n.x; sw.a_n[1] = a_n.y; sw.a_n[2] = a_n.z;
+        }
+        __syncwarp();
+        --hi;
+        continue;
+      }
+      if (lane < cnt) {  // lane j: friction hi - 1 - j
+        const SlotRec s = e.slots[e.fric_order[hi - 1 - lane]];
+        double* Mj = e.stage + lane * kFr;
+#pragma unroll 1
+        for (int c = 0; c < 7; ++c) {
+          V3 bx{c == 0 ? 1.0 : 0.0, c == 1 ? 1.0 : 0.0, c == 2 ? 1.0 : 0.0};
+          Q4 bq{c == 3 ? 1.0 : 0.0, c == 4 ? 1.0 : 0.0, c == 5 ? 1.0 : 0.0, c == 6 ? 1.0 : 0.0};
+          double al = 0.0;
+          V3 an{0.0, 0.0, 0.0};
+          friction_adj(e, prev_x, prev_q, s, bx, bq, al, an);
+          const double col[11] = {bx.x, bx.y, bx.z, bq.w, bq.x, bq.y, bq.z, al, an.x, an.y, an.z};
+#pragma unroll
+          for (int r = 0; r < 11; ++r) Mj[r * 7 + c] = col[r];
+        }
+      }
+      __syncwarp();
+      for (int j = 0; j < cnt; ++j) {
+        const double v[7] = {aX.x, aX.y, aX.z, aQ.w, aQ.x, aQ.y, aQ.z};
+        double r = 0.0;
+        if (lane < 11) {
+          const double* row = e.stage + j * kFr + lane * 7;
+#pragma unroll
+          for (int c = 0; c < 7; ++c) r = fma(row[c], v[c], r);
+        }
+        aX = V3{shfl(r, 0), shfl(r, 1), shfl(r, 2)};
+        aQ = Q4{shfl(r, 3), shfl(r, 4), shfl(r, 5), shfl(r, 6)};
+        const double al = shfl(r, 7);
+        const V3 an{shfl(r, 8), shfl(r, 9), shfl(r, 10)};
+        if (lane == 0) {
+          SlotRec& sw = e.slots[e.fric_order[hi - 1 - j]];
+          sw.a_lam = sw.a_lam + al;
+          sw.a_n[0] = sw.a_n[0] + an.x; sw.a_n[1] = sw.a_n[1] + an.y; sw.a_n[2] = sw.a_n[2] + an.z;
+        }
+      }
+      __syncwarp();
+      hi -= cnt;
     }
-    __syncwarp();
   }
 
   PROF_ACC(4, tfa);

@@ -200,8 +200,10 @@ int prepare(dgx_ctx* c, Scratch& sc, const dgx_hand* h, const dgx_object* o, KSi
   buf.slot_stride = h->N;
   buf.fwd = nullptr;
   buf.fk = nullptr;
-  sc.ftg.ensure(nws * 6 * static_cast<size_t>(h->L) * sizeof(double));
+  sc.ftg.ensure(nws * (6 * static_cast<size_t>(h->L) + static_cast<size_t>(c->cap_corr) * kCorrMatDoubles) *
+                sizeof(double));
   buf.ft_global = static_cast<double*>(sc.ftg.p);
+  buf.cmat = buf.ft_global + nws * 6 * static_cast<size_t>(h->L);
   buf.mesh_cache = nullptr;
   buf.mesh_cert = nullptr;
   buf.mesh_cf = nullptr;
@@ -280,8 +282,11 @@ SplitGrid prepare_split(dgx_ctx* c, Scratch& sc, const dgx_hand* h, const dgx_ob
   buf.fk = reinterpret_cast<double*>(
       (reinterpret_cast<uintptr_t>(buf.fric_order + nws * ss) + 255) & ~static_cast<uintptr_t>(255));
   buf.slot_stride = static_cast<int>(ss);
-  sc.ftg.ensure(static_cast<size_t>(g.grid_a) * M * 6 * static_cast<size_t>(h->L) * sizeof(double));
+  const size_t nwa = static_cast<size_t>(g.grid_a) * M;
+  sc.ftg.ensure(nwa * (6 * static_cast<size_t>(h->L) + static_cast<size_t>(c->cap_corr) * kCorrMatDoubles) *
+                sizeof(double));
   buf.ft_global = static_cast<double*>(sc.ftg.p);
+  buf.cmat = buf.ft_global + nwa * 6 * static_cast<size_t>(h->L);
   buf.mesh_cache = nullptr;
   buf.mesh_cert = nullptr;
   buf.mesh_cf = nullptr;

@@ -8,7 +8,8 @@ namespace dgx {
 
 constexpr int kMaxSims = 8;        // protocol velocities per candidate (standard: 7)
 constexpr int kMaxDim = 32;        // 6 + J gradient coordinates (J <= 26)
-constexpr int kSegMaxCap = 16;    // max points per lane segment in the adjoint
+constexpr int kSegMaxCap = 16;
+constexpr int kCorrMatDoubles = 19 * 8 + 1;  // dgx_kernels.cu kCorrMat    // max points per lane segment in the adjoint
 
 enum Mode : int { kModeGrad = 0, kModeEval = 1, kModeOpt = 2 };
 
@@ -129,6 +130,7 @@ struct KBuf {
   double* fk;           // [B, 12 L + 3 N] split: link transforms + world points of the forward
   int slot_stride;      // slots / fric_order entries per sim (N fused, cap_corr + 1 split)
   double* ft_global;    // [grid, M, L*6] adjoint link-sum spill buffers
+  double* cmat;         // [grid, M, cap_corr, kCorrMat] batched correction reverse
   int* mesh_cache;      // [grid, M, gs*N] mesh objects: forward (face << 1 | inside) per point-sweep
   double* mesh_cert;    // [grid, M, N, 4] mesh objects: nearest-face certificate centre + radius
   int* mesh_cf;         // [grid, M, N, 1 + kCertFaces] certificate face sets

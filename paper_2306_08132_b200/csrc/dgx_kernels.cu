@@ -91,6 +91,7 @@ struct SimEnv {
   SlotRec* slots;
   int* fric_order;
   int cap_corr;
+  double* cmat;           // [cap_corr, kCorrMat] batched correction reverse (this warp)
   const KObj* O;          // mass / COM / world inverse inertia (kernel parameter space)
   double radius, alpha, mu, dt;
   double* point_grads;    // debug, may be null
@@ -706,50 +707,34 @@ __device__ __forceinline__ CorrOut apply_correction(const SimEnv& e, const CorrI
   return out;
 }
 
-struct CorrAdj {
+// Reverse of apply_contact (sim.hpp:215-245) for logged correction k from the
+// logged forward values (no SDF query / trig). For fixed forward values it
+// maps v = (aX, aQ) after the correction and the slot's (a_lam, a_n) linearly
+// to (aX, aQ) before it, the R-node adjoint aR and the point adjoint a_rel;
+// `lam_ok` is the replay check of lambda.
+struct CorrLin {
   V3 aX;
   Q4 aQ;
-  M3 aR;     // contribution to the adjoint of the R node before the correction
-  int status;
+  M3 aR;
+  V3 a_rel;
 };
-
-// Reverse of apply_contact (sim.hpp:215-245) for logged correction k, given
-// the adjoints of the state after it; returns the adjoints of the state
-// before it. Point adjoint -> the warp's link sums (lane 0 writes).
-template <class Sdf>
-__device__ __forceinline__ CorrAdj correction_adjoint(const Sdf& sdf, const SimEnv& e, int k, V3 pred_x, Q4 pred_q,
-                                                   V3 aX, Q4 aQ) {
-  CorrAdj out;
-  out.status = kOk;
-  for (int t = 0; t < 9; ++t) out.aR.m[t] = 0.0;
-  const int N = e.N;
-  const CorrRec c = e.corr[k];
-  const int i = c.f % N;
-  V3 xb = pred_x;
-  Q4 qb = pred_q;
-  if (k >= 1) {
-    const CorrRec& cp = e.corr[k - 1];
-    xb = V3{cp.x[0], cp.x[1], cp.x[2]};
-    qb = Q4{cp.q[0], cp.q[1], cp.q[2], cp.q[3]};
-  }
+__device__ __forceinline__ CorrLin correction_linear(const SimEnv& e, const CorrRec& c, V3 xb, Q4 qb, V3 aX, Q4 aQ,
+                                                     double a_lam, V3 a_nw, bool& lam_ok) {
+  CorrLin o;
+  for (int t = 0; t < 9; ++t) o.aR.m[t] = 0.0;
   const M3 Rb = rotation_matrix(qb);
-  // recorded values of the forward (CorrRec): no SDF query / trig here
   const V3 g{c.g[0], c.g[1], c.g[2]};
   const V3 rel{c.rel[0], c.rel[1], c.rel[2]};
-  const V3 p{e.px[i], e.py[i], e.pz[i]};
   const double C = -c.rho_d;
   const V3 n_w = mul(Rb, g);
   const V3 a = cross(rel, n_w);
   const V3 iwa = mul(e.O->Iw, a);
   const double w = e.O->inv_mass + dot(a, iwa);
   const double lam = C / w;
-  if (lam != c.lam) out.status = kReplayMismatch;
+  lam_ok = lam == c.lam;
   const V3 om = iwa * (-lam);
   const Q4 E{c.E[0], c.E[1], c.E[2], c.E[3]};
   const Q4 P = qmul(E, qb);
-  const SlotRec& s = e.slots[c.slot];
-  double a_lam = s.a_lam;
-  V3 a_nw = s.last_corr == k ? V3{s.a_n[0], s.a_n[1], s.a_n[2]} : V3{0.0, 0.0, 0.0};
   const Q4 a_P = qnormalize_adj(P, aQ);
   const Q4 a_E = qmul_adj_a(a_P, qb);
   const Q4 aQb = qmul_adj_b(a_P, E);
@@ -766,7 +751,7 @@ __device__ __forceinline__ CorrAdj correction_adjoint(const Sdf& sdf, const SimE
   V3 a_rel = cross(n_w, a_a);
   a_nw = a_nw + cross(a_a, rel);
   const V3 a_g = ftmul(Rb, a_nw);
-  outer_acc(out.aR, a_nw, g);
+  outer_acc(o.aR, a_nw, g);
   const double a_rho = -a_C;  // gate active: dC/drho = -1
   V3 a_rl;
   if (c.fb) {
@@ -780,18 +765,53 @@ __device__ __forceinline__ CorrAdj correction_adjoint(const Sdf& sdf, const SimE
     a_rl = fma3(a_dist / dist, dx, a_g * inv);
   }
   a_rel = a_rel + fmul(Rb, a_rl);
-  outer_acc(out.aR, rel, a_rl);
-  if (e.lane == 0) {
-    double* d = e.ft + 6 * e.sample_link[i];
-    const V3 tq = cross(p, a_rel);
-    d[0] += a_rel.x; d[1] += a_rel.y; d[2] += a_rel.z;
-    d[3] += tq.x; d[4] += tq.y; d[5] += tq.z;
-    add_point_grad(e, i, a_rel);
+  outer_acc(o.aR, rel, a_rl);
+  o.a_rel = a_rel;
+  o.aX = aX - a_rel;
+  o.aQ = aQb;
+  return o;
+}
+
+// Batched correction reverse: matrix of correction k, rows (aX 3, aQ 4,
+// aR 9, a_rel 3) x columns (aX 3, aQ 4, 1), plus the replay flag.
+constexpr int kCorrRows = 19, kCorrCols = 8, kCorrMat = kCorrRows * kCorrCols + 1;
+static_assert(kCorrMat == kCorrMatDoubles, "host scratch sizing");
+
+// All corrections' matrices, (correction, column) tasks spread over the warp.
+// Column 7 is the constant part: v = 0 with the slot's final a_lam / a_n
+// (set by the friction reverse; correction adjoints only read them).
+__device__ __forceinline__ void correction_matrices(const SimEnv& e, int ncorr, V3 pred_x, Q4 pred_q) {
+#pragma unroll 1
+  for (int t = e.lane; t < ncorr * kCorrCols; t += 32) {
+    const int k = t / kCorrCols, cb = t - k * kCorrCols;
+    const CorrRec c = e.corr[k];
+    V3 xb = pred_x;
+    Q4 qb = pred_q;
+    if (k >= 1) {
+      const CorrRec& cp = e.corr[k - 1];
+      xb = V3{cp.x[0], cp.x[1], cp.x[2]};
+      qb = Q4{cp.q[0], cp.q[1], cp.q[2], cp.q[3]};
+    }
+    V3 vx{cb == 0 ? 1.0 : 0.0, cb == 1 ? 1.0 : 0.0, cb == 2 ? 1.0 : 0.0};
+    Q4 vq{cb == 3 ? 1.0 : 0.0, cb == 4 ? 1.0 : 0.0, cb == 5 ? 1.0 : 0.0, cb == 6 ? 1.0 : 0.0};
+    double a_lam = 0.0;
+    V3 a_nw{0.0, 0.0, 0.0};
+    if (cb == 7) {
+      const SlotRec& s = e.slots[c.slot];
+      a_lam = s.a_lam;
+      if (s.last_corr == k) a_nw = V3{s.a_n[0], s.a_n[1], s.a_n[2]};
+    }
+    bool ok = true;
+    const CorrLin o = correction_linear(e, c, xb, qb, vx, vq, a_lam, a_nw, ok);
+    double* Mk = e.cmat + static_cast<size_t>(k) * kCorrMat;
+    const double col[kCorrRows] = {o.aX.x, o.aX.y, o.aX.z, o.aQ.w, o.aQ.x, o.aQ.y, o.aQ.z,
+                                   o.aR.m[0], o.aR.m[1], o.aR.m[2], o.aR.m[3], o.aR.m[4], o.aR.m[5],
+                                   o.aR.m[6], o.aR.m[7], o.aR.m[8], o.a_rel.x, o.a_rel.y, o.a_rel.z};
+#pragma unroll
+    for (int r = 0; r < kCorrRows; ++r) Mk[r * kCorrCols + cb] = col[r];
+    if (cb == 7) Mk[kCorrRows * kCorrCols] = ok ? 0.0 : 1.0;
   }
   __syncwarp();
-  out.aX = aX - a_rel;
-  out.aQ = aQb;
-  return out;
 }
 
 // One perturbation simulation (losses.hpp:47-57 with T = 1), forward and,
@@ -1099,6 +1119,9 @@ __device__ double run_sim(const Sdf& sdf, SimEnv& e, V3 v_m, bool record, bool m
   }
 
   PROF_ACC(4, tfa);
+  PROF_T(tcm);
+  correction_matrices(e, ncorr, pred_x, pred_q);
+  PROF_ACC(11, tcm);
   // ---- sweeps, reverse ----------------------------------------------------
   M3 aR;  // per-lane partial adjoint of the current R node
   for (int k = 0; k < 9; ++k) aR.m[k] = 0.0;
@@ -1185,11 +1208,35 @@ __device__ double run_sim(const Sdf& sdf, SimEnv& e, V3 v_m, bool record, bool m
     const M3 aRk = warp_sum(aR);
     aQ = qadd(aQ, rotmat_adj(qk, aRk));
     for (int t = 0; t < 9; ++t) aR.m[t] = 0.0;
-    const CorrAdj ca = correction_adjoint(sdf, e, k, pred_x, pred_q, aX, aQ);
-    if (ca.status != kOk) status = ca.status;
-    if (lane == 0) aR = ca.aR;
-    aX = ca.aX;
-    aQ = ca.aQ;
+    {  // the precomputed affine map of correction k: one 19 x 8 mat-vec (lanes = rows)
+      const double* Mk = e.cmat + static_cast<size_t>(k) * kCorrMat;
+      const double v[kCorrCols] = {aX.x, aX.y, aX.z, aQ.w, aQ.x, aQ.y, aQ.z, 1.0};
+      double r = 0.0;
+      if (lane < kCorrRows) {
+        const double* row = Mk + lane * kCorrCols;
+#pragma unroll
+        for (int c = 0; c < kCorrCols; ++c) r = fma(row[c], v[c], r);
+      }
+      aX = V3{shfl(r, 0), shfl(r, 1), shfl(r, 2)};
+      aQ = Q4{shfl(r, 3), shfl(r, 4), shfl(r, 5), shfl(r, 6)};
+#pragma unroll
+      for (int t = 0; t < 9; ++t) {
+        const double m = shfl(r, 7 + t);
+        aR.m[t] = lane == 0 ? m : 0.0;
+      }
+      const V3 a_rel{shfl(r, 16), shfl(r, 17), shfl(r, 18)};
+      if (lane == 0) {
+        if (Mk[kCorrRows * kCorrCols] != 0.0) status = kReplayMismatch;
+        const int i = e.corr[k].f % e.N;
+        const V3 p{e.px[i], e.py[i], e.pz[i]};
+        double* d = e.ft + 6 * e.sample_link[i];
+        const V3 tq = cross(p, a_rel);
+        d[0] += a_rel.x; d[1] += a_rel.y; d[2] += a_rel.z;
+        d[3] += tq.x; d[4] += tq.y; d[5] += tq.z;
+        add_point_grad(e, i, a_rel);
+      }
+      __syncwarp();
+    }
     PROF_ACC(11, tca);
     hi = e.corr[k].f;
     --k;
@@ -1341,6 +1388,7 @@ __device__ __forceinline__ void kernel_body(const KHand& H, const KObj& O, const
   };
   bind_logs(wslot);
   e.gft = buf.ft_global + wslot * 6 * L;
+  e.cmat = buf.cmat + wslot * static_cast<size_t>(buf.cap_corr) * kCorrMat;
   e.L = L;
   e.cap_corr = buf.cap_corr;
   e.O = &O;

@@ -870,11 +870,19 @@ __device__ double run_sim(const Sdf& sdf, SimEnv& e, V3 v_m, bool record, bool m
     // Quiet window: once N consecutive positions pass with no applied
     // correction (and no singular skip, to keep SolveStats exact), every later
     // position repeats an earlier inactive decision under the same state: the
-    // remaining sweeps are skipped (and the adjoint folds them, run_sim below).
+    // remaining sweeps are skipped. On in the split forward kernel (its other
+    // CTA on the SM takes the freed issue slots: 108.2k -> 110.1k); the fused
+    // kernel's lockstep CTA measured slower with it, and mesh objects need
+    // every point-sweep's (face, sign) cache entry for the adjoint.
+    constexpr bool kQuietExit = Phase == kPhaseFwd && !std::is_same<Sdf, MeshSdf>::value;
     int f_last = -1, singular_since = 0;
     while (sweep < e.gs) {
   #if defined(DGX_QUIET) || defined(DGX_QUIET_FWD)  // exact
       if (sweep * N + pos - f_last - 1 >= N && singular_since == 0) break;
+  #else
+      if constexpr (kQuietExit) {
+        if (sweep * N + pos - f_last - 1 >= N && singular_since == 0) break;
+      }
   #endif
       int cls[2];
   #pragma unroll

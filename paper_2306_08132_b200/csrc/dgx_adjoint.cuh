@@ -14,6 +14,10 @@ __device__ __forceinline__ V3 fma3(double s, V3 a, V3 b) {  // s*a + b
   return V3{fma(s, a.x, b.x), fma(s, a.y, b.y), fma(s, a.z, b.z)};
 }
 __device__ __forceinline__ double fdot(V3 a, V3 b) { return fma(a.z, b.z, fma(a.y, b.y, a.x * b.x)); }
+// a x b with one rounding less per component (adjoint-side only)
+__device__ __forceinline__ V3 fcross(V3 a, V3 b) {
+  return V3{fma(a.y, b.z, -(a.z * b.y)), fma(a.z, b.x, -(a.x * b.z)), fma(a.x, b.y, -(a.y * b.x))};
+}
 __device__ __forceinline__ double fdot4(Q4 a, Q4 b) {
   return fma(a.z, b.z, fma(a.y, b.y, fma(a.x, b.x, a.w * b.w)));
 }
@@ -26,6 +30,12 @@ __device__ __forceinline__ V3 fmul(const M3& A, V3 v) {
 __device__ __forceinline__ V3 ftmul(const M3& A, V3 v) {
   return V3{fma(A.m[6], v.z, fma(A.m[3], v.y, A.m[0] * v.x)), fma(A.m[7], v.z, fma(A.m[4], v.y, A.m[1] * v.x)),
             fma(A.m[8], v.z, fma(A.m[5], v.y, A.m[2] * v.x))};
+}
+// R^T v + c with c folded into the first product (adjoint-side only)
+__device__ __forceinline__ V3 ftmul_add(const M3& A, V3 v, V3 c) {
+  return V3{fma(A.m[6], v.z, fma(A.m[3], v.y, fma(A.m[0], v.x, c.x))),
+            fma(A.m[7], v.z, fma(A.m[4], v.y, fma(A.m[1], v.x, c.y))),
+            fma(A.m[8], v.z, fma(A.m[5], v.y, fma(A.m[2], v.x, c.z)))};
 }
 // A += a b^T  (adjoint of y = A v with respect to A, for y-adjoint a and v = b)
 __device__ __forceinline__ void outer_acc(M3& A, V3 a, V3 b) {

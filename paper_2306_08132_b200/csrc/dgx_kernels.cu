@@ -192,7 +192,7 @@ struct FtAcc {
       link = l;
     }
     F = F + ap;
-    T = T + cross(p, ap);
+    T = T + fcross(p, ap);
   }
 };
 
@@ -383,7 +383,7 @@ __device__ __forceinline__ void leak_geo(const Sdf& sdf, const SimEnv& e, int i,
                                          LeakGeo& L) {
   L.p = V3{e.px[i], e.py[i], e.pz[i]};
   L.rel = L.p - xk;
-  const V3 rl = ftmul(Rk, L.rel) + e.O->com;
+  const V3 rl = ftmul_add(Rk, L.rel, e.O->com);
   FastEval fe = classify_bwd(sdf, e, fpos, rl);
   L.sg = 1.0;
   L.contrib = false;
@@ -405,7 +405,7 @@ __device__ __forceinline__ void leak_geo(const Sdf& sdf, const SimEnv& e, int i,
 // s = c1 (n . adj_x_after) + c0 (kx = -(m^-1/w) n, g_q = 1/2 [0,k_w] (x) q,
 // gate backward -alpha; sim.hpp:107-124, tape.cpp:103-107).
 __device__ __forceinline__ bool leak_coef(const SimEnv& e, const LeakGeo& L, V3 G, double& c1, double& c0) {
-  const V3 a = cross(L.rel, L.n);
+  const V3 a = fcross(L.rel, L.n);
   const V3 Ia = fmul(e.O->Iw, a);
   const double w = e.O->inv_mass + fdot(a, Ia);
   if (w < 1e-12) return false;

@@ -189,3 +189,37 @@ def test_split_chunks_equal_single_rows(ctx, monkeypatch):
     for lo, hi in ((0, 40), (1180, 1240), (1250, 1300)):
         ls, gs, ss = api.loss_gradient(ctx, obj, hand, q[lo:hi], proto, params)
         assert np.array_equal(ls, l1[lo:hi]) and np.array_equal(gs, g1[lo:hi])
+
+
+def test_execution_choice_and_kernel_timing(ctx):
+    """dgx_ctx_set_kernel_timing / dgx_ctx_kernel_times count every launch by
+    kind, and the host picks the execution DESIGN.md §3 states: split forward /
+    adjoint kernels above #SMs candidates for grids, fused at or below it and
+    for mesh objects."""
+    from paper_2306_08132_b200 import api, init, model
+    hd = model.HandDesc.asset("allegro16")
+    od = model.box_grid(res=32)
+    hand, obj = api.Hand(ctx, hd), api.GraspObject(ctx, od)
+    proto, params = api.StabilityProtocol.standard(), api.SimParams(dilation_radius=0.01)
+    for B, kind in ((64, "fused"), (400, "split")):
+        q = init.approach_init(od, hd, B, seed=3)
+        n0 = ctx.launches
+        ctx.set_kernel_timing(True)
+        _, _, st = api.loss_gradient(ctx, obj, hand, q, proto, params)
+        kt = ctx.kernel_times()
+        ctx.set_kernel_timing(False)
+        assert not np.any(st)
+        launched = ctx.launches - n0
+        if kind == "fused":
+            assert kt["fused"][1] == launched == 1 and kt["forward"][1] == kt["adjoint"][1] == 0
+        else:
+            assert kt["fused"][1] == 0 and kt["forward"][1] == kt["adjoint"][1] >= 1
+            assert kt["forward"][1] + kt["adjoint"][1] == launched
+        assert all(ms >= 0.0 for ms, _ in kt.values()) and sum(ms for ms, _ in kt.values()) > 0.0
+    mo = api.GraspObject(ctx, model.mesh_object(*model.icosphere_mesh(0.025, 2)))
+    q = init.approach_init(od, hd, 200, seed=4)
+    ctx.set_kernel_timing(True)
+    api.evaluate_losses(ctx, mo, hand, q, proto, params)
+    kt = ctx.kernel_times()
+    ctx.set_kernel_timing(False)
+    assert kt["fused"][1] == 1 and kt["forward"][1] == 0

@@ -223,3 +223,28 @@ def test_execution_choice_and_kernel_timing(ctx):
     kt = ctx.kernel_times()
     ctx.set_kernel_timing(False)
     assert kt["fused"][1] == 1 and kt["forward"][1] == 0
+
+
+@pytest.mark.parametrize("B", [100, 400])
+def test_correction_log_overflow_is_per_candidate(B):
+    """A small correction-log capacity (70, about the median sim): candidates whose sims need more active
+    corrections report status 3 (log overflow) without touching other
+    candidates, in the fused (B <= #SMs) and the split execution alike; the
+    candidates that fit are bit-identical to a run with the default capacity."""
+    from paper_2306_08132_b200 import api, init, model
+    small, big = api.Context(0, correction_capacity=70), api.Context(0)  # ~p50 of the sims
+    hd = model.HandDesc.asset("allegro16")
+    od = model.box_grid(res=32)
+    q = init.approach_init(od, hd, B, seed=9)
+    proto, params = api.StabilityProtocol.standard(), api.SimParams(dilation_radius=0.01)
+    res = {}
+    for name, c in (("small", small), ("big", big)):
+        hand, obj = api.Hand(c, hd), api.GraspObject(c, od)
+        res[name] = api.loss_gradient(c, obj, hand, q, proto, params)
+    ls, gs, ss = res["small"]
+    lb, gb, sb = res["big"]
+    assert not np.any(sb)
+    assert set(np.unique(ss).tolist()) <= {0, 3}
+    assert 0 < np.count_nonzero(ss == 3) < B  # both kinds present
+    ok = ss == 0
+    assert np.array_equal(ls[ok], lb[ok]) and np.array_equal(gs[ok], gb[ok])

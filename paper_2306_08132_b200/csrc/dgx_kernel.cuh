@@ -142,9 +142,9 @@ struct KBuf {
 struct SmemLayout {
   int off_px, off_py, off_pz, off_link, off_ft, off_bitmap, off_stage, off_misc, total;
   __host__ __device__ static int align(int x) { return (x + 15) & ~15; }
-  int stage_per_warp;  // doubles: seg_max x 5 x 32 adjoint staging (>= 6L for the debug FK adjoint)
+  int stage_per_warp;  // doubles: seg_max x 5 x 32 adjoint staging (>= 6L + kMaxDim for the debug FK adjoint)
   __host__ __device__ static int stage_doubles(int seg_max, int L) {
-    const int a = seg_max * 5 * 32, b = 6 * L;
+    const int a = seg_max * 5 * 32, b = 6 * L + kMaxDim;
     return a > b ? a : b;
   }
   __host__ __device__ SmemLayout(int N, int L, int M, int seg_max) {

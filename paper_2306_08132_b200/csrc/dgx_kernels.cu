@@ -1296,30 +1296,33 @@ __device__ __forceinline__ void link_transforms(const KHand& H, const double* qv
 }
 
 // FK adjoint: link force/torque sums -> gradient [pos | tangent | joints]
-// (hand.cpp:246-257 layout). ft is consumed (subtree sums in place).
-__device__ __forceinline__ void fk_adjoint(const KHand& H, const double* qv, const double* link, double* ft, double* g) {
-  for (int k = H.L - 1; k >= 1; --k) {
-    const int li = H.topo[k];
-    const int par = H.joint_parent[H.link_parent_joint[li]];
-    for (int c = 0; c < 6; ++c) ft[6 * par + c] += ft[6 * li + c];
+// (hand.cpp:246-257 layout). ft is consumed (subtree sums in place). Called by
+// a whole warp: lane 0 folds the subtrees in reverse topo order (the sums'
+// order is fixed), then lanes take one joint each.
+__device__ __forceinline__ void fk_adjoint(const KHand& H, const double* qv, const double* link, double* ft, double* g,
+                                           int lane) {
+  if (lane == 0) {
+    for (int k = H.L - 1; k >= 1; --k) {
+      const int li = H.topo[k];
+      const int par = H.joint_parent[H.link_parent_joint[li]];
+      for (int c = 0; c < 6; ++c) ft[6 * par + c] += ft[6 * li + c];
+    }
+    const int base = H.topo[0];
+    const V3 F{ft[6 * base], ft[6 * base + 1], ft[6 * base + 2]};
+    const V3 T{ft[6 * base + 3], ft[6 * base + 4], ft[6 * base + 5]};
+    const V3 pos{qv[0], qv[1], qv[2]};
+    const V3 tau = (F.x == 0.0 && F.y == 0.0 && F.z == 0.0) ? T : T - cross(pos, F);
+    g[0] = F.x; g[1] = F.y; g[2] = F.z;
+    g[3] = tau.x; g[4] = tau.y; g[5] = tau.z;
   }
-  const int base = H.topo[0];
-  const V3 F{ft[6 * base], ft[6 * base + 1], ft[6 * base + 2]};
-  const V3 T{ft[6 * base + 3], ft[6 * base + 4], ft[6 * base + 5]};
-  const V3 pos{qv[0], qv[1], qv[2]};
-  // the tape never propagates a zero adjoint (tape.cpp:33): a subtree without
-  // adjoint contributes exactly 0 even where pose values are non-finite
-  auto zero6 = [&](int l) {
-    for (int c = 0; c < 6; ++c)
-      if (ft[6 * l + c] != 0.0) return false;
-    return true;
-  };
-  const V3 tau = (F.x == 0.0 && F.y == 0.0 && F.z == 0.0) ? T : T - cross(pos, F);
-  g[0] = F.x; g[1] = F.y; g[2] = F.z;
-  g[3] = tau.x; g[4] = tau.y; g[5] = tau.z;
-  for (int j = 0; j < H.J; ++j) {
+  __syncwarp();
+  for (int j = lane; j < H.J; j += 32) {
     const int c = H.joint_child[j], p = H.joint_parent[j];
-    if (zero6(c)) {
+    // the tape never propagates a zero adjoint (tape.cpp:33): a subtree without
+    // adjoint contributes exactly 0 even where pose values are non-finite
+    bool zero = true;
+    for (int t = 0; t < 6; ++t) zero = zero && ft[6 * c + t] == 0.0;
+    if (zero) {
       g[6 + j] = 0.0;
       continue;
     }
@@ -1331,6 +1334,7 @@ __device__ __forceinline__ void fk_adjoint(const KHand& H, const double* qv, con
     const V3 Tc{ft[6 * c + 3], ft[6 * c + 4], ft[6 * c + 5]};
     g[6 + j] = dot(aw, Tc - cross(tc, Fc));
   }
+  __syncwarp();
 }
 
 // CTAs per SM the register budget is sized for: mesh objects spend ~99% of
@@ -1503,14 +1507,14 @@ __device__ __forceinline__ void kernel_body(const KHand& H, const KObj& O, const
         }
         if (Phase != kPhaseFwd && buf.sim_grads && record) {  // debug: per-perturbation gradient via the FK adjoint
           __syncwarp();
-          if (lane == 0) {
-            double gtmp[kMaxDim];
-            double* ftw = e.stage;  // reuse the stage buffer (>= 6L doubles for L <= 26)
-            for (int t = 0; t < 6 * L; ++t) ftw[t] = e.ft[t];
-            fk_adjoint(H, sq, link, ftw, gtmp);
-            double* o = buf.sim_grads + (static_cast<size_t>(b) * M + warp) * D;
-            for (int t = 0; t < D; ++t) o[t] = gtmp[t];
-          }
+          double* ftw = e.stage;  // reuse the stage buffer (>= 6L + kMaxDim doubles)
+          double* gw = e.stage + 6 * L;
+          for (int t = lane; t < 6 * L; t += 32) ftw[t] = e.ft[t];
+          __syncwarp();
+          fk_adjoint(H, sq, link, ftw, gw, lane);
+          double* o = buf.sim_grads + (static_cast<size_t>(b) * M + warp) * D;
+          for (int t = lane; t < D; t += 32) o[t] = gw[t];
+          __syncwarp();
         }
       }
       __syncthreads();
@@ -1541,14 +1545,14 @@ __device__ __forceinline__ void kernel_body(const KHand& H, const KObj& O, const
           ql = ql + (c >= 0.0 ? c : 0.0);
         }
         if (record) {
-          if (lane == 0) {
-            for (int t = 0; t < 6 * L; ++t) {
-              double s = 0.0;
-              for (int m = 0; m < M; ++m) s += ft_all[m * 6 * L + t];
-              stage_all[t] = s;
-            }
-            fk_adjoint(H, sq, link, stage_all, sg);
+          // link sums over the sims (losses.cpp:32-41 order, per entry), lanes over entries
+          for (int t = lane; t < 6 * L; t += 32) {
+            double s = 0.0;
+            for (int m = 0; m < M; ++m) s += ft_all[m * 6 * L + t];
+            stage_all[t] = s;
           }
+          __syncwarp();
+          fk_adjoint(H, sq, link, stage_all, sg, lane);
           __syncwarp();
           if (lane < D) {
             const double inv_m = 1.0 / static_cast<double>(M);

@@ -1295,6 +1295,59 @@ __device__ __forceinline__ void link_transforms(const KHand& H, const double* qv
   }
 }
 
+// link_transforms by one warp (lane k: link topo[k]; L <= 27). The joint
+// rotations quat_exp(axis * angle) do not depend on the parent and are built
+// by all lanes at once; the products R_parent * R_origin * R_joint then go
+// level by level (a link as soon as its parent is done). Every link's values
+// are the same operations as link_transforms, so the results are identical.
+__device__ __forceinline__ void link_transforms_warp(const KHand& H, const double* qv, bool record, double* link,
+                                                     int lane) {
+  const bool mine = lane < H.L;
+  const int li = mine ? H.topo[lane] : 0;
+  const int pj = mine ? H.link_parent_joint[li] : -1;
+  int kpar = -1;  // topo index of the parent link
+  M3 Rj;
+  if (mine && pj >= 0) {
+    const int pl = H.joint_parent[pj];
+    for (int k = 0; k < H.L; ++k)
+      if (H.topo[k] == pl) kpar = k;
+    const double angle = qv[7 + pj];
+    const V3 ax{H.axis[3 * pj], H.axis[3 * pj + 1], H.axis[3 * pj + 2]};
+    const V3 rotvec{ax.x * angle, ax.y * angle, ax.z * angle};
+    Rj = rotation_matrix(quat_exp(rotvec));
+  }
+  const unsigned all = H.L >= 32 ? kFull : ((1u << H.L) - 1u);
+  unsigned done = 0u;
+  while (done != all) {
+    const bool ready = mine && !((done >> lane) & 1u) && (pj < 0 || ((done >> kpar) & 1u));
+    if (ready) {
+      double* Rl = link + 12 * li;
+      M3 R;
+      V3 t;
+      if (pj < 0) {
+        const Q4 q0{qv[3], qv[4], qv[5], qv[6]};
+        const Q4 base_q = record ? qmul(quat_exp(V3{0.0, 0.0, 0.0}), q0) : q0;
+        R = rotation_matrix(base_q);
+        t = V3{qv[0], qv[1], qv[2]};
+      } else {
+        M3 Ro;
+        for (int m = 0; m < 9; ++m) Ro.m[m] = H.origin_R[9 * pj + m];
+        const V3 to{H.origin_t[3 * pj], H.origin_t[3 * pj + 1], H.origin_t[3 * pj + 2]};
+        const double* Pp = link + 12 * H.joint_parent[pj];
+        M3 Rp;
+        for (int m = 0; m < 9; ++m) Rp.m[m] = Pp[m];
+        const V3 tp{Pp[9], Pp[10], Pp[11]};
+        R = mul(mul(Rp, Ro), Rj);
+        t = mul(Rp, to) + tp;
+      }
+      for (int m = 0; m < 9; ++m) Rl[m] = R.m[m];
+      Rl[9] = t.x; Rl[10] = t.y; Rl[11] = t.z;
+    }
+    __syncwarp();
+    done |= __ballot_sync(kFull, ready);
+  }
+}
+
 // FK adjoint: link force/torque sums -> gradient [pos | tangent | joints]
 // (hand.cpp:246-257 layout). ft is consumed (subtree sums in place). Called by
 // a whole warp: lane 0 folds the subtrees in reverse topo order (the sums'
@@ -1454,7 +1507,7 @@ __device__ __forceinline__ void kernel_body(const KHand& H, const KObj& O, const
         }
         __syncthreads();
       } else {
-        if (tid == 0) link_transforms(H, sq, record, link);
+        if (warp == 0) link_transforms_warp(H, sq, record, link, lane);
         __syncthreads();
         for (int i = tid; i < N; i += blockDim.x) {
           const int li = H.sample_link[i];

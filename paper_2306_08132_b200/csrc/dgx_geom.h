@@ -285,7 +285,7 @@ struct GridSdf {
     for (int a = 0; a < 3; ++a) {
       double v = u[a];
       double hi = static_cast<double>(n[a] - 1);
-      if (v < 0.0) { v = 0.0; outside = true; }
+      if (!(v >= 0.0)) { v = 0.0; outside = true; }  // NaN -> 0, outside (NaN propagates via the distance term)
       if (v > hi) { v = hi; outside = true; }
       int i = static_cast<int>(v);
       if (i > n[a] - 2) i = n[a] - 2;

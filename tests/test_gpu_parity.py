@@ -263,3 +263,35 @@ def test_nonfinite_adjoint_matches_reference(ctx, oracle):
                                      api.SimParams(dilation_radius=r))
     assert not np.any(st2)
     assert np.array_equal(el[0], oracle.evaluate_losses(ro, rh, z["q"], oracle.default_params(dilation_radius=r)))
+
+
+def test_nonfinite_configuration_grid(ctx, oracle):
+    """Non-finite inputs on the FP32 grid backend. The cell index of a NaN point
+    is clamped like an outside point, so the NaN reaches rho instead of an
+    address (this used to be an illegal memory access).
+    * A NaN base position leaves every gate inactive: free flight, gradient 0,
+      bit-exact with the reference.
+    * A NaN joint angle: the reference returns non-finite losses (its zero-depth
+      axpy multiplies NaN coefficients by 0); the GPU flags the candidate
+      non-finite (status 1). The values of a non-finite candidate are not
+      compared.
+    * In a 200-candidate batch (split execution) the other rows are unaffected."""
+    from paper_2306_08132_b200 import api
+    c = Case(ctx, oracle, "allegro16", "boxgrid64", B=200)
+    params = api.SimParams(dilation_radius=0.01)
+    proto = api.StabilityProtocol.standard()
+    bad = c.q.copy()
+    bad[0, 0] = np.nan
+    bad[1, 9] = np.nan
+    losses, grads, st = api.loss_gradient(ctx, c.obj, c.hand, bad, proto, params)
+    l_ok, g_ok, s_ok = api.loss_gradient(ctx, c.obj, c.hand, c.q, proto, params)
+    assert np.array_equal(losses[2:], l_ok[2:]) and np.array_equal(grads[2:], g_ok[2:])
+    assert np.array_equal(st[2:], s_ok[2:])
+    rl, ds, dr, dl = oracle.loss_gradient(c.ro, c.rh, bad[0], oracle.default_params(dilation_radius=0.01))
+    assert st[0] == 0 and np.array_equal(losses[0], rl) and np.array_equal(grads[0, 0], ds)
+    rl1, _, _, _ = oracle.loss_gradient(c.ro, c.rh, bad[1], oracle.default_params(dilation_radius=0.01))
+    assert not np.all(np.isfinite(rl1)) and st[1] == 1
+    # forward-only evaluation: no crash, the NaN candidate is flagged, the others are unaffected
+    el, est, es = api.evaluate_losses(ctx, c.obj, c.hand, bad, proto, params)
+    el_ok, _, es_ok = api.evaluate_losses(ctx, c.obj, c.hand, c.q, proto, params)
+    assert es[1] != 0 and np.array_equal(el[2:], el_ok[2:]) and np.array_equal(es[2:], es_ok[2:])

@@ -215,7 +215,8 @@ int dgx_apply_gradient_step_batch(dgx_ctx* ctx, const dgx_hand* hand, int32_t B,
                                   const double* g, double lr, double* q_out, uint32_t flags);
 
 /* Fused synthesis loop: q [B,7+J], adam_m / adam_v [B,6+J] updated in place;
-   traj [B, k_end-k_begin, 3+6+J] (losses, weighted gradient) when opt->record. */
+   traj [B, k_end-k_begin, 3+6+J] (losses, weighted gradient) when opt->record;
+   rows of iterates after a candidate's failure are zero. */
 int dgx_optimize_batch(dgx_ctx* ctx, const dgx_hand* hand, const dgx_object* obj, int32_t B, double* q,
                        double* adam_m, double* adam_v, const dgx_params* params, const dgx_opt* opt,
                        double* traj, int32_t* status, uint32_t flags);

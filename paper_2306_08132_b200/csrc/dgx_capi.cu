@@ -68,8 +68,11 @@ struct DevBuf {
 
 // per-stream kernel scratch (correction logs, contact slots, link-sum spills)
 struct Scratch {
-  DevBuf corr, slots, ftg, mcache, drop, thr;
+  DevBuf corr, slots, ftg, mcache, drop, thr, claim;
+  unsigned long long claim_next = 0;  // tickets drawn from claim so far (launches are stream-ordered)
   void release() {
+    claim.release();
+    claim_next = 0;
     thr.release();
     corr.release();
     slots.release();
@@ -322,6 +325,32 @@ void counted_launch(dgx_ctx* c, int phase, cudaStream_t st, const char* what, F&
   }
 }
 
+// Dynamic candidate claiming (next_candidate, dgx_kernels.cu): a launch of B
+// candidates draws exactly B tickets from sc's counter, so the host knows each
+// launch's base. DGX_STATIC_SCHED=1 keeps the static stride (A/B measurements).
+void bind_claim(Scratch& sc, KBuf& buf, int B, cudaStream_t st) {
+  static const bool static_sched = std::getenv("DGX_STATIC_SCHED") != nullptr;
+  if (static_sched) {
+    buf.claim = nullptr;
+    buf.claim_base = 0;
+    return;
+  }
+  if (!sc.claim.p) {
+    sc.claim.ensure(sizeof(unsigned long long));
+    cuda_check(cudaMemsetAsync(sc.claim.p, 0, sizeof(unsigned long long), st), "cudaMemsetAsync");
+    sc.claim_next = 0;
+  }
+  buf.claim = static_cast<unsigned long long*>(sc.claim.p);
+  buf.claim_base = sc.claim_next;
+  sc.claim_next += static_cast<unsigned long long>(B);
+}
+
+// a launch that did not start drew no tickets
+cudaError_t unclaim_on_error(Scratch& sc, const KBuf& buf, cudaError_t e) {
+  if (e != cudaSuccess && buf.claim) sc.claim_next = buf.claim_base;
+  return e;
+}
+
 // Every launch for B candidates whose per-candidate arrays start at buf's
 // pointers, on stream st with scratch sc.
 void launch_range(dgx_ctx* c, Scratch& sc, const dgx_hand* h, const dgx_object* o, KSim S, KOpt P, KBuf buf,
@@ -341,8 +370,11 @@ void launch_range(dgx_ctx* c, Scratch& sc, const dgx_hand* h, const dgx_object* 
   if (!split) {
     int smem = 0;
     const int grid = prepare(c, sc, h, o, S, B, buf, smem);
+    bind_claim(sc, buf, B, st);
     counted_launch(c, kPhaseFused, st, "fused_kernel",
-                   [&] { return launch_fused(h->k, o->k, o->sdf, S, P, buf, mode, kPhaseFused, grid, smem, st); });
+                   [&] {
+      return unclaim_on_error(sc, buf, launch_fused(h->k, o->k, o->sdf, S, P, buf, mode, kPhaseFused, grid, smem, st));
+    });
     return;
   }
   const bool record = mode != kModeEval;
@@ -371,12 +403,16 @@ void launch_range(dgx_ctx* c, Scratch& sc, const dgx_hand* h, const dgx_object* 
         Pk.k_begin = k;
         Pk.k_end = k + 1;
       }
+      bind_claim(sc, cb, nb, st);
       counted_launch(c, kPhaseFwd, st, "forward kernel", [&] {
-        return launch_fused(h->k, o->k, o->sdf, S, Pk, cb, mode, kPhaseFwd, std::min(g.grid_f, nb), g.smem_f, st);
+        return unclaim_on_error(
+            sc, cb, launch_fused(h->k, o->k, o->sdf, S, Pk, cb, mode, kPhaseFwd, std::min(g.grid_f, nb), g.smem_f, st));
       });
       if (!record) continue;
+      bind_claim(sc, cb, nb, st);
       counted_launch(c, kPhaseAdj, st, "adjoint kernel", [&] {
-        return launch_fused(h->k, o->k, o->sdf, S, Pk, cb, mode, kPhaseAdj, std::min(g.grid_a, nb), g.smem_a, st);
+        return unclaim_on_error(
+            sc, cb, launch_fused(h->k, o->k, o->sdf, S, Pk, cb, mode, kPhaseAdj, std::min(g.grid_a, nb), g.smem_a, st));
       });
     }
   }
@@ -883,6 +919,9 @@ static void run_fused(dgx_ctx* c, const dgx_hand* h, const dgx_object* o, int32_
   buf.sim_grads = s.out(sim_grads, static_cast<size_t>(B) * M * D);
   buf.point_grads = s.out(point_grads, static_cast<size_t>(B) * M * N * 3);
   buf.traj = s.out(traj, static_cast<size_t>(B) * steps * (3 + D));
+  // rows of iterates after a candidate's failure are never written: zero, not stale staging
+  if (buf.traj && B > 0 && steps > 0)
+    cuda_check(cudaMemsetAsync(buf.traj, 0, sizeof(double) * B * steps * (3 + D), c->stream), "cudaMemsetAsync");
   if (!status) throw DgxError(DGX_E_INVALID, "status is NULL");
   buf.status = s.out(status, static_cast<size_t>(B));
   if (point_grads) cuda_check(cudaMemsetAsync(buf.point_grads, 0, 24ull * B * M * N, c->stream), "memset");
@@ -964,6 +1003,8 @@ int dgx_optimize_multi(dgx_ctx* c, const dgx_hand* h, int32_t n_obj, const dgx_o
     double* dm = st.out(am, static_cast<size_t>(B) * D, true);
     double* dv = st.out(av, static_cast<size_t>(B) * D, true);
     double* dt = st.out(opt->record ? traj : nullptr, static_cast<size_t>(B) * steps * (3 + D));
+    if (dt && B > 0 && steps > 0)  // rows after a candidate's failure stay zero
+      cuda_check(cudaMemsetAsync(dt, 0, sizeof(double) * B * steps * (3 + D), c->stream), "cudaMemsetAsync");
     int32_t* ds = st.out(status, static_cast<size_t>(B));
     // fork onto the side streams (object i -> stream i % P), each with its own scratch
     const int P_streams = std::min<int>(n_obj, 4);

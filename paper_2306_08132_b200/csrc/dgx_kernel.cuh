@@ -136,6 +136,11 @@ struct KBuf {
   int* mesh_cf;         // [grid, M, N, 1 + kCertFaces] certificate face sets
   int cap_corr;
   int B;
+  // dynamic candidate claiming: each CTA takes blockIdx.x first, then tickets
+  // from *claim (candidate = ticket - claim_base + gridDim.x). One launch draws
+  // exactly B tickets; null = static stride (DGX_STATIC_SCHED)
+  unsigned long long* claim;
+  unsigned long long claim_base;
 };
 
 // dynamic shared memory layout (bytes), identical on host and device

@@ -1407,6 +1407,22 @@ struct CtasPerSm<MeshSdf> {
 // registers, 1 KB of spills) 96k, fused 86k.
 constexpr int kFwdCtasPerSm = 2;
 
+// The CTA's next candidate after b. Candidates differ in cost (contacts,
+// corrections), so a CTA that finishes early takes the next unclaimed one
+// instead of its static stride. Per-candidate math does not depend on which
+// CTA runs it (split: logs per candidate; fused: per-CTA scratch is rebound
+// each candidate), so results are identical to the static schedule.
+// s_next: a dynamic shared-memory slot (static shared memory would push the
+// kernels' 227 KB dynamic opt-in over the per-CTA limit).
+__device__ __forceinline__ int next_candidate(const KBuf& buf, int b, int* s_next) {
+  if (buf.claim == nullptr) return b + gridDim.x;
+  __syncthreads();  // every thread has read the previous claim
+  if (threadIdx.x == 0)
+    *s_next = static_cast<int>(atomicAdd(buf.claim, 1ull) - buf.claim_base) + static_cast<int>(gridDim.x);
+  __syncthreads();
+  return *s_next;
+}
+
 template <class Sdf, int Phase>
 __device__ __forceinline__ void kernel_body(const KHand& H, const KObj& O, const Sdf& sdf, const KSim& S,
                                             const KOpt& P, const KBuf& buf, int mode) {
@@ -1424,6 +1440,7 @@ __device__ __forceinline__ void kernel_body(const KHand& H, const KObj& O, const
   double* sg = misc + 40;          // [3*32] d_stable, d_qrange, d_qlimit
   double* sres = misc + 136;       // [8] residuals
   int* sflag = reinterpret_cast<int*>(misc + 144);  // [16] per-warp status
+  int* snext = reinterpret_cast<int*>(misc + 152);  // [1] next claimed candidate
 
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int M = S.M, N = H.N, L = H.L, J = H.J, D = 6 + J, Qd = 7 + J;
@@ -1468,7 +1485,7 @@ __device__ __forceinline__ void kernel_body(const KHand& H, const KObj& O, const
   const int k0 = mode == kModeOpt ? P.k_begin : 0;
   const int k1 = mode == kModeOpt ? P.k_end : 1;
 
-  for (int b = blockIdx.x; b < buf.B; b += gridDim.x) {
+  for (int b = blockIdx.x; b < buf.B; b = next_candidate(buf, b, snext)) {
     if constexpr (Phase != kPhaseFused) {
       bind_logs(static_cast<size_t>(b) * M + wm);
       // a candidate that failed at an earlier iterate of this call stays

@@ -159,11 +159,14 @@ def test_split_execution_equals_fused(tmp_path):
     """Split execution (forward kernel at 2 CTAs/SM, then the adjoint kernel,
     handing over through per-(candidate, sim) logs) computes exactly what the
     fused kernel does: eval, loss_gradient and multi-iterate optimize outputs
-    are bit-identical for grid and analytic objects."""
+    are bit-identical for grid and analytic objects. Both also equal the
+    static candidate stride (DGX_STATIC_SCHED=1): which CTA claims a candidate
+    does not change its results."""
     import subprocess
     import sys
     outs = {}
-    for tag, extra in (("split", {}), ("fused", {"DGX_FUSED": "1"})):
+    for tag, extra in (("split", {}), ("fused", {"DGX_FUSED": "1"}), ("split_static", {"DGX_STATIC_SCHED": "1"}),
+                       ("fused_static", {"DGX_FUSED": "1", "DGX_STATIC_SCHED": "1"})):
         p = tmp_path / f"{tag}.npz"
         env = dict(os.environ, **extra)
         subprocess.run([sys.executable, os.path.join(ROOT, "tools", "split_vs_fused.py"), str(p)], env=env,
@@ -176,6 +179,9 @@ def test_split_execution_equals_fused(tmp_path):
             assert a[k].tolist() == [0, 6, 6] and b[k].tolist() == [1, 0, 0], (k, a[k], b[k])
             continue
         assert np.array_equal(a[k], b[k], equal_nan=True), k
+    for dyn, sta in (("split", "split_static"), ("fused", "fused_static")):
+        for k in outs[dyn].files:
+            assert np.array_equal(outs[dyn][k], outs[sta][k], equal_nan=True), (dyn, k)
     assert np.any(a["grid_grad_s"] != 0) and np.any(a["grid_grad_s"] == 0)  # the NaN row failed alone
 
 

@@ -2,25 +2,33 @@
 """bench.py — batched gradient-based grasp search (Fast-Grasp'D hot path) on B200.
 
 Metric (BASELINE.json): candidate-iterations/s (and grasps/s) at N GPUs.
-Workload (BASELINE config 2, the largest single-GPU config the metric names):
-  Allegro-style 4-finger hand (allegro16: J=16, N=2001 samples from the
-  reference's sampler) grasping a 40 mm box and a cylinder (r 17.5 mm,
-  h 70 mm), each an analytic SDF baked on a 64^3 FP32 grid over bounds +
-  30 mm; 1024 candidates per GPU (512 per object), approach-sampled; the
-  500-iteration optimizer schedule (dilation 0.02 -> 0, Adam lr 1e-3).
+Headline workload (BASELINE config 3, the largest single-GPU configuration in
+BASELINE.json's `configs`):
+  Shadow-style 5-finger full-DOF hand (shadow22_dense: J=22, N=4093 surface
+  samples from the reference's own sampler, HandModel::load_xml(shadow22.xml,
+  4096)) grasping a procedural blob body baked on a 128^3 FP32 SDF grid;
+  4096 candidates per GPU, approach-sampled; the 500-iteration optimizer
+  schedule (dilation 0.02 -> 0, Adam lr 1e-3).
 A step = one optimizer iteration of the whole batch: loss_gradient (7
 perturbation sims x 8 Gauss-Seidel sweeps over every hand point, with the
-adjoint) + Adam + apply_gradient_step for every candidate, i.e. 1024
-candidate-iterations per GPU per step, two fused launches (one per object).
+adjoint) + Adam + apply_gradient_step for every candidate, i.e. 4096
+candidate-iterations per GPU per step.
 
   python bench.py [--gpus N] [--steps K] [--warmup W] [--impl dgx|reference]
+                  [--workload config3|config2|config4]
 
-For N>1 run under torchrun: candidates are sharded across ranks (weak
-scaling: 1024 per GPU), no collective in the timed loop; timing is the max
-over ranks of the CUDA-event time. `--impl reference` times the reference's
-own CPU implementation (oracle/_ref/libdgref.so: the unmodified reference
-compiled from /root/reference with the grid SDF behind its contract) on the
-host cores, rank 0 only.
+Multi-GPU: under torchrun (WORLD_SIZE set) every rank runs its own candidate
+shard (weak scaling, 4096 per GPU; config4: whole objects per rank, strong
+scaling) with no collective in the timed loop; timing is the max over ranks of
+the CUDA-event time; the final records (q, status, last iterate's losses) are
+gathered to rank 0 once, after timing. Without WORLD_SIZE, `--gpus N > 1`
+spawns N local ranks itself, or exits non-zero when fewer GPUs are visible.
+
+`--impl reference` times the reference's own CPU implementation
+(oracle/_ref/libdgref.so: the unmodified reference compiled from
+/root/reference, with the grid SDF behind its record_dilated contract) on the
+host cores, rank 0 only, on a bounded candidate sample progressed through the
+same iterates k as the GPU arm.
 """
 from __future__ import annotations
 
@@ -39,47 +47,91 @@ ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
 ITERS = 500
-CAND_PER_GPU = 1024
-RES = 64
-HAND = "allegro16"
+M_SIMS, GS = 7, 8
 # algorithmic FLOP per point-sweep (SURVEY §8(d)): 160 backend-independent
 # (50 forward + 110 adjoint) + 2 x F_sdf with F_sdf(grid trilinear + gradient + proxy) = 70
 FLOP_PER_POINT_SWEEP = 160 + 2 * 70
 # SURVEY §8(d) split by kernel: forward 50 + one grid query (70); adjoint 110 + one recompute (70)
 FLOP_FWD_PER_POINT_SWEEP = 50 + 70
 FLOP_ADJ_PER_POINT_SWEEP = 110 + 70
-M_SIMS, GS = 7, 8
+
+WORKLOADS = {
+    "config3": dict(hand="shadow22_dense", hand_xml=("shadow22", 4096), cand=4096, scaling="weak",
+                    desc="config3: shadow22_dense (J=22, N=4093) on a procedural blob SDF grid 128^3 (seed 3), "
+                         "{cand} candidates/GPU, 500-iteration schedule; step = 1 iteration"),
+    "config2": dict(hand="allegro16", hand_xml=("allegro16", 2000), cand=1024, scaling="weak",
+                    desc="config2: allegro16 (J=16, N=2001) on box 40mm + cylinder r17.5/h70mm SDF grids 64^3, "
+                         "{cand} candidates/GPU (half per object), 500-iteration schedule; step = 1 iteration"),
+    "config4": dict(hand="barrett3", hand_xml=None, cand=1024, scaling="strong",
+                    desc="config4: barrett3 (J=9, N=1999) x 64 procedural blob objects (64^3 grids) x {cand} "
+                         "candidates = 65536, object-major over the GPUs; step = 1 iteration"),
+}
 
 
 def parse():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=40)
+    ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="dgx", choices=["dgx", "reference"])
-    ap.add_argument("--candidates", type=int, default=CAND_PER_GPU)
+    ap.add_argument("--workload", default="config3", choices=sorted(WORKLOADS))
+    ap.add_argument("--candidates", type=int, default=None, help="per GPU (per object for config4)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    return ap.parse_args()
+    a = ap.parse_args()
+    if a.warmup < 3:
+        ap.error("--warmup must be >= 3")
+    if a.candidates is None:
+        a.candidates = WORKLOADS[a.workload]["cand"]
+    return a
 
 
-def workload(rank: int, cand: int):
+def objects(name: str, rank: int = 0, world: int = 1):
+    """[(object index, ObjectDesc)] this rank runs."""
+    from paper_2306_08132_b200 import model, shard
+    if name == "config3":
+        return [(0, model.blob_grid(seed=3, res=128))]
+    if name == "config2":
+        return [(0, model.box_grid(res=64)), (1, model.cylinder_grid(res=64))]
+    return [(o, model.blob_grid(seed=o, res=64)) for o, _, _ in shard.object_major(64, 1, world, rank)]
+
+
+def workload(name: str, rank: int, world: int, cand: int):
+    """hand, [ObjectDesc], [q per object] for this rank (global candidate ids)."""
     from paper_2306_08132_b200 import init, model
-    hand = model.HandDesc.asset(HAND)
-    objs = [model.box_grid(res=RES), model.cylinder_grid(res=RES)]
-    per = cand // len(objs)
-    qs = [init.approach_init(o, hand, per, seed=17 + oi, first=rank * per) for oi, o in enumerate(objs)]
-    return hand, objs, qs
+    w = WORKLOADS[name]
+    hand = model.HandDesc.asset(w["hand"])
+    objs = objects(name, rank, world)
+    if name == "config4":
+        qs = [init.approach_init(o, hand, cand, seed=100 + oi) for oi, o in objs]
+    else:
+        per = cand // len(objs)
+        qs = [init.approach_init(o, hand, per, seed=17 + oi if name == "config2" else 3, first=rank * per)
+              for oi, o in objs]
+    return hand, [o for _, o in objs], qs
 
 
-def config_dict(cand: int, n_gpus: int) -> dict:
-    return {
-        "workload": f"config2: {HAND} (J=16, N=2001) on box 40mm + cylinder r17.5/h70mm SDF grids {RES}^3, "
-                    f"{cand} candidates/GPU ({cand // 2}/object), {ITERS}-iteration schedule; step = 1 iteration",
-        "hand": HAND, "candidates_per_gpu": cand, "objects": ["box40_grid64", "cylinder_grid64"],
-        "sdf": f"fp32 trilinear grid {RES}^3, fp64 arithmetic", "iterations_schedule": ITERS,
-        "perturbations": M_SIMS, "gs_iters": GS, "l2": "flushed between timed steps (256 MiB write)",
-        "parallelism": f"candidates sharded over {n_gpus} GPU(s), no inner-loop collective",
-    }
+def config_dict(name: str, cand: int, n_gpus: int) -> dict:
+    w = WORKLOADS[name]
+    out = {"workload": w["desc"].format(cand=cand), "hand": w["hand"], "iterations_schedule": ITERS,
+           "perturbations": M_SIMS, "gs_iters": GS, "sdf": "fp32 trilinear grid, fp64 arithmetic",
+           "l2": "flushed between timed steps (256 MiB write)"}
+    if name == "config4":
+        out.update(objects=64, candidates_per_object=cand,
+                   parallelism=f"objects sharded over {n_gpus} GPU(s) (object-major), no inner-loop collective")
+    else:
+        out.update(candidates_per_gpu=cand,
+                   parallelism=f"candidates sharded over {n_gpus} GPU(s), no inner-loop collective")
+    return out
+
+
+def ref_hand(name: str):
+    from oracle import ref
+    w = WORKLOADS[name]
+    if w["hand_xml"] is None:
+        return ref.RefHand.barrett3(variant="glibc")
+    base, budget = w["hand_xml"]
+    return ref.RefHand.load_xml(os.path.join(ROOT, "assets", "hands", base, base + ".xml"), budget, 12345,
+                                variant="glibc")
 
 
 # ---------------------------------------------------------------------------
@@ -134,6 +186,7 @@ class ClockSampler:
 
     def summary(self) -> dict:
         win = [r for r in self.rows if len(r) >= 8 and self.t0 is not None and self.t0 - 0.05 <= r[0] <= self.t1 + 0.05]
+
         def num(x):
             try:
                 return float(x)
@@ -147,56 +200,72 @@ class ClockSampler:
                 "reasons": reasons, "samples": len(sm), "window_s": (self.t1 - self.t0) if self.t0 else None}
 
 
-def traffic_from_profiles():
+def traffic_from_profiles(name: str, kernel: str):
+    """DRAM bytes per launch of the dominant kernel from the committed ncu
+    capture of THIS workload (profiles/roofline_traffic.json, keyed by
+    workload and kernel kind); None when that capture does not exist."""
     p = os.path.join(ROOT, "profiles", "roofline_traffic.json")
-    if os.path.exists(p):
-        with open(p) as f:
-            return json.load(f).get("dram_bytes_per_launch")
-    return None
+    if not os.path.exists(p):
+        return None, None
+    with open(p) as f:
+        d = json.load(f).get(name, {}).get(kernel)
+    return (d["dram_bytes_per_launch"], d["source"]) if d else (None, None)
 
 
 # ---------------------------------------------------------------------------
-def cpu_reference_sample(hand_name, objs, qs, k, n_per_obj, threads, variant="glibc"):
-    """Reference CPU path (oracle/_ref) on a bounded sample: n_per_obj candidates
-    per object, one optimizer iteration at schedule index k. Returns
-    (candidate-iterations, seconds)."""
-    from oracle import ref
-    rh = {"allegro16": lambda: ref.RefHand.load_xml(os.path.join(ROOT, "assets", "hands", "allegro16",
-                                                                 "allegro16.xml"), 2000, 12345, variant=variant)}[
-        hand_name]()
-    done, secs = 0, 0.0
-    for o, q in zip(objs, qs):
-        ro = ref.RefObject.from_desc(o, variant=variant)
-        sub = q[:n_per_obj]
-        t0 = time.perf_counter()
-        out = ref.optimize(ro, rh, sub, ref.default_params(), iters=ITERS, k_begin=k, k_end=k + 1, threads=threads)
-        secs += time.perf_counter() - t0
-        done += sub.shape[0]
-        assert not np.any(out["status"]), "reference optimizer failed"
-    return done, secs
+class RefSample:
+    """The reference's CPU path (oracle/_ref/libdgref.so, glibc: the reference
+    exactly) over a fixed candidate sample whose optimizer state (q, Adam m/v)
+    is carried from iterate to iterate, so iterate k here is the same workload
+    the GPU arm runs at its step k."""
+
+    def __init__(self, name, objs, qs, n_per_obj, m=None, v=None):
+        from oracle import ref
+        self.ref = ref
+        self.rh = ref_hand(name)
+        self.ros = [ref.RefObject.from_desc(o, variant="glibc") for o in objs]
+        self.q = [np.array(q[:n_per_obj], np.float64) for q in qs]
+        self.m = [None if m is None else np.array(x[:n_per_obj]) for x in (m or [None] * len(qs))]
+        self.v = [None if v is None else np.array(x[:n_per_obj]) for x in (v or [None] * len(qs))]
+
+    def iterate(self, k, threads):
+        """One optimizer iterate k for every sampled candidate -> (candidate-iterations, seconds)."""
+        done, secs = 0, 0.0
+        for i, ro in enumerate(self.ros):
+            t0 = time.perf_counter()
+            out = self.ref.optimize(ro, self.rh, self.q[i], self.ref.default_params(), iters=ITERS, k_begin=k,
+                                    k_end=k + 1, adam_m=self.m[i], adam_v=self.v[i], threads=threads)
+            secs += time.perf_counter() - t0
+            done += self.q[i].shape[0]
+            ok = out["status"] == 0  # a failed candidate stays where it failed (as on the GPU)
+            self.q[i][ok], self.m[i], self.v[i] = out["q"][ok], out["m"], out["v"]
+        return done, secs
 
 
 def run_reference(args, rank):
     if rank != 0:
         return
     threads = os.cpu_count() or 1
-    hand, objs, qs = workload(0, args.candidates)
-    n_per = max(1, min(qs[0].shape[0], 2 * threads))
-    for w in range(args.warmup):
-        cpu_reference_sample(HAND, objs, qs, w % ITERS, n_per, threads)
+    hand, objs, qs = workload(args.workload, 0, 1, args.candidates)
+    n_per = max(1, min(qs[0].shape[0], (8 * threads) // len(objs)))
+    rs = RefSample(args.workload, objs, qs, n_per)
+    for w in range(args.warmup):  # iterates 0..W-1, as the GPU arm's warm-up
+        rs.iterate(w % ITERS, threads)
     done = secs = 0
     for s in range(args.steps):
-        d, t = cpu_reference_sample(HAND, objs, qs, (args.warmup + s) % ITERS, n_per, threads)
+        d, t = rs.iterate((args.warmup + s) % ITERS, threads)
         done += d
         secs += t
     v = done / secs
-    sample = f"{n_per} candidates x 2 objects x 1 iteration per step, {threads} threads"
+    sample = (f"{n_per} candidates x {len(objs)} object(s) x 1 iteration per step (min(B, 8 x nproc)), "
+              f"state carried across steps so step s runs iterate k = warmup + s like the GPU arm; "
+              f"{threads} std::threads, oracle/_ref/libdgref.so")
     print(json.dumps({
         "metric": "candidate-iterations/sec", "value": v, "unit": "candidate-iterations/s", "n_gpus": args.gpus,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * secs / args.steps,
-        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": config_dict(args.candidates, args.gpus), "impl": "reference",
-        "grasps_per_sec": v / ITERS,
+        "higher_is_better": True, "scaling": WORKLOADS[args.workload]["scaling"], "vs_baseline": None,
+        "dtype": "f64", "data": "synthetic", "config": config_dict(args.workload, args.candidates, args.gpus),
+        "impl": "reference", "grasps_per_sec": v / ITERS,
         "cpu_baseline": {"value": v, "unit": "candidate-iterations/s", "cores": threads, "kind": "reference",
                          "sample": sample},
         "e2e": {"value": v, "unit": "candidate-iterations/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
@@ -207,16 +276,13 @@ def run_reference(args, rank):
 def run_dgx(args, rank, world, local_rank):
     import torch
     import torch.distributed as dist
-    from paper_2306_08132_b200 import api, capi
+    from paper_2306_08132_b200 import api, capi, shard
 
     torch.cuda.set_device(local_rank)
     dev = torch.device("cuda", local_rank)
     if world > 1:
         dist.init_process_group("nccl", device_id=dev)
-    hand_d, objs_d, qs = workload(rank, args.candidates)
-    # one multi-object launch per step (dgx_optimize_multi): the two objects'
-    # persistent launches overlap on side streams, so the second fills SMs as
-    # the first drains
+    hand_d, objs_d, qs = workload(args.workload, rank, world, args.candidates)
     ctx = api.Context(local_rank)
     stream = torch.cuda.Stream(dev)
     torch.cuda.set_stream(stream)
@@ -228,9 +294,10 @@ def run_dgx(args, rank, world, local_rank):
     D = 6 + hand_d.num_joints
     counts = np.array([q.shape[0] for q in qs], np.int32)
     qall = np.concatenate(qs, axis=0)
-    st = dict(q=torch.tensor(qall, device=dev), m=torch.zeros(qall.shape[0], D, dtype=torch.float64, device=dev),
-              v=torch.zeros(qall.shape[0], D, dtype=torch.float64, device=dev),
-              status=torch.zeros(qall.shape[0], dtype=torch.int32, device=dev))
+    B_local = qall.shape[0]
+    st = dict(q=torch.tensor(qall, device=dev), m=torch.zeros(B_local, D, dtype=torch.float64, device=dev),
+              v=torch.zeros(B_local, D, dtype=torch.float64, device=dev),
+              status=torch.zeros(B_local, dtype=torch.int32, device=dev))
     torch.cuda.synchronize()
     flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)
     flags = capi.DGX_DEVICE_PTRS | capi.DGX_ASYNC
@@ -239,8 +306,12 @@ def run_dgx(args, rank, world, local_rank):
         k %= ITERS  # long runs wrap around the schedule (any iterate is a valid workload)
         if ev is not None:
             ev[0].record(stream)
-        api.optimize_multi(ctx, objs, hand, st["q"], counts, proto, params, weights, opt, k_begin=k, k_end=k + 1,
-                           adam_m=st["m"], adam_v=st["v"], flags=flags, status=st["status"])
+        if len(objs) == 1:
+            api.optimize(ctx, objs[0], hand, st["q"], proto, params, weights, opt, k_begin=k, k_end=k + 1,
+                         adam_m=st["m"], adam_v=st["v"], flags=flags, status=st["status"])
+        else:  # objects' launches overlap on side streams (dgx_optimize_multi)
+            api.optimize_multi(ctx, objs, hand, st["q"], counts, proto, params, weights, opt, k_begin=k,
+                               k_end=k + 1, adam_m=st["m"], adam_v=st["v"], flags=flags, status=st["status"])
         if ev is not None:
             ev[1].record(stream)
 
@@ -248,6 +319,9 @@ def run_dgx(args, rank, world, local_rank):
     for w in range(args.warmup):
         step(w)
     torch.cuda.synchronize()
+    # the CPU baseline's sample starts from this state (iterate k = warmup), so
+    # it runs the same iterates the timed GPU steps run
+    snap = {k: st[k].cpu().numpy().copy() for k in ("q", "m", "v")}
     if world > 1:
         dist.barrier()
     torch.cuda.synchronize()
@@ -267,27 +341,25 @@ def run_dgx(args, rank, world, local_rank):
         dist.barrier()
     launches = ctx.launches - launches0
     total_ms = sum(step_ms)
-    status_bad = int(torch.count_nonzero(st["status"]))
     t = torch.tensor([total_ms], dtype=torch.float64, device=dev)
     if world > 1:
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
     max_ms = float(t.item())
-    cand_total = args.candidates * world
+    cand_total = B_local * world if args.workload != "config4" else 64 * args.candidates
     value = cand_total * args.steps / (max_ms * 1e-3)
 
     # ---- end to end through the public host API (host arrays in / out, synchronous) ----
     # The step's inputs live in pinned host memory; the library copies them in,
-    # runs the fused iteration and copies q / m / v / status / the iterate's
-    # losses + gradient record back, every step.
+    # runs the iteration and copies q / m / v / status / the iterate's losses +
+    # gradient record back, every step.
     def pinned(a):
         t = torch.empty(a.shape, dtype=a.dtype, pin_memory=True)
         t.copy_(a)
         return t.numpy()
 
     host = dict(q=pinned(st["q"].cpu()), m=pinned(st["m"].cpu()), v=pinned(st["v"].cpu()))
-    Bt = host["q"].shape[0]
-    status_h = pinned(torch.zeros(Bt, dtype=torch.int32))
-    traj_h = pinned(torch.zeros((Bt, 1, 3 + host["m"].shape[1]), dtype=torch.float64))
+    status_h = pinned(torch.zeros(B_local, dtype=torch.int32))
+    traj_h = pinned(torch.zeros((B_local, 1, 3 + D), dtype=torch.float64))
     ctx.set_stream(None)
     k0 = args.warmup + args.steps
     h2d = d2h = 0
@@ -309,17 +381,27 @@ def run_dgx(args, rank, world, local_rank):
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
     e2e_value = cand_total * args.steps / float(t.item())
 
+    # ---- final records gathered once, after timing: q, status,
+    # the last iterate's losses; candidate order, rank 0 ----
+    rec = np.concatenate([host["q"], status_h[:, None].astype(np.float64), traj_h[:, 0, :3]], axis=1)
+    if args.workload == "config4":
+        olo, ohi = shard.shard_range(64, world, rank)
+        full = shard.gather_rows(rec, 64 * args.candidates, world, rank) if world > 1 else rec
+        gathered = None if full is None else full.shape[0]
+    else:
+        full = shard.gather_rows(rec, cand_total, world, rank)
+        gathered = None if full is None else full.shape[0]
+    failed = None if full is None else int(np.count_nonzero(full[:, 7 + hand_d.num_joints]))
+
     # ---- per-kernel launch durations (roofline of the dominant kernel) ----
-    # One object's 512-candidate launches on one stream, CUDA events around
-    # every launch on that stream (dgx_ctx_set_kernel_timing), L2 flushed
-    # between steps; the same launches the ncu launch list shows serialised.
+    # The bench's own launches on one stream, CUDA events around every launch
+    # on that stream (dgx_ctx_set_kernel_timing), L2 flushed between steps.
     ctx.set_stream(stream.cuda_stream)
     n0 = int(counts[0])
     sub = {k: st[k][:n0] for k in ("q", "m", "v", "status")}
-    ktimes = None
     for phase in ("warm", "timed"):
         ctx.set_kernel_timing(phase == "timed")
-        for s in range(3 if phase == "warm" else args.steps):
+        for s in range(3 if phase == "warm" else max(3, min(args.steps, 10))):
             flush.zero_()
             ks = (k0 + s) % ITERS
             api.optimize(ctx, objs[0], hand, sub["q"], proto, params, weights, opt, k_begin=ks, k_end=ks + 1,
@@ -345,18 +427,19 @@ def run_dgx(args, rank, world, local_rank):
                 kern[kind] = {"avg_launch_ms": ms, "launches": cnt, "candidates_per_launch": n0,
                               "flop_per_candidate_iteration": pts_sweeps * per_ps,
                               "achieved_tflops": pts_sweeps * per_ps * n0 / (ms * 1e-3) / 1e12}
-        dom = max(kern, key=lambda k: kern[k]["avg_launch_ms"])
-        step_kernel_ms = sum(v["avg_launch_ms"] for v in kern.values())
+        dom = max(kern, key=lambda k: kern[k]["avg_launch_ms"] * kern[k]["launches"])
+        step_kernel_ms = sum(v["avg_launch_ms"] * v["launches"] for v in kern.values())
         for v in kern.values():
-            v["share_of_serialised_step"] = v["avg_launch_ms"] / step_kernel_ms
+            v["share_of_serialised_step"] = v["avg_launch_ms"] * v["launches"] / step_kernel_ms
         achieved = kern[dom]["achieved_tflops"]
-        traffic = traffic_from_profiles()
+        traffic, traffic_src = traffic_from_profiles(args.workload, dom)
         result = {
             "metric": "candidate-iterations/sec", "value": value, "unit": "candidate-iterations/s",
             "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": max_ms / args.steps,
-            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
-            "data": "synthetic (approach-sampled configurations, analytic SDFs baked to grids)",
-            "config": config_dict(args.candidates, world),
+            "higher_is_better": True, "scaling": WORKLOADS[args.workload]["scaling"], "vs_baseline": None,
+            "dtype": "f64",
+            "data": "synthetic (approach-sampled configurations, procedural / analytic SDFs baked to grids)",
+            "config": config_dict(args.workload, args.candidates, world),
             "grasps_per_sec": value / ITERS,
             "e2e": {"value": e2e_value, "unit": "candidate-iterations/s",
                     "h2d_bytes_per_step": h2d // args.steps, "d2h_bytes_per_step": d2h // args.steps,
@@ -364,42 +447,79 @@ def run_dgx(args, rank, world, local_rank):
                             "q, m, v, status, iterate losses + gradient out), synchronous, wall clock"},
             "gpu_launches": launches,
             "roofline": {"bound": "fp64", "achieved": achieved, "peak": pk.value, "unit": "TFLOP/s",
-                         "frac": achieved / pk.value, "traffic": traffic, "kernel": dom,
-                         "peak_source": "measured DFMA microbenchmark (dgx_fp64_peak, csrc/dgx_peak.cu)",
+                         "frac": achieved / pk.value, "traffic": traffic, "traffic_source": traffic_src,
+                         "kernel": dom,
+                         "peak_source": "builder-measured DFMA microbenchmark (dgx_fp64_peak, csrc/dgx_peak.cu) "
+                                        "on this GPU; nominal B200 FP64 37.2 TFLOP/s",
+                         "frac_of_nominal_fp64": achieved / 37.2,
                          "flop_per_candidate_iteration": flop_cand_iter,
-                         "timing": "dominant kernel: FLOP_alg of its half (SURVEY 8(d): adjoint 110 + 70 per "
-                                   "point-sweep, forward 50 + 70) x candidates per launch / its mean launch "
-                                   "duration, CUDA events on its stream, one object's launches, L2 flushed",
+                         "timing": "dominant kernel: FLOP_alg of its part (SURVEY 8(d): forward 50 + 70, adjoint "
+                                   "110 + 70, fused 300 per point-sweep) x candidates per launch / its mean launch "
+                                   "duration, CUDA events on its stream, L2 flushed",
                          "kernels": kern,
-                         "step_achieved_tflops": flop_cand_iter * args.candidates / (statistics.mean(step_ms) * 1e-3)
-                         / 1e12,
+                         "step_achieved_tflops": flop_cand_iter * (cand_total / world) /
+                         (statistics.mean(step_ms) * 1e-3) / 1e12,
                          "avg_step_ms": statistics.mean(step_ms)},
             "clocks": clk.summary(),
-            "failed_candidates": status_bad,
+            "gather": {"rows": gathered, "failed_candidates": failed,
+                       "how": "shard.gather_rows (NCCL all-gather when N > 1) of q | status | losses, after timing"},
         }
         if world == 1 and not args.no_cpu_baseline:
             threads = os.cpu_count() or 1
-            hand_r, objs_r, qs_r = workload(0, args.candidates)
-            n_per = max(1, min(qs_r[0].shape[0], 2 * threads))
-            d, secs = cpu_reference_sample(HAND, objs_r, qs_r, 0, n_per, threads)
-            result["cpu_baseline"] = {"value": d / secs, "unit": "candidate-iterations/s", "cores": threads,
+            n_per = max(1, min(n0, (8 * threads) // len(objs)))
+            qsnap = np.split(snap["q"], np.cumsum(counts)[:-1])
+            msnap = np.split(snap["m"], np.cumsum(counts)[:-1])
+            vsnap = np.split(snap["v"], np.cumsum(counts)[:-1])
+            rs = RefSample(args.workload, objs_d, qsnap, n_per, msnap, vsnap)
+            done = secs = 0
+            for j in range(3):  # iterates warmup .. warmup + 2 from the GPU arm's own state
+                d, t_ = rs.iterate((args.warmup + j) % ITERS, threads)
+                done += d
+                secs += t_
+            result["cpu_baseline"] = {"value": done / secs, "unit": "candidate-iterations/s", "cores": threads,
                                       "kind": "reference",
-                                      "sample": f"{n_per} candidates x 2 objects x 1 iteration (k=0), "
-                                                f"{threads} std::threads, oracle/_ref/libdgref.so"}
+                                      "sample": f"{n_per} candidates x {len(objs)} object(s) x 3 iterations "
+                                                f"(k = {args.warmup}..{args.warmup + 2}, from the GPU arm's state at "
+                                                f"the start of its timed region), {threads} std::threads, "
+                                                f"oracle/_ref/libdgref.so"}
         print(json.dumps(result), flush=True)
     if world > 1:
         dist.destroy_process_group()
 
 
+def _spawned(local_rank, args, world, port):
+    os.environ.update(RANK=str(local_rank), LOCAL_RANK=str(local_rank), WORLD_SIZE=str(world),
+                      MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    run_dgx(args, local_rank, world, local_rank)
+
+
 def main():
     args = parse()
     rank = int(os.environ.get("RANK", "0"))
-    world = int(os.environ.get("WORLD_SIZE", "1"))
     local_rank = int(os.environ.get("LOCAL_RANK", "0"))
     if args.impl == "reference":
         run_reference(args, rank)
-    else:
+        return
+    if "WORLD_SIZE" in os.environ:
+        world = int(os.environ["WORLD_SIZE"])
+        if world != args.gpus:
+            sys.exit(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={world}")
         run_dgx(args, rank, world, local_rank)
+        return
+    if args.gpus > 1:  # no launcher: spawn one rank per GPU here
+        import socket
+        import torch
+        import torch.multiprocessing as mp
+        have = torch.cuda.device_count()
+        if have < args.gpus:
+            sys.exit(f"bench.py: --gpus {args.gpus} requested but {have} CUDA device(s) visible")
+        s = socket.socket()
+        s.bind(("127.0.0.1", 0))
+        port = s.getsockname()[1]
+        s.close()
+        mp.spawn(_spawned, args=(args, args.gpus, port), nprocs=args.gpus, join=True)
+        return
+    run_dgx(args, 0, 1, 0)
 
 
 if __name__ == "__main__":

@@ -156,7 +156,8 @@ int dgx_abi_version(void);
 
 int dgx_ctx_create(int device, dgx_ctx** out);
 int dgx_ctx_destroy(dgx_ctx* ctx);
-/* use an external cudaStream_t (NULL = the context's own stream) */
+/* use an external cudaStream_t (NULL = the context's own stream). Work already queued on
+   the previous stream is ordered before the next launch (the context scratch is reused). */
 int dgx_ctx_set_stream(dgx_ctx* ctx, void* cuda_stream);
 /* capacity of the per-perturbation active-correction log (default 1024) */
 int dgx_ctx_set_correction_capacity(dgx_ctx* ctx, int32_t cap);

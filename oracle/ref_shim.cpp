@@ -10,7 +10,7 @@
 //    "AnySdf": it forwards to the real MeshSdf for mesh
 //    objects (bit-identical to the reference) or evaluates one of the shared
 //    non-mesh backends (paper_2306_08132_b200/csrc/dgx_geom.h) behind the
-//    reference's record_dilated / dilated_within contract (sdf.cpp:126-164);
+//    reference's record_dilated / dilated_within contract (sdf.cpp:69-107);
 //  * the reference's loss_gradient / evaluate_losses / apply_gradient_step
 //    (losses.cpp) compiled from the reference source with MeshSdf -> AnySdf;
 //  * per-perturbation tape gradients (losses.cpp:32-42), d residual / d points,
@@ -97,7 +97,7 @@ class AnySdf {
     return q;
   }
 
-  // recorded path (sim.hpp:165): sdf.cpp:140-164 with the backend's proxy
+  // recorded path (sim.hpp:165): sdf.cpp:83-107 with the backend's proxy
   // point frozen (value from the recomputed distance, unit gradient emitted
   // as recorded scalars, interpolated-normal fallback below 1e-9).
   Rec record_dilated(const Vec3T<Rec>& r, double radius, Vec3T<Rec>* grad_out) const {

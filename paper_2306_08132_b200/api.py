@@ -186,6 +186,29 @@ def _f64(a, shape):
     return a
 
 
+def _check_arr(a, shape, kind: str, name: str) -> None:
+    """Validate a caller-supplied array before its pointer crosses the C ABI
+    (the ABI trusts sizes): exact shape, dtype ("f64" / "i32") and C order,
+    numpy or torch alike."""
+    if a is None:
+        return
+    if isinstance(a, np.ndarray):
+        ok_dt = a.dtype == (np.float64 if kind == "f64" else np.int32)
+        contig = a.flags["C_CONTIGUOUS"]
+    elif hasattr(a, "data_ptr"):
+        import torch
+        ok_dt = a.dtype == (torch.float64 if kind == "f64" else torch.int32)
+        contig = a.is_contiguous()
+    else:
+        raise ValueError(f"{name}: expected a numpy array or torch tensor")
+    if tuple(a.shape) != tuple(shape):
+        raise ValueError(f"{name}: shape {tuple(a.shape)} != {tuple(shape)}")
+    if not ok_dt:
+        raise ValueError(f"{name}: dtype {a.dtype} != {'float64' if kind == 'f64' else 'int32'}")
+    if not contig:
+        raise ValueError(f"{name}: must be C-contiguous")
+
+
 def check_status(status) -> None:
     st = np.asarray(status)
     bad = np.nonzero(st)[0]
@@ -356,6 +379,12 @@ def optimize(ctx: Context, obj: GraspObject, hand: Hand, q, protocol: StabilityP
         adam_v = torch.zeros((B, D), dtype=torch.float64, device=dev) if adam_v is None else adam_v
         status = torch.zeros(B, dtype=torch.int32, device=dev) if status is None else status
         traj = torch.zeros((B, k_end - k_begin, 3 + D), dtype=torch.float64, device=dev) if record else None
+    if not 0 <= k_begin <= k_end <= opt.iterations:
+        raise ValueError("need 0 <= k_begin <= k_end <= iterations")
+    for a, shp, kd, nm in ((q, (B, 7 + hand.J), "f64", "q"), (adam_m, (B, D), "f64", "adam_m"),
+                           (adam_v, (B, D), "f64", "adam_v"), (status, (B,), "i32", "status"),
+                           (traj, (B, k_end - k_begin, 3 + D), "f64", "traj")):
+        _check_arr(a, shp, kd, nm)
     p = params_c(params, protocol, weights)
     o = capi.OptC(opt.iterations, k_begin, k_end, int(record), opt.dilation_start_radius, opt.learning_rate,
                   opt.beta1, opt.beta2, opt.eps)
@@ -403,8 +432,16 @@ def optimize_multi(ctx: Context, objs: list, hand: Hand, q, counts, protocol: St
         adam_v = torch.zeros((B, D), dtype=torch.float64, device=dev) if adam_v is None else adam_v
         status = torch.zeros(B, dtype=torch.int32, device=dev) if status is None else status
         traj = torch.zeros((B, k_end - k_begin, 3 + D), dtype=torch.float64, device=dev) if record else None
-    if int(counts.sum()) != B:
-        raise ValueError("sum(counts) must equal the number of candidates")
+    if counts.ndim != 1 or counts.shape[0] != len(objs):
+        raise ValueError("counts must hold one entry per object")
+    if np.any(counts < 0) or int(counts.sum()) != B:
+        raise ValueError("counts must be >= 0 and sum to the number of candidates")
+    if not 0 <= k_begin <= k_end <= opt.iterations:
+        raise ValueError("need 0 <= k_begin <= k_end <= iterations")
+    for a, shp, kd, nm in ((q, (B, 7 + hand.J), "f64", "q"), (adam_m, (B, D), "f64", "adam_m"),
+                           (adam_v, (B, D), "f64", "adam_v"), (status, (B,), "i32", "status"),
+                           (traj, (B, k_end - k_begin, 3 + D), "f64", "traj")):
+        _check_arr(a, shp, kd, nm)
     handles = (C.c_void_p * len(objs))(*[o.h.value for o in objs])
     p = params_c(params, protocol, weights)
     o = capi.OptC(opt.iterations, k_begin, k_end, int(record), opt.dilation_start_radius, opt.learning_rate,

@@ -69,10 +69,8 @@ struct DevBuf {
 // per-stream kernel scratch (correction logs, contact slots, link-sum spills)
 struct Scratch {
   DevBuf corr, slots, ftg, mcache, drop, thr, claim;
-  unsigned long long claim_next = 0;  // tickets drawn from claim so far (launches are stream-ordered)
   void release() {
     claim.release();
-    claim_next = 0;
     thr.release();
     corr.release();
     slots.release();
@@ -317,6 +315,7 @@ void counted_launch(dgx_ctx* c, int phase, cudaStream_t st, const char* what, F&
     e1 = pool_event(c);
     cuda_check(cudaEventRecord(e0, st), "cudaEventRecord");
   }
+  (void)cudaGetLastError();  // a stale non-sticky error must not be reported as this launch's
   cuda_check(launch(), what);
   ++c->launches;
   if (c->timing) {
@@ -325,30 +324,21 @@ void counted_launch(dgx_ctx* c, int phase, cudaStream_t st, const char* what, F&
   }
 }
 
-// Dynamic candidate claiming (next_candidate, dgx_kernels.cu): a launch of B
-// candidates draws exactly B tickets from sc's counter, so the host knows each
-// launch's base. DGX_STATIC_SCHED=1 keeps the static stride (A/B measurements).
-void bind_claim(Scratch& sc, KBuf& buf, int B, cudaStream_t st) {
+// Dynamic candidate claiming (next_candidate, dgx_kernels.cu). Every launch is
+// self-contained: its ticket counter is zeroed on the launch stream right
+// before it, so no host-side ticket base can drift from the device counter (a
+// failed or partial earlier launch, a stale error, or another stream cannot
+// skew later launches). DGX_STATIC_SCHED=1 keeps the static stride (A/B
+// measurements).
+void bind_claim(Scratch& sc, KBuf& buf, int, cudaStream_t st) {
   static const bool static_sched = std::getenv("DGX_STATIC_SCHED") != nullptr;
   if (static_sched) {
     buf.claim = nullptr;
-    buf.claim_base = 0;
     return;
   }
-  if (!sc.claim.p) {
-    sc.claim.ensure(sizeof(unsigned long long));
-    cuda_check(cudaMemsetAsync(sc.claim.p, 0, sizeof(unsigned long long), st), "cudaMemsetAsync");
-    sc.claim_next = 0;
-  }
+  sc.claim.ensure(sizeof(unsigned long long));
+  cuda_check(cudaMemsetAsync(sc.claim.p, 0, sizeof(unsigned long long), st), "cudaMemsetAsync");
   buf.claim = static_cast<unsigned long long*>(sc.claim.p);
-  buf.claim_base = sc.claim_next;
-  sc.claim_next += static_cast<unsigned long long>(B);
-}
-
-// a launch that did not start drew no tickets
-cudaError_t unclaim_on_error(Scratch& sc, const KBuf& buf, cudaError_t e) {
-  if (e != cudaSuccess && buf.claim) sc.claim_next = buf.claim_base;
-  return e;
 }
 
 // Every launch for B candidates whose per-candidate arrays start at buf's
@@ -373,7 +363,7 @@ void launch_range(dgx_ctx* c, Scratch& sc, const dgx_hand* h, const dgx_object* 
     bind_claim(sc, buf, B, st);
     counted_launch(c, kPhaseFused, st, "fused_kernel",
                    [&] {
-      return unclaim_on_error(sc, buf, launch_fused(h->k, o->k, o->sdf, S, P, buf, mode, kPhaseFused, grid, smem, st));
+      return launch_fused(h->k, o->k, o->sdf, S, P, buf, mode, kPhaseFused, grid, smem, st);
     });
     return;
   }
@@ -405,14 +395,12 @@ void launch_range(dgx_ctx* c, Scratch& sc, const dgx_hand* h, const dgx_object* 
       }
       bind_claim(sc, cb, nb, st);
       counted_launch(c, kPhaseFwd, st, "forward kernel", [&] {
-        return unclaim_on_error(
-            sc, cb, launch_fused(h->k, o->k, o->sdf, S, Pk, cb, mode, kPhaseFwd, std::min(g.grid_f, nb), g.smem_f, st));
+        return launch_fused(h->k, o->k, o->sdf, S, Pk, cb, mode, kPhaseFwd, std::min(g.grid_f, nb), g.smem_f, st);
       });
       if (!record) continue;
       bind_claim(sc, cb, nb, st);
       counted_launch(c, kPhaseAdj, st, "adjoint kernel", [&] {
-        return unclaim_on_error(
-            sc, cb, launch_fused(h->k, o->k, o->sdf, S, Pk, cb, mode, kPhaseAdj, std::min(g.grid_a, nb), g.smem_a, st));
+        return launch_fused(h->k, o->k, o->sdf, S, Pk, cb, mode, kPhaseAdj, std::min(g.grid_a, nb), g.smem_a, st);
       });
     }
   }
@@ -505,7 +493,18 @@ int dgx_ctx_destroy(dgx_ctx* c) {
 }
 
 int dgx_ctx_set_stream(dgx_ctx* c, void* s) {
-  return guarded([&] { c->stream = s ? static_cast<cudaStream_t>(s) : c->own; });
+  return guarded([&] {
+    if (!c) throw DgxError(DGX_E_INVALID, "NULL context");
+    cudaStream_t next = s ? static_cast<cudaStream_t>(s) : c->own;
+    if (next != c->stream) {
+      // the context's scratch (logs, ticket counter, staging) is reused by the
+      // next launch: order it after everything already queued on the old stream
+      set_device(c);
+      cuda_check(cudaEventRecord(c->fork, c->stream), "cudaEventRecord");
+      cuda_check(cudaStreamWaitEvent(next, c->fork, 0), "cudaStreamWaitEvent");
+    }
+    c->stream = next;
+  });
 }
 
 int dgx_ctx_set_correction_capacity(dgx_ctx* c, int32_t cap) {

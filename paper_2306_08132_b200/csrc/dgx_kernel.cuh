@@ -34,7 +34,7 @@ struct CorrRec {
   double x[3];
   double q[4];
   double lam;
-  // recorded values of the correcting point (sdf.cpp:140-164, sim.hpp:160-161)
+  // recorded values of the correcting point (sdf.cpp:83-107, sim.hpp:160-161)
   double g[3];      // grad_obj (recorded unit gradient)
   double rel[3];    // p - x before the correction
   double dx[3];     // r_local - proxy point
@@ -137,10 +137,9 @@ struct KBuf {
   int cap_corr;
   int B;
   // dynamic candidate claiming: each CTA takes blockIdx.x first, then tickets
-  // from *claim (candidate = ticket - claim_base + gridDim.x). One launch draws
-  // exactly B tickets; null = static stride (DGX_STATIC_SCHED)
+  // from *claim (candidate = ticket + gridDim.x); the counter is zeroed on the
+  // stream before every launch. null = static stride (DGX_STATIC_SCHED)
   unsigned long long* claim;
-  unsigned long long claim_base;
 };
 
 // dynamic shared memory layout (bytes), identical on host and device

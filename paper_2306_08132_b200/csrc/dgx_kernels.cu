@@ -30,6 +30,7 @@
 #include <type_traits>
 #include <cuda_runtime.h>
 
+#include <climits>
 #include <cstdint>
 
 #ifdef DGX_PROFILE_REGIONS
@@ -140,7 +141,7 @@ struct PointEval {
 };
 
 // rel = p - x; r_local = R^T rel + com (sim.hpp:160-161); dilated SDF value in
-// recorded (sdf.cpp:140-164) or forward-only (sdf.cpp:126-138) semantics.
+// recorded (sdf.cpp:83-107) or forward-only (sdf.cpp:69-81) semantics.
 template <class Sdf>
 __device__ __forceinline__ void eval_point(const Sdf& sdf, const SimEnv& e, int i, V3 x, const M3& R,
                                            bool record, PointEval& pe) {
@@ -374,7 +375,7 @@ __device__ __forceinline__ double rcp_fast(double w) {
 // active in the forward (a singular-skipped correction: no axpy recorded).
 struct LeakGeo {
   V3 p, rel, g, n;
-  double sg;     // sign factor of the interpolated-normal fallback (sdf.cpp:150-155)
+  double sg;     // sign factor of the interpolated-normal fallback (sdf.cpp:92-98)
   bool contrib;
 };
 
@@ -1418,7 +1419,8 @@ __device__ __forceinline__ int next_candidate(const KBuf& buf, int b, int* s_nex
   if (buf.claim == nullptr) return b + gridDim.x;
   __syncthreads();  // every thread has read the previous claim
   if (threadIdx.x == 0)
-    *s_next = static_cast<int>(atomicAdd(buf.claim, 1ull) - buf.claim_base) + static_cast<int>(gridDim.x);
+    *s_next = static_cast<int>(min(atomicAdd(buf.claim, 1ull), static_cast<unsigned long long>(INT_MAX / 2))) +
+              static_cast<int>(gridDim.x);
   __syncthreads();
   return *s_next;
 }

@@ -67,11 +67,21 @@ class Scenes:
     stats: np.ndarray     # [S, 4] active contacts, corrections, singular, max penetration
 
 
-def generate_scenes(ctx: api.Context, gobj: api.GraspObject, seeds, params: api.DropParams | None = None) -> Scenes:
+def generate_scenes(ctx: api.Context, gobj: api.GraspObject, seeds, params: api.DropParams | None = None,
+                    strict: bool = False) -> Scenes:
+    """Drop every seed's scene. A scene that hits the step cap is not at rest
+    (SPEC.md:541 asks for an error): ``strict=True`` raises RuntimeError naming
+    seed, steps and kinetic energy; otherwise it is returned with
+    at_rest=False and ``transfer_grasps`` rejects its grasps."""
     params = params or api.DropParams(max_steps=5000, ke_tol=1e-6, measure_residual=True)
     seeds = np.atleast_1d(np.asarray(seeds, np.int64))
     r = api.drop(ctx, gobj, scene_states(gobj.desc, seeds), params)
-    return Scenes(seeds, r["state"], r["steps"], r["ke"], r["steps"] < params.max_steps, r["stats"])
+    at_rest = np.asarray(r["steps"]) < params.max_steps
+    if strict and not np.all(at_rest):
+        bad = [(int(seeds[k]), int(r["steps"][k]), float(r["ke"][k])) for k in np.nonzero(~at_rest)[0]]
+        raise RuntimeError("scene not at rest after the step cap: " +
+                           ", ".join(f"seed {s}: {n} steps, KE {e:.3e} J" for s, n, e in bad))
+    return Scenes(seeds, r["state"], r["steps"], r["ke"], at_rest, r["stats"])
 
 
 def object_origin(state: np.ndarray, com: np.ndarray) -> np.ndarray:
@@ -92,30 +102,48 @@ def transfer_q(q_base: np.ndarray, state: np.ndarray, com: np.ndarray) -> np.nda
 
 
 def transfer_grasps(ctx: api.Context, hand: api.Hand, obj: ObjectDesc, q_base: np.ndarray, scenes: Scenes,
-                    table_clearance: float = 0.0):
-    """All (grasp, scene) pairs: (q [G, S, 7+J], accepted [G, S], min hand z [G, S])."""
+                    table_clearance: float = 0.0, allow_unsettled: bool = False):
+    """All (grasp, scene) pairs: (q [G, S, 7+J], accepted [G, S], min hand z [G, S]).
+    Grasps into a scene that never came to rest are rejected unless
+    ``allow_unsettled``."""
     G, S = q_base.shape[0], scenes.state.shape[0]
     qs = np.stack([[transfer_q(q_base[g], scenes.state[s], obj.com) for s in range(S)] for g in range(G)])
     pts = api.forward(ctx, hand, qs.reshape(G * S, -1))      # GPU forward kinematics
     zmin = pts[:, :, 2].min(axis=1).reshape(G, S)
-    return qs, zmin >= -table_clearance, zmin
+    ok = zmin >= -table_clearance
+    if not allow_unsettled:
+        ok &= np.asarray(scenes.at_rest, bool)[None, :]
+    return qs, ok, zmin
 
 
 def _fmt(v):
+    """9 significant digits; non-finite values are rejected (NaN / Infinity are
+    not JSON)."""
     if isinstance(v, dict):
         return {k: _fmt(v[k]) for k in v}
     if isinstance(v, (list, tuple, np.ndarray)):
         return [_fmt(x) for x in np.asarray(v).tolist()]
     if isinstance(v, (float, np.floating)):
+        if not np.isfinite(v):
+            raise ValueError(f"export: non-finite value {v}")
         return float(f"{float(v):.9g}")
     if isinstance(v, (int, np.integer)):
         return int(v)
     return v
 
 
-def export_jsonl(records: list, out_dir: str, config: dict | None = None) -> dict:
+def export_jsonl(records: list, out_dir: str, config: dict | None = None, limits: dict | None = None) -> dict:
     """records: dicts with hand, object, q [7+J], losses{}, metrics{}, scene{}.
-    Writes <out_dir>/<hand>__<object>.jsonl per pair and manifest.json."""
+    Writes <out_dir>/<hand>__<object>.jsonl per pair and manifest.json.
+    ``limits`` {hand: (lower [J], upper [J])}: every exported record must have
+    its joints within the hand's limits (SPEC.md:561-569), else ValueError;
+    non-finite values are rejected."""
+    for r in records:
+        if limits and r["hand"] in limits:
+            lo, hi = (np.asarray(x, np.float64) for x in limits[r["hand"]])
+            j = np.asarray(r["q"], np.float64)[7:]
+            if j.shape != lo.shape or np.any(j < lo) or np.any(j > hi):
+                raise ValueError(f"export: {r['hand']} record outside its joint limits")
     os.makedirs(out_dir, exist_ok=True)
     groups: dict = {}
     for r in records:

@@ -5,11 +5,15 @@ Bars:
     evaluate_losses, SolveStats (contact culling / indexing) — BIT-EXACT
     against the parity-mode oracle (libdgref_sm: the reference with the
     kernels' deterministic sin/cos/atan2);
-  * gradients (per perturbation, per point, total) within rel 1e-9 of the
-    reference tape (the tape sums adjoints in node order; the kernel in closed
-    form, so ~1e-13 is expected);
+  * gradients (per perturbation, per point, total) within rel GRAD_RTOL = 1e-8
+    of the reference tape. The tape sums adjoints in node order, the kernel in
+    closed form, so results differ by rounding amplified along correction
+    chains: typically ~1e-13, and over the 43k-sim random fuzz
+    (profiles/r01/parity_fuzz.jsonl) the worst case was 3.2e-9 at |grad| ~
+    1e17-1e22. The bar is set above that distribution (not tuned to the chosen
+    inputs) and is still 4 orders inside north_star's rel 1e-4;
   * one optimizer step from the oracle's iterate (teacher forcing): losses
-    bit-exact, q_{k+1} within rel 1e-9 (north_star: FP32-level rel 1e-4);
+    bit-exact, q_{k+1} within GRAD_RTOL (north_star: FP32-level rel 1e-4);
   * against the UNMODIFIED reference (glibc libm): losses within rel 1e-6.
 """
 import os
@@ -19,7 +23,7 @@ import pytest
 
 pytestmark = pytest.mark.gpu
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
-GRAD_RTOL = 1e-9
+GRAD_RTOL = 1e-8  # see the module docstring: fuzz worst case 3.2e-9
 
 
 def relerr(a, b):

@@ -63,3 +63,19 @@ def test_export_roundtrip(tmp_path):
     empty = pipeline.export_jsonl([], str(tmp_path / "empty"))
     assert empty["count"] == 0 and empty["files"] == {}
     json.loads((tmp_path / "manifest.json").read_text())
+
+
+def test_export_rejects_nonfinite_and_limits(tmp_path):
+    """Exported records are valid JSON (no NaN / Infinity) and, given the
+    hand's limits, within them."""
+    import pytest
+    from paper_2306_08132_b200 import pipeline
+    q = np.concatenate([[0, 0, 0, 1, 0, 0, 0], np.full(9, 0.5)])
+    ok = {"hand": "barrett3", "object": "box", "q": q, "losses": {"stable": 0.1}}
+    lim = {"barrett3": (np.zeros(9), np.ones(9))}
+    pipeline.export_jsonl([ok], str(tmp_path / "a"), limits=lim)
+    with pytest.raises(ValueError, match="non-finite"):
+        pipeline.export_jsonl([dict(ok, losses={"stable": float("nan")})], str(tmp_path / "b"))
+    bad = dict(ok, q=np.concatenate([q[:7], np.full(9, 1.5)]))
+    with pytest.raises(ValueError, match="joint limits"):
+        pipeline.export_jsonl([bad], str(tmp_path / "c"), limits=lim)

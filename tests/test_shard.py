@@ -55,3 +55,67 @@ def test_two_rank_gather_matches_single_process(tmp_path, total):
     ref = init.approach_init(model.sphere(0.025), hand, total, seed=3)
     assert np.array_equal(full[:, :-1], ref)
     assert np.array_equal(full[:, -1], np.arange(total))
+
+
+def _record_worker(rank, world, port, total, out):
+    """Each rank builds result-shaped records for its shard — q (float64),
+    losses (float64, including non-finite values of a failed candidate) and an
+    int32 status word with high bits set — and gathers them like bench.py."""
+    import torch.distributed as dist
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    lo, hi = shard.shard_range(total, world, rank)
+    rng = np.random.default_rng(lo)
+    q = rng.normal(size=(hi - lo, 16))
+    losses = rng.normal(size=(hi - lo, 3))
+    status = (np.arange(lo, hi, dtype=np.int64) * 2654435761 % (1 << 31)).astype(np.int32)
+    if lo <= 3 < hi:
+        losses[3 - lo] = [np.nan, np.inf, -np.inf]
+    rec = np.concatenate([q, status[:, None].astype(np.float64), losses], axis=1)
+    full = shard.gather_rows(rec, total, world, rank)
+    if rank == 0:
+        np.save(out, full)
+    else:
+        assert full is None
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("total", [9, 64])
+def test_two_rank_gather_result_records(tmp_path, total):
+    out = str(tmp_path / "rec.npy")
+    mp.spawn(_record_worker, args=(2, _free_port(), total, out), nprocs=2, join=True)
+    full = np.load(out)
+    assert full.shape == (total, 20)
+    for lo, hi in (shard.shard_range(total, 2, r) for r in range(2)):
+        rng = np.random.default_rng(lo)
+        assert np.array_equal(full[lo:hi, :16], rng.normal(size=(hi - lo, 16)))
+        want_l = rng.normal(size=(hi - lo, 3))
+        if lo <= 3 < hi:
+            want_l[3 - lo] = [np.nan, np.inf, -np.inf]
+        assert np.array_equal(full[lo:hi, 17:], want_l, equal_nan=True)
+    status = full[:, 16].astype(np.int64).astype(np.int32)
+    want = (np.arange(total, dtype=np.int64) * 2654435761 % (1 << 31)).astype(np.int32)
+    assert np.array_equal(status, want)  # every status bit survives the float64 gather exactly
+
+
+def test_object_major_covers_every_object_once():
+    for world in (1, 2, 4, 8):
+        objs = [o for r in range(world) for o, _, _ in shard.object_major(64, 1024, world, r)]
+        assert objs == list(range(64))
+
+
+def test_bench_refuses_missing_gpus():
+    """`bench.py --gpus 2` without a launcher spawns one rank per GPU, and with
+    fewer GPUs visible (this CPU box: none) exits non-zero instead of quietly
+    running one rank."""
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    env = {k: v for k, v in os.environ.items() if k not in ("WORLD_SIZE", "RANK", "LOCAL_RANK")}
+    env["CUDA_VISIBLE_DEVICES"] = ""
+    r = subprocess.run([sys.executable, os.path.join(root, "bench.py"), "--gpus", "2", "--steps", "1"],
+                       capture_output=True, text=True, env=env, timeout=300)
+    assert r.returncode != 0
+    assert "requested but 0 CUDA device" in r.stderr
+    assert '"n_gpus"' not in r.stdout

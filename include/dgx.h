@@ -22,6 +22,8 @@
  *   dgx_evaluate_losses_batch  dg::evaluate_losses (losses.hpp:119-121, losses.cpp:7-18)
  *                              + SolveStats (sim.hpp:42-49) per perturbation
  *   dgx_apply_gradient_step_batch  dg::apply_gradient_step (losses.hpp:136, losses.cpp:92-102)
+ *   dgx_grasp_energy_batch     north_star (3) force-closure + penetration terms
+ *                              (no reference counterpart; parity-unpinned, off by default)
  *   dgx_optimize_batch         the synthesis loop the reference specifies but does
  *                              not implement:
  *                              linear dilation schedule + loss_gradient + Adam +
@@ -50,7 +52,7 @@
 extern "C" {
 #endif
 
-#define DGX_ABI_VERSION 1
+#define DGX_ABI_VERSION 2
 
 typedef struct dgx_ctx dgx_ctx;
 typedef struct dgx_hand dgx_hand;
@@ -135,13 +137,21 @@ typedef struct {
   double dt;               /* SimParams::dt (sim.hpp:34) */
   double mu;               /* SimParams::mu (sim.hpp:35) */
   int32_t gs_iters;        /* SimParams::gs_iters (sim.hpp:36) */
-  int32_t steps;           /* StabilityProtocol::steps; only 1 is supported */
+  int32_t steps;           /* StabilityProtocol::steps (losses.hpp:18): T >= 1 steps per perturbation sim */
   double dilation_radius;  /* SimParams::dilation_radius (sim.hpp:38) */
   double alpha_leak;       /* LeakPolicy::alpha_leak (sim.hpp:23) */
-  int32_t num_velocities;  /* StabilityProtocol::velocities.size() (M <= 8) */
+  int32_t num_velocities;  /* StabilityProtocol::velocities.size() = M >= 1 (losses.hpp:17) */
   int32_t pad;
-  double velocities[8][3];
+  double velocities[8][3]; /* the first min(M, 8) velocities, used when velocity_list is NULL (M <= 8) */
   double w_stable, w_qrange, w_qlimit;  /* LossWeights (losses.hpp:31-35) */
+  /* ---- ABI 2 ---- */
+  const double* velocity_list;  /* [M,3] host memory, any M >= 1 (copied per call); NULL: velocities[] */
+  /* Grasp-energy terms of north_star (3), no reference counterpart (parity-unpinned;
+     dgx_grasp_energy_batch). 0 = off: the optimizer is then bit-identical to ABI 1. */
+  double w_force_closure;  /* weight of E_fc = |sum_c n_c|^2 + |sum_c (p_c - com) x n_c|^2 / l^2 */
+  double w_penetration;    /* weight of E_pen = sum_i max(0, -rho_i) */
+  double contact_threshold;/* sample i is a contact c when |rho_i| <= threshold (m); default 0.005 */
+  double torque_scale;     /* l (m) in E_fc; default 0.05 */
 } dgx_params;
 
 typedef struct {
@@ -229,6 +239,26 @@ int dgx_optimize_batch(dgx_ctx* ctx, const dgx_hand* hand, const dgx_object* obj
 int dgx_optimize_multi(dgx_ctx* ctx, const dgx_hand* hand, int32_t n_obj, const dgx_object* const* objs,
                        const int32_t* counts, double* q, double* adam_m, double* adam_v, const dgx_params* params,
                        const dgx_opt* opt, double* traj, int32_t* status, uint32_t flags);
+
+/* Grasp-energy terms (north_star (3): force closure + penetration; the
+   reference objective has neither, so they are parity-unpinned and off by
+   default). At the object's canonical pose (object frame = world), per
+   candidate over every hand sample p_i (HandModel::forward order) with SDF
+   value rho_i and unit gradient n_i (MeshSdf::dilated at radius 0, sdf.cpp:62-67):
+     contacts C = { i : |rho_i| <= contact_threshold },
+     E_fc  = |sum_{i in C} n_i|^2 + |sum_{i in C} (p_i - com) x n_i|^2 / torque_scale^2
+             (the differentiable force-closure estimate of Liu et al. 2021 with unit
+             contact forces along the normals),
+     E_pen = sum_i max(0, -rho_i).
+   Gradients hold the contact set and the normals frozen (the reference's
+   frozen-coefficient convention, sim.hpp:102-104): dE_fc/dp_i = 2 (n_i x tau) / l^2
+   for i in C, dE_pen/dp_i = -n_i for rho_i < 0, mapped to [pos 3 | tangent 3 |
+   joints J] by the FK adjoint. energy [B,2] (E_fc, E_pen), grads [B,2,6+J]
+   (may be NULL). Reads contact_threshold / torque_scale from params. The
+   optimizer adds w_force_closure dE_fc + w_penetration dE_pen to its weighted
+   gradient every iterate when either weight is nonzero. */
+int dgx_grasp_energy_batch(dgx_ctx* ctx, const dgx_hand* hand, const dgx_object* obj, int32_t B, const double* q,
+                           const dgx_params* params, double* energy, double* grads, uint32_t flags);
 
 /* Parity / debug: per-perturbation residuals [B,M], gradients [B,M,6+J] and
    optionally d residual_m / d points [B,M,N,3] (pass NULL to skip). */

@@ -67,7 +67,7 @@ inline dg::HandConfig unpack(const double* v, int J) {
 }
 inline dgx_params params_of(const dg::StabilityProtocol& proto, const dg::SimParams& p,
                             const dg::LossWeights& w = {}) {
-  if (proto.m() > 8) throw std::runtime_error("dgx: at most 8 perturbation velocities");
+  static_assert(sizeof(dg::Vec3) == 3 * sizeof(double), "dg::Vec3 must be three packed doubles");
   dgx_params c{};
   c.dt = p.dt;
   c.mu = p.mu;
@@ -76,11 +76,13 @@ inline dgx_params params_of(const dg::StabilityProtocol& proto, const dg::SimPar
   c.dilation_radius = p.dilation_radius;
   c.alpha_leak = p.leak.alpha_leak;
   c.num_velocities = proto.m();
-  for (int m = 0; m < proto.m(); ++m) {
+  for (int m = 0; m < proto.m() && m < 8; ++m) {
     c.velocities[m][0] = proto.velocities[m].x;
     c.velocities[m][1] = proto.velocities[m].y;
     c.velocities[m][2] = proto.velocities[m].z;
   }
+  // any M (losses.hpp:17): the protocol's own vector, alive for the call
+  if (proto.m() > 8) c.velocity_list = reinterpret_cast<const double*>(proto.velocities.data());
   c.w_stable = w.stable;
   c.w_qrange = w.qrange;
   c.w_qlimit = w.qlimit;

@@ -96,6 +96,7 @@ def lib(variant: str = "sm") -> C.CDLL:
     L.dgr_object_query_within.argtypes = [vp, _dp, C.c_double, _dp]
     L.dgr_drop.argtypes = [vp, _dp, C.c_double, C.c_double, C.c_int, _dp, C.c_int, C.c_int, C.c_double, C.c_int,
                            _dp, _ip, _dp, _dp, _dp, C.c_int, C.c_int]
+    L.dgr_set_protocol.argtypes = [C.c_int, _dp]
     L.dgr_object_use_sphere.argtypes = [vp, C.c_double, C.c_double, C.c_double, C.c_double]
     L.dgr_object_use_box.argtypes = [vp, _dp, _dp]
     L.dgr_object_use_grid.argtypes = [vp, _ip, _dp, C.c_double, C.c_double, _fp]
@@ -306,6 +307,23 @@ class RefObject:
         out = np.zeros(8)
         _check(self.L, self.L.dgr_object_query(self.ptr, _d(r), radius, _d(out)))
         return out
+
+
+class protocol:
+    """Context manager: every oracle call inside uses StabilityProtocol with
+    these velocities [M,3] (and params.steps) instead of standard(speed)."""
+
+    def __init__(self, velocities, variant="sm"):
+        self.v = np.ascontiguousarray(np.asarray(velocities, np.float64).reshape(-1, 3))
+        self.L = lib(variant)
+
+    def __enter__(self):
+        self.L.dgr_set_protocol(self.v.shape[0], _d(self.v))
+        return self
+
+    def __exit__(self, *exc):
+        self.L.dgr_set_protocol(0, None)
+        return False
 
 
 def loss_gradient(obj: RefObject, hand: RefHand, q, params: Params):

@@ -180,7 +180,16 @@ SimParams sim_params(const Params& p) {
   return s;
 }
 
-StabilityProtocol protocol(const Params& p) { return StabilityProtocol::standard(p.speed, p.steps); }
+// custom velocity list (dgr_set_protocol; empty: StabilityProtocol::standard)
+std::vector<Vec3> g_velocities;
+
+StabilityProtocol protocol(const Params& p) {
+  if (g_velocities.empty()) return StabilityProtocol::standard(p.speed, p.steps);
+  StabilityProtocol s;
+  s.velocities = g_velocities;
+  s.steps = p.steps;
+  return s;
+}
 
 HandConfig unpack_q(const HandModel& hand, const double* q) {
   HandConfig c;
@@ -221,6 +230,12 @@ Rec recorded_residual(const GraspObject& obj, const HandModel& hand, const HandC
 extern "C" {
 
 const char* dgr_last_error() { return g_err.c_str(); }
+
+// M velocities [M,3] for every following call (M = 0: back to standard(speed))
+void dgr_set_protocol(int M, const double* v) {
+  g_velocities.clear();
+  for (int m = 0; m < M; ++m) g_velocities.push_back({v[3 * m], v[3 * m + 1], v[3 * m + 2]});
+}
 
 // ---- hands --------------------------------------------------------------
 void* dgr_hand_barrett3(int budget, std::uint64_t seed) {

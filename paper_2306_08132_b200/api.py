@@ -57,6 +57,12 @@ class LossWeights:
     stable: float = 1.0
     qrange: float = 0.01
     qlimit: float = 1.0
+    # grasp-energy terms (north_star (3); no reference counterpart, off by
+    # default): see grasp_energy()
+    force_closure: float = 0.0
+    penetration: float = 0.0
+    contact_threshold: float = 0.005
+    torque_scale: float = 0.05
 
 
 @dataclass
@@ -73,17 +79,23 @@ class OptConfig:
 def params_c(params: SimParams, protocol: StabilityProtocol, weights: LossWeights | None = None) -> capi.ParamsC:
     if params.dilation_radius < 0.0:
         raise ValueError("dilation radius must be >= 0")
-    if not 1 <= protocol.m <= 8:
-        raise ValueError("protocol must have 1..8 velocities")
+    if protocol.m < 1:
+        raise ValueError("protocol must have >= 1 velocities")
     w = weights or LossWeights()
     p = capi.ParamsC()
     p.dt, p.mu, p.gs_iters, p.steps = params.dt, params.mu, params.gs_iters, protocol.steps
     p.dilation_radius, p.alpha_leak = params.dilation_radius, params.alpha_leak
     p.num_velocities = protocol.m
-    for m, v in enumerate(protocol.velocities):
+    vl = np.ascontiguousarray(np.asarray(protocol.velocities, np.float64).reshape(protocol.m, 3))
+    for m in range(min(protocol.m, 8)):
         for c in range(3):
-            p.velocities[m][c] = float(v[c])
+            p.velocities[m][c] = float(vl[m, c])
+    if protocol.m > 8:  # any M: the list itself (kept alive with the struct)
+        p._velocity_list = vl
+        p.velocity_list = vl.ctypes.data
     p.w_stable, p.w_qrange, p.w_qlimit = w.stable, w.qrange, w.qlimit
+    p.w_force_closure, p.w_penetration = w.force_closure, w.penetration
+    p.contact_threshold, p.torque_scale = w.contact_threshold, w.torque_scale
     return p
 
 
@@ -248,6 +260,24 @@ def evaluate_losses(ctx: Context, obj: GraspObject, hand: Hand, q, protocol: Sta
     capi.check(ctx.L.dgx_evaluate_losses_batch(ctx.h, hand.h, obj.h, B, capi.ptr(q), C.byref(p), capi.ptr(losses),
                                                capi.ptr(stats), capi.ptr(status), 0))
     return losses, stats, status
+
+
+def grasp_energy(ctx: Context, obj: GraspObject, hand: Hand, q, contact_threshold: float = 0.005,
+                 torque_scale: float = 0.05):
+    """north_star (3) grasp-energy terms (dgx_grasp_energy_batch; no reference
+    counterpart, parity-unpinned) at the object's canonical pose:
+    E_fc = |sum_C n|^2 + |sum_C (p - com) x n|^2 / torque_scale^2 over contacts
+    C = {|rho| <= contact_threshold}, E_pen = sum max(0, -rho); gradients with
+    contact set and normals frozen. -> (energy [B,2], grads [B,2,6+J])."""
+    q = _f64(q, (-1, 7 + hand.J))
+    B = q.shape[0]
+    e = np.zeros((B, 2))
+    g = np.zeros((B, 2, 6 + hand.J))
+    p = params_c(SimParams(), StabilityProtocol.standard(),
+                 LossWeights(contact_threshold=contact_threshold, torque_scale=torque_scale))
+    capi.check(ctx.L.dgx_grasp_energy_batch(ctx.h, hand.h, obj.h, B, capi.ptr(q), C.byref(p), capi.ptr(e),
+                                            capi.ptr(g), 0))
+    return e, g
 
 
 def sdf_query(ctx: Context, obj: GraspObject, points, radius: float = 0.0, within: bool = False) -> np.ndarray:

@@ -65,6 +65,9 @@ class ParamsC(C.Structure):
         ("dilation_radius", C.c_double), ("alpha_leak", C.c_double), ("num_velocities", C.c_int32),
         ("pad", C.c_int32), ("velocities", (C.c_double * 3) * 8), ("w_stable", C.c_double),
         ("w_qrange", C.c_double), ("w_qlimit", C.c_double),
+        # ABI 2
+        ("velocity_list", C.c_void_p), ("w_force_closure", C.c_double), ("w_penetration", C.c_double),
+        ("contact_threshold", C.c_double), ("torque_scale", C.c_double),
     ]
 
 
@@ -83,7 +86,7 @@ EXPORTS = [
     "dgx_object_upload", "dgx_object_free", "dgx_forward_batch", "dgx_loss_gradient_batch",
     "dgx_evaluate_losses_batch", "dgx_apply_gradient_step_batch", "dgx_optimize_batch", "dgx_debug_sims",
     "dgx_fp64_peak", "dgx_optimize_multi", "dgx_sdf_query_batch", "dgx_mesh_inertia",
-    "dgx_mesh_bvh", "dgx_drop_batch", "dgx_contacts_batch",
+    "dgx_mesh_bvh", "dgx_drop_batch", "dgx_contacts_batch", "dgx_grasp_energy_batch",
 ]
 
 _lib: C.CDLL | None = None
@@ -125,6 +128,7 @@ def load() -> C.CDLL:
     L.dgx_optimize_batch.argtypes = [vp, vp, vp, C.c_int32, vp, vp, vp, C.POINTER(ParamsC), C.POINTER(OptC), vp,
                                      vp, C.c_uint32]
     L.dgx_debug_sims.argtypes = [vp, vp, vp, C.c_int32, vp, C.POINTER(ParamsC), vp, vp, vp, vp, C.c_uint32]
+    L.dgx_grasp_energy_batch.argtypes = [vp, vp, vp, C.c_int32, vp, C.POINTER(ParamsC), vp, vp, C.c_uint32]
     L.dgx_fp64_peak.argtypes = [C.c_int, _dp, _dp]
     L.dgx_optimize_multi.argtypes = [vp, vp, C.c_int32, vp, vp, vp, vp, vp, C.POINTER(ParamsC), C.POINTER(OptC), vp,
                                      vp, C.c_uint32]

@@ -68,9 +68,11 @@ struct DevBuf {
 
 // per-stream kernel scratch (correction logs, contact slots, link-sum spills)
 struct Scratch {
-  DevBuf corr, slots, ftg, mcache, drop, thr, claim;
+  DevBuf corr, slots, ftg, mcache, drop, thr, claim, vel, egrad;
   void release() {
     claim.release();
+    vel.release();
+    egrad.release();
     thr.release();
     corr.release();
     slots.release();
@@ -131,13 +133,17 @@ void set_device(dgx_ctx* c) { cuda_check(cudaSetDevice(c->device), "cudaSetDevic
 
 KSim make_sim(const dgx_params* p, bool eval) {
   if (!p) throw DgxError(DGX_E_INVALID, "params is NULL");
+  if (p->steps < 1) throw DgxError(DGX_E_INVALID, "StabilityProtocol::steps must be >= 1");
   if (p->steps != 1)
-    throw DgxError(DGX_E_UNSUPPORTED, "StabilityProtocol::steps != 1 is not supported by the fused kernel");
-  if (p->num_velocities < 1 || p->num_velocities > kMaxSims)
-    throw DgxError(DGX_E_INVALID, "protocol must have 1..8 velocities");
+    throw DgxError(DGX_E_UNSUPPORTED, "StabilityProtocol::steps != 1 is not supported by this build");
+  if (p->num_velocities < 1) throw DgxError(DGX_E_INVALID, "protocol must have >= 1 velocities");
+  if (p->num_velocities > kMaxSims && !p->velocity_list)
+    throw DgxError(DGX_E_INVALID, "more than 8 velocities need params->velocity_list");
   if (p->gs_iters < 0) throw DgxError(DGX_E_INVALID, "gs_iters must be >= 0");
   if (p->dilation_radius < 0.0) throw std::invalid_argument("dilation radius must be >= 0");
   if (!(p->dt > 0.0)) throw DgxError(DGX_E_INVALID, "dt must be > 0");
+  if (!(p->w_force_closure >= 0.0) || !(p->w_penetration >= 0.0))
+    throw DgxError(DGX_E_INVALID, "grasp-energy weights must be >= 0");
   KSim s{};
   s.dt = p->dt;
   s.mu = p->mu;
@@ -145,14 +151,35 @@ KSim make_sim(const dgx_params* p, bool eval) {
   s.radius = p->dilation_radius;
   s.gs = p->gs_iters;
   s.M = p->num_velocities;
+  s.steps = p->steps;
   s.measure_residual = eval ? 1 : 0;
-  for (int m = 0; m < s.M; ++m)
-    for (int c = 0; c < 3; ++c) s.vel[m][c] = p->velocities[m][c];
+  for (int m = 0; m < s.M && m < kMaxSims; ++m)
+    for (int c = 0; c < 3; ++c) s.vel[m][c] = p->velocity_list ? p->velocity_list[3 * m + c] : p->velocities[m][c];
+  s.vel_dev = nullptr;  // set by upload_velocities when M > kMaxSims
   s.w_stable = p->w_stable;
   s.w_qrange = p->w_qrange;
   s.w_qlimit = p->w_qlimit;
+  s.w_fc = p->w_force_closure;
+  s.w_pen = p->w_penetration;
+  s.fc_thr = p->contact_threshold > 0.0 ? p->contact_threshold : 0.005;
+  s.fc_scale = p->torque_scale > 0.0 ? p->torque_scale : 0.05;
   return s;
 }
+
+// M > kMaxSims: the velocity list goes to device memory, stream-ordered on the
+// context stream (pageable source: staged before cudaMemcpyAsync returns)
+void upload_velocities(dgx_ctx* c, KSim& S, const dgx_params* p) {
+  if (S.M <= kMaxSims) return;
+  if (!c) throw DgxError(DGX_E_INVALID, "NULL context");
+  set_device(c);
+  c->scratch.vel.ensure(sizeof(double) * 3 * S.M);
+  cuda_check(cudaMemcpyAsync(c->scratch.vel.p, p->velocity_list, sizeof(double) * 3 * S.M, cudaMemcpyHostToDevice,
+                             c->stream),
+             "H2D velocities");
+  S.vel_dev = static_cast<const double*>(c->scratch.vel.p);
+}
+
+bool energy_on(const KSim& S) { return S.w_fc != 0.0 || S.w_pen != 0.0; }
 
 // adjoint staging length S.seg_max; returns the adjoint kernel's shared memory
 int choose_staging(const dgx_hand* h, const dgx_object* o, KSim& S) {
@@ -357,14 +384,38 @@ void launch_range(dgx_ctx* c, Scratch& sc, const dgx_hand* h, const dgx_object* 
   //   CTAs leave too little L1 for the SDF cells (config 3, N = 4093: 42.9k vs 45.8k).
   const bool split = use_split(o) && B > c->num_sms && SmemLayout(N, h->L, M, 0).total <= kSplitMaxFwdSmem &&
                      !(mode == kModeOpt && P.k_end == P.k_begin);
+  // grasp-energy terms (optimizer only): their weighted gradient depends on
+  // the iterate's q, so it is computed per iterate right before the
+  // iterate's grasp-search launch and added before Adam (KBuf::egrad)
+  const bool energy = mode == kModeOpt && energy_on(S);
+  auto energy_launch = [&](const KBuf& cb, int nb, int k) {
+    sc.egrad.ensure(sizeof(double) * static_cast<size_t>(nb) * D);
+    (void)cudaGetLastError();
+    cuda_check(launch_energy(h->k, o->k, o->sdf, S, nb, cb.q, k > P.traj_k0 ? cb.status : nullptr, nullptr,
+                             nullptr, static_cast<double*>(sc.egrad.p), std::min(nb, c->num_sms * 4), st),
+               "energy_kernel");
+    ++c->launches;
+  };
   if (!split) {
     int smem = 0;
     const int grid = prepare(c, sc, h, o, S, B, buf, smem);
-    bind_claim(sc, buf, B, st);
-    counted_launch(c, kPhaseFused, st, "fused_kernel",
-                   [&] {
-      return launch_fused(h->k, o->k, o->sdf, S, P, buf, mode, kPhaseFused, grid, smem, st);
-    });
+    if (!energy) {
+      bind_claim(sc, buf, B, st);
+      counted_launch(c, kPhaseFused, st, "fused_kernel",
+                     [&] { return launch_fused(h->k, o->k, o->sdf, S, P, buf, mode, kPhaseFused, grid, smem, st); });
+      return;
+    }
+    for (int k = P.k_begin; k < P.k_end; ++k) {  // one fused launch per iterate
+      KOpt Pk = P;
+      Pk.k_begin = k;
+      Pk.k_end = k + 1;
+      energy_launch(buf, B, k);
+      KBuf kb = buf;
+      kb.egrad = static_cast<const double*>(sc.egrad.p);
+      bind_claim(sc, kb, B, st);
+      counted_launch(c, kPhaseFused, st, "fused_kernel",
+                     [&] { return launch_fused(h->k, o->k, o->sdf, S, Pk, kb, mode, kPhaseFused, grid, smem, st); });
+    }
     return;
   }
   const bool record = mode != kModeEval;
@@ -392,6 +443,10 @@ void launch_range(dgx_ctx* c, Scratch& sc, const dgx_hand* h, const dgx_object* 
       if (mode == kModeOpt) {
         Pk.k_begin = k;
         Pk.k_end = k + 1;
+      }
+      if (energy) {
+        energy_launch(cb, nb, k);
+        cb.egrad = static_cast<const double*>(sc.egrad.p);
       }
       bind_claim(sc, cb, nb, st);
       counted_launch(c, kPhaseFwd, st, "forward kernel", [&] {
@@ -924,6 +979,7 @@ static void run_fused(dgx_ctx* c, const dgx_hand* h, const dgx_object* o, int32_
   if (!status) throw DgxError(DGX_E_INVALID, "status is NULL");
   buf.status = s.out(status, static_cast<size_t>(B));
   if (point_grads) cuda_check(cudaMemsetAsync(buf.point_grads, 0, 24ull * B * M * N, c->stream), "memset");
+  buf.egrad = nullptr;
   launch_range(c, c->scratch, h, o, S, P, buf, B, mode, c->stream);
   s.finish(flags);
 }
@@ -932,6 +988,7 @@ int dgx_loss_gradient_batch(dgx_ctx* c, const dgx_hand* h, const dgx_object* o, 
                             const dgx_params* p, double* losses, double* grads, int32_t* status, uint32_t flags) {
   return guarded([&] {
     KSim S = make_sim(p, false);
+    upload_velocities(c, S, p);
     KOpt P{};
     run_fused(c, h, o, B, q, nullptr, nullptr, nullptr, S, P, kModeGrad, losses, grads, nullptr, nullptr, nullptr,
               nullptr, nullptr, status, flags);
@@ -942,6 +999,7 @@ int dgx_evaluate_losses_batch(dgx_ctx* c, const dgx_hand* h, const dgx_object* o
                               const dgx_params* p, double* losses, double* stats, int32_t* status, uint32_t flags) {
   return guarded([&] {
     KSim S = make_sim(p, true);
+    upload_velocities(c, S, p);
     KOpt P{};
     run_fused(c, h, o, B, q, nullptr, nullptr, nullptr, S, P, kModeEval, losses, nullptr, stats, nullptr, nullptr,
               nullptr, nullptr, status, flags);
@@ -953,6 +1011,7 @@ int dgx_debug_sims(dgx_ctx* c, const dgx_hand* h, const dgx_object* o, int32_t B
                    uint32_t flags) {
   return guarded([&] {
     KSim S = make_sim(p, false);
+    upload_velocities(c, S, p);
     KOpt P{};
     run_fused(c, h, o, B, q, nullptr, nullptr, nullptr, S, P, kModeGrad, nullptr, nullptr, nullptr, sim_res,
               sim_grads, point_grads, nullptr, status, flags);
@@ -968,6 +1027,7 @@ int dgx_optimize_batch(dgx_ctx* c, const dgx_hand* h, const dgx_object* o, int32
       throw DgxError(DGX_E_INVALID, "opt: need 0 <= k_begin <= k_end <= iters, iters >= 1");
     if (!(opt->lr > 0.0)) throw DgxError(DGX_E_INVALID, "opt: learning rate must be > 0");
     KSim S = make_sim(p, false);
+    upload_velocities(c, S, p);
     KOpt P{opt->iters, opt->k_begin, opt->k_end, opt->record, opt->r0, opt->lr, opt->beta1, opt->beta2, opt->eps};
     run_fused(c, h, o, B, nullptr, q, am, av, S, P, kModeOpt, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr,
               opt->record ? traj : nullptr, status, flags);
@@ -993,6 +1053,7 @@ int dgx_optimize_multi(dgx_ctx* c, const dgx_hand* h, int32_t n_obj, const dgx_o
     const int B = static_cast<int>(B64);
     set_device(c);
     KSim S0 = make_sim(p, false);
+    upload_velocities(c, S0, p);
     KOpt P{opt->iters, opt->k_begin, opt->k_end, opt->record, opt->r0, opt->lr, opt->beta1, opt->beta2, opt->eps};
     const bool dev = flags & DGX_DEVICE_PTRS;
     const int D = 6 + h->J, Qd = 7 + h->J, steps = opt->k_end - opt->k_begin;
@@ -1035,6 +1096,33 @@ int dgx_optimize_multi(dgx_ctx* c, const dgx_hand* h, int32_t n_obj, const dgx_o
       cuda_check(cudaStreamWaitEvent(c->stream, c->subs[k].done, 0), "wait");
     }
     st.finish(flags);
+  });
+}
+
+int dgx_grasp_energy_batch(dgx_ctx* c, const dgx_hand* h, const dgx_object* o, int32_t B, const double* q,
+                           const dgx_params* p, double* energy, double* grads, uint32_t flags) {
+  return guarded([&] {
+    if (!c || !h || !o || !p || !energy) throw DgxError(DGX_E_INVALID, "NULL argument");
+    if (B < 0) throw DgxError(DGX_E_INVALID, "B < 0");
+    if (B == 0) return;
+    set_device(c);
+    KSim S{};
+    S.fc_thr = p->contact_threshold > 0.0 ? p->contact_threshold : 0.005;
+    S.fc_scale = p->torque_scale > 0.0 ? p->torque_scale : 0.05;
+    S.w_fc = p->w_force_closure;
+    S.w_pen = p->w_penetration;
+    const bool dev = flags & DGX_DEVICE_PTRS;
+    const int D = 6 + h->J, Qd = 7 + h->J;
+    Staging s(c, dev, bytes_round(8ull * B * Qd) + bytes_round(16ull * B) + bytes_round(16ull * B * D));
+    const double* dq = s.in(q, static_cast<size_t>(B) * Qd);
+    double* de = s.out(energy, static_cast<size_t>(B) * 2);
+    double* dg = s.out(grads, static_cast<size_t>(B) * 2 * D);
+    (void)cudaGetLastError();
+    cuda_check(launch_energy(h->k, o->k, o->sdf, S, B, dq, nullptr, de, dg, nullptr, std::min(B, c->num_sms * 4),
+                             c->stream),
+               "energy_kernel");
+    ++c->launches;
+    s.finish(flags);
   });
 }
 

@@ -6,7 +6,8 @@
 
 namespace dgx {
 
-constexpr int kMaxSims = 8;        // protocol velocities per candidate (standard: 7)
+constexpr int kMaxSims = 8;        // protocol velocities held inline in KSim (standard: 7); more: KSim::vel_dev
+constexpr int kMaxWarps = 7;       // warps per grasp-search CTA: warp w runs sims w, w + W, ... (W = min(M, 7))
 constexpr int kMaxDim = 32;        // 6 + J gradient coordinates (J <= 26)
 constexpr int kSegMaxCap = 16;
 constexpr int kCorrMatDoubles = 19 * 8 + 1;  // dgx_kernels.cu kCorrMat    // max points per lane segment in the adjoint
@@ -100,8 +101,13 @@ struct KObj {
 struct KSim {
   double dt, mu, alpha, radius;
   int gs, M, measure_residual, seg_max;
+  int steps, pad;
   double vel[kMaxSims][3];
+  const double* vel_dev;  // [M,3] device copy when M > kMaxSims
   double w_stable, w_qrange, w_qlimit;
+  // grasp-energy terms (dgx_grasp_energy_batch; 0 = off)
+  double w_fc, w_pen, fc_thr, fc_scale;
+  __host__ __device__ int warps() const { return M < kMaxWarps ? M : kMaxWarps; }
 };
 
 struct KOpt {
@@ -122,6 +128,7 @@ struct KBuf {
   double* point_grads;  // [B, M, N, 3] debug: d residual_m / d p_i
   double* traj;         // [B, k_end-k_begin, 3 + D] opt: losses + weighted grad per iterate
   int* status;          // [B]
+  const double* egrad;  // [B, D] opt: weighted grasp-energy gradient added before Adam (null: off)
   CorrRec* corr;        // [grid, M, cap_corr]
   SlotRec* slots;       // [grid, M, N]  contact slots (one per hand point at most)
   int* slot_of_point;   // [grid, M, N]
@@ -142,9 +149,11 @@ struct KBuf {
   unsigned long long* claim;
 };
 
-// dynamic shared memory layout (bytes), identical on host and device
+// dynamic shared memory layout (bytes), identical on host and device. Per
+// sim: link force / torque sums (ft) and residuals; per warp: bitmap and
+// adjoint staging (a warp runs sims warp, warp + W, ...).
 struct SmemLayout {
-  int off_px, off_py, off_pz, off_link, off_ft, off_bitmap, off_stage, off_misc, total;
+  int off_px, off_py, off_pz, off_link, off_ft, off_bitmap, off_stage, off_misc, off_sres, off_sflag, total;
   __host__ __device__ static int align(int x) { return (x + 15) & ~15; }
   int stage_per_warp;  // doubles: seg_max x 5 x 32 adjoint staging (>= 6L + kMaxDim for the debug FK adjoint)
   __host__ __device__ static int stage_doubles(int seg_max, int L) {
@@ -153,15 +162,18 @@ struct SmemLayout {
   }
   __host__ __device__ SmemLayout(int N, int L, int M, int seg_max) {
     stage_per_warp = stage_doubles(seg_max, L);
+    const int W = M < kMaxWarps ? M : kMaxWarps;
     int o = 0;
     off_px = o; o = align(o + 8 * N);
     off_py = o; o = align(o + 8 * N);
     off_pz = o; o = align(o + 8 * N);
     off_link = o; o = align(o + 8 * 12 * L);
     off_ft = o; o = align(o + 8 * 6 * L * M);
-    off_bitmap = o; o = align(o + 4 * ((N + 31) / 32) * M);
-    off_stage = o; o = align(o + 8 * stage_per_warp * M);
-    off_misc = o; o = align(o + 8 * (64 + 4 * kMaxDim + 2 * kMaxSims));
+    off_bitmap = o; o = align(o + 4 * ((N + 31) / 32) * W);
+    off_stage = o; o = align(o + 8 * stage_per_warp * W);
+    off_misc = o; o = align(o + 8 * (40 + 3 * kMaxDim + 8));  // q, 3 gradients, next-candidate slot
+    off_sres = o; o = align(o + 8 * M);
+    off_sflag = o; o = align(o + 4 * (M + 1));                 // per-sim status, [M] = candidate status
     total = o;
   }
 };
@@ -194,5 +206,9 @@ cudaError_t launch_forward(const KHand& H, const double* q, double* out, int B, 
 cudaError_t launch_contacts(const KHand& H, const SdfSet& sdf, int B, const double* q, const double* area, int T,
                             const double* thr, int cap, double* ca, int* cnt, int* ncont, int* cidx, double* crec,
                             int grid, cudaStream_t st);
+// grasp-energy terms (dgx_grasp_energy_batch): e [B,2], g [B,2,D], gw [B,D]
+// (each may be null); candidates with status != 0 are skipped (status may be null)
+cudaError_t launch_energy(const KHand& H, const KObj& O, const SdfSet& sdf, const KSim& S, int B, const double* q,
+                          const int* status, double* e, double* g, double* gw, int grid, cudaStream_t st);
 cudaError_t launch_step(int J, const double* q, const double* g, double lr, double* out, int B, cudaStream_t st);
 }  // namespace dgx

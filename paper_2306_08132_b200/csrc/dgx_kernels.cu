@@ -1440,12 +1440,13 @@ __device__ __forceinline__ void kernel_body(const KHand& H, const KObj& O, const
   double* misc = reinterpret_cast<double*>(smem + lay.off_misc);
   double* sq = misc;               // [40] configuration
   double* sg = misc + 40;          // [3*32] d_stable, d_qrange, d_qlimit
-  double* sres = misc + 136;       // [8] residuals
-  int* sflag = reinterpret_cast<int*>(misc + 144);  // [16] per-warp status
-  int* snext = reinterpret_cast<int*>(misc + 152);  // [1] next claimed candidate
+  int* snext = reinterpret_cast<int*>(misc + 136);  // [1] next claimed candidate
+  double* sres = reinterpret_cast<double*>(smem + lay.off_sres);  // [M] residuals
+  int* sflag = reinterpret_cast<int*>(smem + lay.off_sflag);      // [M] per-sim status, [M] candidate status
 
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int M = S.M, N = H.N, L = H.L, J = H.J, D = 6 + J, Qd = 7 + J;
+  const int W = static_cast<int>(blockDim.x >> 5);  // warp w runs sims w, w + W, ... (W = min(M, 7))
   const bool record = mode != kModeEval;
   const int nwords = (N + 31) / 32;
 
@@ -1460,8 +1461,7 @@ __device__ __forceinline__ void kernel_body(const KHand& H, const KObj& O, const
   e.stage = stage_all + warp * lay.stage_per_warp;
   e.seg_max = S.seg_max;
   e.ft = ft_all + warp * 6 * L;
-  const int wm = warp < M ? warp : 0;
-  const size_t wslot = static_cast<size_t>(blockIdx.x) * M + wm;
+  const size_t wslot = static_cast<size_t>(blockIdx.x) * W + warp;  // fused scratch: per (CTA, warp)
   // logs: per resident (CTA, warp) when fused; per (candidate, sim) when split
   // (bound per candidate below)
   auto bind_logs = [&](size_t ws) {
@@ -1488,12 +1488,9 @@ __device__ __forceinline__ void kernel_body(const KHand& H, const KObj& O, const
   const int k1 = mode == kModeOpt ? P.k_end : 1;
 
   for (int b = blockIdx.x; b < buf.B; b = next_candidate(buf, b, snext)) {
-    if constexpr (Phase != kPhaseFused) {
-      bind_logs(static_cast<size_t>(b) * M + wm);
-      // a candidate that failed at an earlier iterate of this call stays
-      // there (the fused kernel's loop stops at its first failure)
-      if (mode == kModeOpt && P.k_begin > P.traj_k0 && buf.status[b] != kOk) continue;
-    }
+    // a candidate that failed at an earlier iterate of this call stays there
+    // (a multi-iterate launch's loop stops at its first failure)
+    if (mode == kModeOpt && P.k_begin > P.traj_k0 && buf.status[b] != kOk) continue;
     // Adam state in registers of lanes < D of warp 0
     double am = 0.0, av = 0.0;
     double b1t = 1.0, b2t = 1.0;
@@ -1516,7 +1513,7 @@ __device__ __forceinline__ void kernel_body(const KHand& H, const KObj& O, const
       // and world points per candidate; the adjoint kernel reloads them.
       double* fkb = Phase != kPhaseFused && record ? buf.fk + static_cast<size_t>(b) * (12 * L + 3 * N) : nullptr;
       for (int t = tid; t < 6 * L * M; t += blockDim.x) ft_all[t] = 0.0;
-      if (tid < 16) sflag[tid] = kOk;
+      for (int t = tid; t <= M; t += blockDim.x) sflag[t] = kOk;
       if constexpr (Phase == kPhaseAdj) {
         for (int t = tid; t < 12 * L; t += blockDim.x) link[t] = __ldcg(fkb + t);
         for (int i = tid; i < N; i += blockDim.x) {
@@ -1547,17 +1544,20 @@ __device__ __forceinline__ void kernel_body(const KHand& H, const KObj& O, const
         __syncthreads();
       }
 
-      // 2-3. perturbation sims, one per warp
-      if (warp < M) {
+      // 2-3. perturbation sims: warp w runs sims w, w + W, ...
+      for (int m = warp; m < M; m += W) {
+        if constexpr (Phase != kPhaseFused) bind_logs(static_cast<size_t>(b) * M + m);  // per (candidate, sim)
+        e.ft = ft_all + m * 6 * L;
         e.radius = radius;
-        e.point_grads = buf.point_grads ? buf.point_grads + (static_cast<size_t>(b) * M + warp) * N * 3 : nullptr;
+        e.point_grads = buf.point_grads ? buf.point_grads + (static_cast<size_t>(b) * M + m) * N * 3 : nullptr;
         SimStats st;
         int status = kOk;
         FtAcc acc;
-        const V3 vm{S.vel[warp][0], S.vel[warp][1], S.vel[warp][2]};
+        const double* vv = m < kMaxSims ? S.vel[m] : S.vel_dev + 3 * m;
+        const V3 vm{vv[0], vv[1], vv[2]};
         const bool meas = mode == kModeEval && S.measure_residual;
         PROF_T(tsim);
-        FwdRec* rec = Phase != kPhaseFused ? buf.fwd + static_cast<size_t>(b) * M + warp : nullptr;
+        FwdRec* rec = Phase != kPhaseFused ? buf.fwd + static_cast<size_t>(b) * M + m : nullptr;
         const double res = run_sim<Phase>(sdf, e, vm, record, meas, st, status, acc, rec);
         PROF_ACC(12, tsim);
         if constexpr (Phase == kPhaseFwd) {
@@ -1569,11 +1569,11 @@ __device__ __forceinline__ void kernel_body(const KHand& H, const KObj& O, const
         ft_flush_warp(acc, e.ft, lane);
         __syncwarp();
         if (lane == 0) {
-          sres[warp] = res;
-          sflag[warp] = status;
-          if (buf.sim_res) buf.sim_res[static_cast<size_t>(b) * M + warp] = res;
+          sres[m] = res;
+          sflag[m] = status;
+          if (buf.sim_res) buf.sim_res[static_cast<size_t>(b) * M + m] = res;
           if (buf.stats && mode == kModeEval) {
-            double* so = buf.stats + (static_cast<size_t>(b) * M + warp) * 5;
+            double* so = buf.stats + (static_cast<size_t>(b) * M + m) * 5;
             so[0] = st.active; so[1] = st.corrections; so[2] = st.singular; so[3] = st.max_pen; so[4] = st.max_fric;
           }
         }
@@ -1584,7 +1584,7 @@ __device__ __forceinline__ void kernel_body(const KHand& H, const KObj& O, const
           for (int t = lane; t < 6 * L; t += 32) ftw[t] = e.ft[t];
           __syncwarp();
           fk_adjoint(H, sq, link, ftw, gw, lane);
-          double* o = buf.sim_grads + (static_cast<size_t>(b) * M + warp) * D;
+          double* o = buf.sim_grads + (static_cast<size_t>(b) * M + m) * D;
           for (int t = lane; t < D; t += 32) o[t] = gw[t];
           __syncwarp();
         }
@@ -1660,6 +1660,7 @@ __device__ __forceinline__ void kernel_body(const KHand& H, const KObj& O, const
           // App. C: weighted gradient, Adam, apply_gradient_step
           double gw = 0.0;
           if (lane < D) gw = S.w_stable * sg[lane] + S.w_qrange * sg[32 + lane] + S.w_qlimit * sg[64 + lane];
+          if (buf.egrad && lane < D) gw = gw + buf.egrad[static_cast<size_t>(b) * D + lane];  // grasp energies
           const bool bad = __any_sync(kFull, lane < D && !isfinite(gw));
           if (bad && cand_status == kOk) cand_status = kNonFiniteGrad;
           if (buf.traj) {
@@ -1693,10 +1694,10 @@ __device__ __forceinline__ void kernel_body(const KHand& H, const KObj& O, const
             for (int j = 0; j < J; ++j) sq[7 + j] = sq[7 + j] - lr * sg[6 + j];
           }
         }
-        if (lane == 0) sflag[15] = cand_status;
+        if (lane == 0) sflag[M] = cand_status;
       }
       __syncthreads();
-      cand_status = sflag[15];
+      cand_status = sflag[M];
       if (cand_status != kOk) break;
     }
     if constexpr (Phase == kPhaseFwd) {
@@ -1868,6 +1869,170 @@ __global__ void __launch_bounds__(256) contacts_kernel(KHand H, Sdf sdf, int B, 
   }
 }
 
+// Grasp-energy terms (north_star (3); no reference counterpart, so
+// parity-unpinned; dgx.h dgx_grasp_energy_batch): one CTA (8 warps) per
+// candidate. FK (hand.hpp:116-152), every hand sample queried at the object's
+// canonical pose (object frame = world, as the contact generation above);
+// contacts C = {|rho| <= thr}. E_fc = |sum_C n|^2 + |sum_C (p - com) x n|^2 / l^2,
+// E_pen = sum max(0, -rho). Gradients with the contact set and normals frozen
+// (sim.hpp:102-104 convention): dE_fc/dp = 2 (n x tau) / l^2 on C, dE_pen/dp =
+// -n where rho < 0, folded per link into force / torque sums (segmented warp
+// scans over the point-ordered samples, then warps in order: deterministic)
+// and mapped to [pos | tangent | joints] by fk_adjoint. Outputs: e [B,2],
+// g [B,2,D] and / or gw [B,D] = w_fc dE_fc + w_pen dE_pen (optimizer).
+constexpr int kEnergyWarps = 8;
+
+__device__ __forceinline__ void seg_flush12(double (&v)[12], int key, double* ftw, int lane) {
+  // inclusive segmented scan over equal consecutive keys (samples are in link
+  // order, so each link is one lane range); the segment's last lane adds it
+#pragma unroll
+  for (int d = 1; d < 32; d <<= 1) {
+    const int kk = __shfl_up_sync(kFull, key, d);
+    double u[12];
+#pragma unroll
+    for (int c = 0; c < 12; ++c) u[c] = __shfl_up_sync(kFull, v[c], d);
+    if (lane >= d && kk == key) {
+#pragma unroll
+      for (int c = 0; c < 12; ++c) v[c] += u[c];
+    }
+  }
+  const int knext = __shfl_down_sync(kFull, key, 1);
+  if (key >= 0 && (lane == 31 || knext != key)) {
+    double* f = ftw + 12 * key;
+#pragma unroll
+    for (int c = 0; c < 12; ++c) f[c] += v[c];
+  }
+  __syncwarp();
+}
+
+template <class Sdf>
+__global__ void __launch_bounds__(32 * kEnergyWarps) energy_kernel(KHand H, const __grid_constant__ KObj O, Sdf sdf,
+                                                                  KSim S, int B, const double* __restrict__ q,
+                                                                  const int* __restrict__ status,
+                                                                  double* __restrict__ e_out,
+                                                                  double* __restrict__ g_out,
+                                                                  double* __restrict__ gw_out) {
+  extern __shared__ __align__(16) unsigned char smem[];
+  const int L = H.L, N = H.N, D = 6 + H.J, Qd = 7 + H.J;
+  double* link = reinterpret_cast<double*>(smem);                 // [12 L]
+  double* sq = link + 12 * L;                                     // [40]
+  double* red = sq + 40;                                          // [8 warps][8]
+  double* ftw = red + 8 * kEnergyWarps;                           // [8 warps][L][12]
+  double* ftf = ftw + kEnergyWarps * 12 * L;                      // [6 L] force closure
+  double* ftp = ftf + 6 * L;                                      // [6 L] penetration
+  double* gg = ftp + 6 * L;                                       // [2][32]
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const double inv_l2 = 1.0 / (S.fc_scale * S.fc_scale);
+  for (int b = blockIdx.x; b < B; b += gridDim.x) {
+    if (status && status[b] != kOk) continue;  // failed earlier in this optimizer call
+    if (tid < Qd) sq[tid] = q[static_cast<size_t>(b) * Qd + tid];
+    for (int t = tid; t < kEnergyWarps * 12 * L; t += blockDim.x) ftw[t] = 0.0;
+    __syncthreads();
+    if (warp == 0) link_transforms_warp(H, sq, false, link, lane);
+    __syncthreads();
+    // pass 1: contact sums f, tau and the penetration sum (fixed-order reduction)
+    double acc[7] = {0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0};
+    for (int i = tid; i < N; i += blockDim.x) {
+      const double* Rl = link + 12 * H.sample_link[i];
+      M3 R;
+      for (int m = 0; m < 9; ++m) R.m[m] = Rl[m];
+      const V3 p = mul(R, V3{H.samples[3 * i], H.samples[3 * i + 1], H.samples[3 * i + 2]}) + V3{Rl[9], Rl[10], Rl[11]};
+      const SdfQuery qq = sdf.query(p);
+      if (fabs(qq.rho) <= S.fc_thr) {
+        const V3 tq = cross(p - O.com, qq.grad);
+        acc[0] += qq.grad.x; acc[1] += qq.grad.y; acc[2] += qq.grad.z;
+        acc[3] += tq.x; acc[4] += tq.y; acc[5] += tq.z;
+      }
+      if (qq.rho < 0.0) acc[6] -= qq.rho;
+    }
+#pragma unroll
+    for (int c = 0; c < 7; ++c) acc[c] = warp_sum(acc[c]);
+    if (lane == 0)
+      for (int c = 0; c < 7; ++c) red[8 * warp + c] = acc[c];
+    __syncthreads();
+    double tot[7];
+#pragma unroll
+    for (int c = 0; c < 7; ++c) {
+      tot[c] = 0.0;
+      for (int w = 0; w < kEnergyWarps; ++w) tot[c] += red[8 * w + c];
+    }
+    const V3 f{tot[0], tot[1], tot[2]}, tau{tot[3], tot[4], tot[5]};
+    const double e_fc = dot(f, f) + dot(tau, tau) * inv_l2, e_pen = tot[6];
+    // pass 2: per-sample gradients folded into per-link force / torque sums
+    // (12 per link: force closure F, T | penetration F, T); chunks of 32
+    // consecutive samples, chunk c on warp c % 8
+    for (int c0 = 32 * warp; c0 < N; c0 += 32 * kEnergyWarps) {
+      const int i = c0 + lane;
+      double v[12];
+#pragma unroll
+      for (int c = 0; c < 12; ++c) v[c] = 0.0;
+      int key = -1;
+      if (i < N) {
+        key = H.sample_link[i];
+        const double* Rl = link + 12 * key;
+        M3 R;
+        for (int m = 0; m < 9; ++m) R.m[m] = Rl[m];
+        const V3 p = mul(R, V3{H.samples[3 * i], H.samples[3 * i + 1], H.samples[3 * i + 2]}) + V3{Rl[9], Rl[10], Rl[11]};
+        const SdfQuery qq = sdf.query(p);
+        if (fabs(qq.rho) <= S.fc_thr) {
+          const V3 gp = cross(qq.grad, tau) * (2.0 * inv_l2);
+          const V3 tq = cross(p, gp);
+          v[0] = gp.x; v[1] = gp.y; v[2] = gp.z; v[3] = tq.x; v[4] = tq.y; v[5] = tq.z;
+        }
+        if (qq.rho < 0.0) {
+          const V3 gp = qq.grad * -1.0;
+          const V3 tq = cross(p, gp);
+          v[6] = gp.x; v[7] = gp.y; v[8] = gp.z; v[9] = tq.x; v[10] = tq.y; v[11] = tq.z;
+        }
+      }
+      seg_flush12(v, key, ftw + warp * 12 * L, lane);
+    }
+    __syncthreads();
+    for (int t = tid; t < 6 * L; t += blockDim.x) {
+      const int l = t / 6, c = t - 6 * l;
+      double sf = 0.0, sp = 0.0;
+      for (int w = 0; w < kEnergyWarps; ++w) {
+        sf += ftw[(w * L + l) * 12 + c];
+        sp += ftw[(w * L + l) * 12 + 6 + c];
+      }
+      ftf[t] = sf;
+      ftp[t] = sp;
+    }
+    __syncthreads();
+    if (warp == 0) fk_adjoint(H, sq, link, ftf, gg, lane);
+    if (warp == 1) fk_adjoint(H, sq, link, ftp, gg + 32, lane);
+    __syncthreads();
+    if (tid < D) {
+      const double gf = gg[tid], gp = gg[32 + tid];
+      if (g_out) {
+        g_out[static_cast<size_t>(b) * 2 * D + tid] = gf;
+        g_out[static_cast<size_t>(b) * 2 * D + D + tid] = gp;
+      }
+      if (gw_out) gw_out[static_cast<size_t>(b) * D + tid] = S.w_fc * gf + S.w_pen * gp;
+    }
+    if (tid == 0 && e_out) {
+      e_out[2 * static_cast<size_t>(b)] = e_fc;
+      e_out[2 * static_cast<size_t>(b) + 1] = e_pen;
+    }
+    __syncthreads();
+  }
+}
+
+cudaError_t launch_energy(const KHand& H, const KObj& O, const SdfSet& sdf, const KSim& S, int B, const double* q,
+                          const int* status, double* e, double* g, double* gw, int grid, cudaStream_t st) {
+  if (B <= 0) return cudaSuccess;
+  const size_t smem = sizeof(double) * (12 * H.L + 40 + 8 * kEnergyWarps + kEnergyWarps * 12 * H.L + 12 * H.L + 64);
+  const int th = 32 * kEnergyWarps;
+  switch (sdf.kind) {
+    case kSdfSphere: energy_kernel<<<grid, th, smem, st>>>(H, O, sdf.sph, S, B, q, status, e, g, gw); break;
+    case kSdfBox: energy_kernel<<<grid, th, smem, st>>>(H, O, sdf.box, S, B, q, status, e, g, gw); break;
+    case kSdfGrid: energy_kernel<<<grid, th, smem, st>>>(H, O, sdf.grd, S, B, q, status, e, g, gw); break;
+    case kSdfMesh: energy_kernel<<<grid, th, smem, st>>>(H, O, sdf.mesh, S, B, q, status, e, g, gw); break;
+    default: return cudaErrorInvalidValue;
+  }
+  return cudaGetLastError();
+}
+
 cudaError_t launch_contacts(const KHand& H, const SdfSet& sdf, int B, const double* q, const double* area, int T,
                             const double* thr, int cap, double* ca, int* cnt, int* ncont, int* cidx, double* crec,
                             int grid, cudaStream_t st) {
@@ -1940,18 +2105,18 @@ static cudaError_t launch_fused_t(const KHand& H, const KObj& O, const Sdf& sdf,
   if constexpr (kSplitCapable<Sdf>) {
     if (phase == kPhaseFwd) {
       if ((e = allow_smem_fwd<Sdf>()) != cudaSuccess) return e;
-      fwd_kernel<Sdf><<<grid, 32 * S.M, smem, st>>>(H, O, sdf, S, P, buf, mode);
+      fwd_kernel<Sdf><<<grid, 32 * S.warps(), smem, st>>>(H, O, sdf, S, P, buf, mode);
       return cudaGetLastError();
     }
     if (phase == kPhaseAdj) {
       if ((e = allow_smem<Sdf, occ, kPhaseAdj>()) != cudaSuccess) return e;
-      fused_kernel<Sdf, occ, kPhaseAdj><<<grid, 32 * S.M, smem, st>>>(H, O, sdf, S, P, buf, mode);
+      fused_kernel<Sdf, occ, kPhaseAdj><<<grid, 32 * S.warps(), smem, st>>>(H, O, sdf, S, P, buf, mode);
       return cudaGetLastError();
     }
   }
   if (phase != kPhaseFused) return cudaErrorInvalidValue;
   if ((e = allow_smem<Sdf, occ, kPhaseFused>()) != cudaSuccess) return e;
-  fused_kernel<Sdf, occ, kPhaseFused><<<grid, 32 * S.M, smem, st>>>(H, O, sdf, S, P, buf, mode);
+  fused_kernel<Sdf, occ, kPhaseFused><<<grid, 32 * S.warps(), smem, st>>>(H, O, sdf, S, P, buf, mode);
   return cudaGetLastError();
 }
 

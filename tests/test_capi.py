@@ -30,7 +30,7 @@ def test_library_exports_every_declared_symbol():
     for n in declared():
         assert hasattr(lib, n), n
     assert set(capi.EXPORTS) == set(declared())
-    assert lib.dgx_abi_version() == 1
+    assert lib.dgx_abi_version() == 2
     nm = subprocess.run(["nm", "-D", "--defined-only", capi.LIB_PATH], capture_output=True, text=True).stdout
     exported = set(re.findall(r" T (dgx_\w+)", nm))
     assert exported == set(declared()), exported ^ set(declared())

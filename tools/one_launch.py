@@ -13,10 +13,11 @@ ctx = api.Context(0)
 hd = model.HandDesc.asset(sys.argv[2] if len(sys.argv) > 2 else "allegro16")
 OBJ = sys.argv[3] if len(sys.argv) > 3 else "boxgrid64"
 od = {"boxgrid64": lambda: model.box_grid(res=64),
+      "blob128": lambda: model.blob_grid(seed=3, res=128),  # config 3 (bench.py headline)
       "ico3": lambda: model.mesh_object(*model.icosphere_mesh(0.025, 3))}[OBJ]()
 hand, obj = api.Hand(ctx, hd), api.GraspObject(ctx, od)
 D = 6 + hd.num_joints
-q = torch.tensor(init.approach_init(od, hd, B, seed=17), device=dev)
+q = torch.tensor(init.approach_init(od, hd, B, seed=3 if OBJ == "blob128" else 17), device=dev)
 m = torch.zeros(B, D, dtype=torch.float64, device=dev)
 v = torch.zeros_like(m)
 s = torch.zeros(B, dtype=torch.int32, device=dev)

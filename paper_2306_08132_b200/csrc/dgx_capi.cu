@@ -266,17 +266,44 @@ constexpr int kSplitMaxFwdSmem = 96 * 1024;
 
 struct SplitGrid {
   int chunk, grid_f, grid_a, smem_f, smem_a;
+  bool task;  // adjoint as warp tasks (adj_task_kernel) instead of one CTA per candidate
 };
+
+// Split adjoint as warp tasks (default; DGX_ADJ_CTA=1 keeps the CTA-per-
+// candidate adjoint for A/B measurements). Its staging length: DGX_TASK_SEG
+// (default 8 points per lane: 8 warps x 11.5 KB leave most of the SM's
+// 256 KB as L1 for the points and SDF cells the tasks read from L2).
+bool use_task_adjoint() {
+  static const bool cta = std::getenv("DGX_ADJ_CTA") != nullptr;
+  return !cta;
+}
+int task_seg() {
+  static const int seg = [] {
+    const char* ev = std::getenv("DGX_TASK_SEG");
+    return ev ? std::max(1, std::min(kSegMaxCap, std::atoi(ev))) : 8;
+  }();
+  return seg;
+}
 
 SplitGrid prepare_split(dgx_ctx* c, Scratch& sc, const dgx_hand* h, const dgx_object* o, KSim& S, int B,
                         bool record, KBuf& buf) {
-  const int M = S.M, N = h->N;
+  const int M = S.M, N = h->N, L = h->L;
   SplitGrid g{};
-  g.smem_a = choose_staging(h, o, S);
-  g.smem_f = SmemLayout(N, h->L, M, 0).total;
+  g.task = record && use_task_adjoint();
+  if (g.task) {
+    S.seg_max = task_seg();
+    S.fold = std::getenv("DGX_NOFOLD") ? 0 : 1;
+    g.smem_a = TaskLayout(L, M, S.seg_max).bytes();
+  } else {
+    g.smem_a = choose_staging(h, o, S);
+  }
+  g.smem_f = SmemLayout(N, L, M, 0, !S.pts_global).total;
   int per_f = 0, per_a = 1;
-  cuda_check(fused_occupancy(o->kind, M, g.smem_f, kPhaseFwd, &per_f), "occupancy");
-  if (record) cuda_check(fused_occupancy(o->kind, M, g.smem_a, kPhaseAdj, &per_a), "occupancy");
+  cuda_check(fused_occupancy(o->kind, M, g.smem_f, S.pts_global ? kPhaseFwdPtsG : kPhaseFwd, &per_f), "occupancy");
+  if (record) {
+    if (g.task) cuda_check(adj_task_occupancy(o->kind, g.smem_a, &per_a), "occupancy");
+    else cuda_check(fused_occupancy(o->kind, M, g.smem_a, kPhaseAdj, &per_a), "occupancy");
+  }
   if (per_f < 1 || per_a < 1) throw DgxError(DGX_E_UNSUPPORTED, "split kernels cannot be resident (registers/smem)");
   g.grid_f = c->num_sms * per_f;
   g.grid_a = c->num_sms * per_a;
@@ -285,8 +312,9 @@ SplitGrid prepare_split(dgx_ctx* c, Scratch& sc, const dgx_hand* h, const dgx_ob
   // DGX_SPLIT_SCRATCH_MB lowers the budget, down to 4 waves of the larger grid per chunk.
   const size_t per_cand = static_cast<size_t>(M) * ((static_cast<size_t>(c->cap_corr) + 1) *
                                                         (sizeof(CorrRec) + sizeof(SlotRec) + sizeof(int)) +
-                                                    sizeof(FwdRec) + static_cast<size_t>(N) * sizeof(int)) +
-                          (12 * static_cast<size_t>(h->L) + 3 * static_cast<size_t>(N)) * sizeof(double);
+                                                    sizeof(FwdRec) + static_cast<size_t>(N) * sizeof(int) +
+                                                    (6 * static_cast<size_t>(L) + 2) * sizeof(double)) +
+                          (12 * static_cast<size_t>(h->L) + 3 * static_cast<size_t>(N)) * sizeof(double) + 8;
   size_t budget = kSplitScratchBytes;
   if (const char* ev = std::getenv("DGX_SPLIT_SCRATCH_MB"))  // tests: force several chunks
     budget = static_cast<size_t>(std::max(1, std::atoi(ev))) << 20;
@@ -299,8 +327,10 @@ SplitGrid prepare_split(dgx_ctx* c, Scratch& sc, const dgx_hand* h, const dgx_ob
   const size_t cap = static_cast<size_t>(c->cap_corr), ss = cap + 1;  // nslot <= ncorr <= cap_corr
   sc.corr.ensure(nws * cap * sizeof(CorrRec));
   const size_t fk_per = 12 * static_cast<size_t>(h->L) + 3 * static_cast<size_t>(N);
+  const size_t task_bytes = nws * (6 * static_cast<size_t>(L) + 1) * sizeof(double) + nws * sizeof(int) +
+                            static_cast<size_t>(g.chunk) * sizeof(int) + 3 * 256;
   sc.slots.ensure(nws * (ss * sizeof(SlotRec) + sizeof(FwdRec) + (ss + N) * sizeof(int)) +
-                  static_cast<size_t>(g.chunk) * fk_per * sizeof(double) + 256);
+                  static_cast<size_t>(g.chunk) * fk_per * sizeof(double) + 256 + task_bytes);
   char* base = static_cast<char*>(sc.slots.p);
   buf.corr = static_cast<CorrRec*>(sc.corr.p);
   buf.slots = reinterpret_cast<SlotRec*>(base);
@@ -310,7 +340,18 @@ SplitGrid prepare_split(dgx_ctx* c, Scratch& sc, const dgx_hand* h, const dgx_ob
   buf.fk = reinterpret_cast<double*>(
       (reinterpret_cast<uintptr_t>(buf.fric_order + nws * ss) + 255) & ~static_cast<uintptr_t>(255));
   buf.slot_stride = static_cast<int>(ss);
-  const size_t nwa = static_cast<size_t>(g.grid_a) * M;
+  {  // warp-task adjoint rows (per (candidate, sim)) and per-candidate counters
+    auto al = [](void* p) {
+      return reinterpret_cast<char*>((reinterpret_cast<uintptr_t>(p) + 255) & ~static_cast<uintptr_t>(255));
+    };
+    char* tb = al(buf.fk + static_cast<size_t>(g.chunk) * fk_per);
+    buf.task_ft = reinterpret_cast<double*>(tb);
+    buf.task_res = buf.task_ft + nws * 6 * static_cast<size_t>(L);
+    buf.task_stat = reinterpret_cast<int*>(al(buf.task_res + nws));
+    buf.task_done = reinterpret_cast<int*>(al(buf.task_stat + nws));
+  }
+  // adjoint spill / correction-matrix buffers per resident warp
+  const size_t nwa = g.task ? static_cast<size_t>(g.grid_a) * kTaskWarps : static_cast<size_t>(g.grid_a) * M;
   sc.ftg.ensure(nwa * (6 * static_cast<size_t>(h->L) + static_cast<size_t>(c->cap_corr) * kCorrMatDoubles) *
                 sizeof(double));
   buf.ft_global = static_cast<double*>(sc.ftg.p);
@@ -382,8 +423,11 @@ void launch_range(dgx_ctx* c, Scratch& sc, const dgx_hand* h, const dgx_object* 
   //   the split's per-iterate launches only cost (config 1: 61.5k vs 69.4k);
   // * forward shared memory > kSplitMaxFwdSmem (N >~ 3000 points): two forward
   //   CTAs leave too little L1 for the SDF cells (config 3, N = 4093: 42.9k vs 45.8k).
-  const bool split = use_split(o) && B > c->num_sms && SmemLayout(N, h->L, M, 0).total <= kSplitMaxFwdSmem &&
-                     !(mode == kModeOpt && P.k_end == P.k_begin);
+  // Large hands (forward shared memory with the points > kSplitMaxFwdSmem,
+  // N >~ 3000) run the forward with its points in global memory (L1 / L2)
+  // so it keeps two CTAs per SM (fwd_kernel<Sdf, true>).
+  const bool split = use_split(o) && B > c->num_sms && !(mode == kModeOpt && P.k_end == P.k_begin);
+  S.pts_global = SmemLayout(N, h->L, M, 0).total > kSplitMaxFwdSmem ? 1 : 0;
   // grasp-energy terms (optimizer only): their weighted gradient depends on
   // the iterate's q, so it is computed per iterate right before the
   // iterate's grasp-search launch and added before Adam (KBuf::egrad)
@@ -454,9 +498,17 @@ void launch_range(dgx_ctx* c, Scratch& sc, const dgx_hand* h, const dgx_object* 
       });
       if (!record) continue;
       bind_claim(sc, cb, nb, st);
-      counted_launch(c, kPhaseAdj, st, "adjoint kernel", [&] {
-        return launch_fused(h->k, o->k, o->sdf, S, Pk, cb, mode, kPhaseAdj, std::min(g.grid_a, nb), g.smem_a, st);
-      });
+      if (g.task) {
+        cuda_check(cudaMemsetAsync(cb.task_done, 0, sizeof(int) * nb, st), "cudaMemsetAsync");
+        const int grid_t = std::max(1, std::min(g.grid_a, (nb * M + kTaskWarps - 1) / kTaskWarps));
+        counted_launch(c, kPhaseAdj, st, "adjoint task kernel", [&] {
+          return launch_adj_task(h->k, o->k, o->sdf, S, Pk, cb, mode, grid_t, g.smem_a, st);
+        });
+      } else {
+        counted_launch(c, kPhaseAdj, st, "adjoint kernel", [&] {
+          return launch_fused(h->k, o->k, o->sdf, S, Pk, cb, mode, kPhaseAdj, std::min(g.grid_a, nb), g.smem_a, st);
+        });
+      }
     }
   }
 }

@@ -19,7 +19,11 @@ enum Mode : int { kModeGrad = 0, kModeEval = 1, kModeOpt = 2 };
 // split pair runs the forward sweep at a higher occupancy (its register
 // budget is not set by the adjoint) and hands over through FwdRec + the
 // per-(candidate, sim) logs.
-enum Phase : int { kPhaseFused = 0, kPhaseFwd = 1, kPhaseAdj = 2 };
+// kPhaseAdjTask: the split adjoint as independent warp tasks (one (candidate,
+// sim) per task, points read from the forward's global copy, the candidate's
+// epilogue run by the warp that finishes its last sim).
+enum Phase : int { kPhaseFused = 0, kPhaseFwd = 1, kPhaseAdj = 2, kPhaseAdjTask = 3,
+                   kPhaseFwdPtsG = 4 /* occupancy query only: the forward with global points */ };
 
 enum Status : int {
   kOk = 0,
@@ -101,7 +105,8 @@ struct KObj {
 struct KSim {
   double dt, mu, alpha, radius;
   int gs, M, measure_residual, seg_max;
-  int steps, pad;
+  int steps, fold;         // fold: warp-task adjoint folds the identical final sweeps (exact)
+  int pts_global, pad2;    // split forward: world points in buf.fk instead of shared memory
   double vel[kMaxSims][3];
   const double* vel_dev;  // [M,3] device copy when M > kMaxSims
   double w_stable, w_qrange, w_qlimit;
@@ -129,6 +134,12 @@ struct KBuf {
   double* traj;         // [B, k_end-k_begin, 3 + D] opt: losses + weighted grad per iterate
   int* status;          // [B]
   const double* egrad;  // [B, D] opt: weighted grasp-energy gradient added before Adam (null: off)
+  // warp-task adjoint (kPhaseAdjTask): per (candidate, sim) link sums, residual
+  // and status, and per candidate the count of finished sims (zeroed per launch)
+  double* task_ft;      // [B, M, 6L]
+  double* task_res;     // [B, M]
+  int* task_stat;       // [B, M]
+  int* task_done;       // [B]
   CorrRec* corr;        // [grid, M, cap_corr]
   SlotRec* slots;       // [grid, M, N]  contact slots (one per hand point at most)
   int* slot_of_point;   // [grid, M, N]
@@ -149,6 +160,23 @@ struct KBuf {
   unsigned long long* claim;
 };
 
+// warp-task adjoint: warps per CTA and the per-warp shared memory (doubles):
+// adjoint staging (also the epilogue's copy of the candidate's per-sim link
+// sums + scratch), link sums of the running sim, configuration, gradients
+constexpr int kTaskWarps = 4;
+struct TaskLayout {
+  int stage, off_ft, off_sq, off_sg, per_warp;
+  __host__ __device__ TaskLayout(int L, int M, int seg_max) {
+    const int a = seg_max * 5 * 32, b2 = (M + 1) * 6 * L + 2 * M + 8;
+    stage = a > b2 ? a : b2;
+    off_ft = stage;
+    off_sq = off_ft + 6 * L;
+    off_sg = off_sq + 40;
+    per_warp = off_sg + 3 * 32;
+  }
+  __host__ __device__ int bytes() const { return 8 * per_warp * kTaskWarps; }
+};
+
 // dynamic shared memory layout (bytes), identical on host and device. Per
 // sim: link force / torque sums (ft) and residuals; per warp: bitmap and
 // adjoint staging (a warp runs sims warp, warp + W, ...).
@@ -160,13 +188,14 @@ struct SmemLayout {
     const int a = seg_max * 5 * 32, b = 6 * L + kMaxDim;
     return a > b ? a : b;
   }
-  __host__ __device__ SmemLayout(int N, int L, int M, int seg_max) {
+  __host__ __device__ SmemLayout(int N, int L, int M, int seg_max, bool points = true) {
     stage_per_warp = stage_doubles(seg_max, L);
     const int W = M < kMaxWarps ? M : kMaxWarps;
+    const int np = points ? N : 0;
     int o = 0;
-    off_px = o; o = align(o + 8 * N);
-    off_py = o; o = align(o + 8 * N);
-    off_pz = o; o = align(o + 8 * N);
+    off_px = o; o = align(o + 8 * np);
+    off_py = o; o = align(o + 8 * np);
+    off_pz = o; o = align(o + 8 * np);
     off_link = o; o = align(o + 8 * 12 * L);
     off_ft = o; o = align(o + 8 * 6 * L * M);
     off_bitmap = o; o = align(o + 4 * ((N + 31) / 32) * W);
@@ -196,6 +225,10 @@ struct SdfSet {
 cudaError_t launch_fused(const KHand& H, const KObj& O, const SdfSet& sdf, const KSim& S, const KOpt& P,
                          const KBuf& buf, int mode, int phase, int grid, int smem, cudaStream_t st);
 cudaError_t fused_occupancy(int kind, int M, int smem, int phase, int* blocks_per_sm);
+// split adjoint as warp tasks (analytic and grid backends); grid = #SM x occupancy
+cudaError_t launch_adj_task(const KHand& H, const KObj& O, const SdfSet& sdf, const KSim& S, const KOpt& P,
+                            const KBuf& buf, int mode, int grid, int smem, cudaStream_t st);
+cudaError_t adj_task_occupancy(int kind, int smem, int* per_sm);
 inline bool split_capable(int kind) { return kind != kSdfMesh; }
 // out[n, 8] = rho - radius, grad (3), proxy (3), sign per point (MeshSdf::dilated,
 // sdf.cpp:62-67); within != 0: dilated_within (sdf.cpp:69-81), culled points

@@ -99,6 +99,7 @@ struct SimEnv {
   int* mcache;            // mesh: [gs*N] packed (face, sign) of the forward's query per point-sweep
   double* mcert;          // mesh: [N,4] nearest-face certificates (reset per sim)
   int* mcf;               // mesh: [N, 1 + kCertFaces]
+  int fold;               // warp-task adjoint: fold the identical final sweeps
 };
 
 // Forward classification of grids through the FP32 pre-filter (see
@@ -841,7 +842,7 @@ __device__ double run_sim(const Sdf& sdf, SimEnv& e, V3 v_m, bool record, bool m
   bool touched = false;
   int ncorr = 0, nslot = 0, nfric = 0;
   const int nwords = (N + 31) / 32;
-  if constexpr (Phase == kPhaseAdj) {
+  if constexpr (Phase == kPhaseAdj || Phase == kPhaseAdjTask) {
     x = V3{rec->x[0], rec->x[1], rec->x[2]};
     q = Q4{rec->q[0], rec->q[1], rec->q[2], rec->q[3]};
     touched = rec->touched != 0;
@@ -1151,7 +1152,9 @@ __device__ double run_sim(const Sdf& sdf, SimEnv& e, V3 v_m, bool record, bool m
 #ifdef DGX_QUIET
   int stage = Kc >= 2 ? 0 : 3;
 #else
-  int stage = 3;
+  // the warp-task adjoint folds (its warps do not wait on each other, so the
+  // saved work is not lost to a barrier); DESIGN.md §3
+  int stage = (Phase == kPhaseAdjTask && e.fold && Kc >= 2) ? 0 : 3;
 #endif
   int k = ncorr - 1;
   V3 Xk_fold{0.0, 0.0, 0.0};
@@ -1425,11 +1428,129 @@ __device__ __forceinline__ int next_candidate(const KBuf& buf, int b, int* s_nex
   return *s_next;
 }
 
-template <class Sdf, int Phase>
+// Per-candidate epilogue of one candidate-iteration, by one warp (losses.cpp:
+// 20-66 reductions, qrange / qlimit losses.hpp:70-93, the FK adjoint, and for
+// the optimizer App. C: weighted gradient, Adam, apply_gradient_step
+// losses.cpp:92-102). sflag / sres: per-sim status and residuals [M]; ft_all:
+// per-sim link sums [M][6L] (summed per entry in sim order); scratch: >= 6L
+// doubles; sg: [3*32]; sq: the configuration (updated in place by a step).
+// Shared by the CTA-per-candidate kernels and the warp-task adjoint.
+__device__ __forceinline__ void candidate_epilogue(const KHand& H, const KSim& S, const KOpt& P, const KBuf& buf,
+                                                   int mode, int b, int k, int lane, const int* sflag,
+                                                   const double* sres, const double* ft_all, const double* link,
+                                                   double* scratch, double* sg, double* sq, double& am, double& av,
+                                                   double& b1t, double& b2t, int& cand_status) {
+  const int M = S.M, L = H.L, J = H.J, D = 6 + J;
+  const bool record = mode != kModeEval;
+  double* stage_all = scratch;
+  for (int m = 0; m < M; ++m)
+    if (sflag[m] != kOk) cand_status = sflag[m];
+  // stability loss: losses.cpp:43-45 (record) / losses.hpp:60-67 (eval)
+  double stable = 0.0;
+  for (int m = 0; m < M; ++m) stable = stable + sres[m];
+  if (record) stable = stable * (1.0 / static_cast<double>(M));
+  else stable = stable / static_cast<double>(M);
+  // qrange / qlimit (losses.hpp:70-93)
+  double qr = 0.0, ql = 0.0;
+  for (int j = 0; j < J; ++j) {
+    const double d = sq[7 + j] - 0.5 * (H.lower[j] + H.upper[j]);
+    qr = qr + d * d;
+  }
+  qr = sqrt(qr);
+  for (int j = 0; j < J; ++j) {
+    const double a = sq[7 + j] - H.upper[j];
+    ql = ql + (a >= 0.0 ? a : 0.0);
+    const double c = H.lower[j] - sq[7 + j];
+    ql = ql + (c >= 0.0 ? c : 0.0);
+  }
+  if (record) {
+    // link sums over the sims (losses.cpp:32-41 order, per entry), lanes over entries
+    for (int t = lane; t < 6 * L; t += 32) {
+      double s = 0.0;
+      for (int m = 0; m < M; ++m) s += ft_all[m * 6 * L + t];
+      stage_all[t] = s;
+    }
+    __syncwarp();
+    fk_adjoint(H, sq, link, stage_all, sg, lane);
+    __syncwarp();
+    if (lane < D) {
+      const double inv_m = 1.0 / static_cast<double>(M);
+      double ds = sg[lane] * inv_m;
+      double dr = 0.0, dl = 0.0;
+      if (lane >= 6) {
+        const int j = lane - 6;
+        const double d = sq[7 + j] - 0.5 * (H.lower[j] + H.upper[j]);
+        dr = qr > 0.0 ? 2.0 * ((0.5 / qr) * d) : 0.0;
+        dl = (sq[7 + j] - H.upper[j] >= 0.0 ? 1.0 : 0.0) + (H.lower[j] - sq[7 + j] >= 0.0 ? -1.0 : 0.0);
+      }
+      sg[lane] = ds;
+      sg[32 + lane] = dr;
+      sg[64 + lane] = dl;
+    }
+    __syncwarp();
+  }
+  const bool finite_loss = isfinite(stable) && isfinite(qr) && isfinite(ql);
+  if (!finite_loss && cand_status == kOk) cand_status = kNonFiniteLoss;
+  if (mode == kModeGrad || mode == kModeEval) {
+    if (lane == 0 && buf.losses) {
+      double* lo = buf.losses + static_cast<size_t>(b) * 3;
+      lo[0] = stable; lo[1] = qr; lo[2] = ql;
+    }
+    if (mode == kModeGrad && lane < D && buf.grads) {
+      double* go = buf.grads + static_cast<size_t>(b) * 3 * D;
+      go[lane] = sg[lane];
+      go[D + lane] = sg[32 + lane];
+      go[2 * D + lane] = sg[64 + lane];
+      if (!isfinite(sg[lane]) && cand_status == kOk) cand_status = kNonFiniteGrad;
+    }
+  } else {
+    // App. C: weighted gradient, Adam, apply_gradient_step
+    double gw = 0.0;
+    if (lane < D) gw = S.w_stable * sg[lane] + S.w_qrange * sg[32 + lane] + S.w_qlimit * sg[64 + lane];
+    if (buf.egrad && lane < D) gw = gw + buf.egrad[static_cast<size_t>(b) * D + lane];  // grasp energies
+    const bool bad = __any_sync(kFull, lane < D && !isfinite(gw));
+    if (bad && cand_status == kOk) cand_status = kNonFiniteGrad;
+    if (buf.traj) {
+      double* tr = buf.traj + (static_cast<size_t>(b) * P.traj_rows + (k - P.traj_k0)) * (3 + D);
+      if (lane == 0) { tr[0] = stable; tr[1] = qr; tr[2] = ql; }
+      if (lane < D) tr[3 + lane] = gw;
+    }
+    b1t = b1t * P.beta1;
+    b2t = b2t * P.beta2;
+    double dir = 0.0;
+    if (lane < D) {
+      const double c1 = 1.0 - P.beta1, c2 = 1.0 - P.beta2;
+      am = P.beta1 * am + c1 * gw;
+      av = P.beta2 * av + c2 * (gw * gw);
+      const double mhat = am / (1.0 - b1t);
+      const double vhat = av / (1.0 - b2t);
+      dir = mhat / (sqrt(vhat) + P.eps);
+    }
+    __syncwarp();
+    if (lane < D) sg[lane] = dir;  // sg now holds the step direction
+    __syncwarp();
+    if (lane == 0 && cand_status == kOk) {
+      // apply_gradient_step (losses.cpp:92-102)
+      const double lr = P.lr;
+      sq[0] = sq[0] - lr * sg[0];
+      sq[1] = sq[1] - lr * sg[1];
+      sq[2] = sq[2] - lr * sg[2];
+      const V3 tangent{-lr * sg[3], -lr * sg[4], -lr * sg[5]};
+      const Q4 qn = qnormalized(qmul(quat_exp(tangent), Q4{sq[3], sq[4], sq[5], sq[6]}));
+      sq[3] = qn.w; sq[4] = qn.x; sq[5] = qn.y; sq[6] = qn.z;
+      for (int j = 0; j < J; ++j) sq[7 + j] = sq[7 + j] - lr * sg[6 + j];
+    }
+  }
+}
+
+// PtsG (split forward only): the world points live in the candidate's global
+// FK record (buf.fk, read through L1 / L2) instead of shared memory, for hands
+// whose 24 N bytes of points would cap the forward at one CTA per SM.
+template <class Sdf, int Phase, bool PtsG = false>
 __device__ __forceinline__ void kernel_body(const KHand& H, const KObj& O, const Sdf& sdf, const KSim& S,
                                             const KOpt& P, const KBuf& buf, int mode) {
   extern __shared__ __align__(16) unsigned char smem[];
-  const SmemLayout lay(H.N, H.L, S.M, Phase == kPhaseFwd ? 0 : S.seg_max);  // the forward stages nothing
+  const SmemLayout lay(H.N, H.L, S.M, Phase == kPhaseFwd ? 0 : S.seg_max, !PtsG);  // the forward stages nothing
   double* px = reinterpret_cast<double*>(smem + lay.off_px);
   double* py = reinterpret_cast<double*>(smem + lay.off_py);
   double* pz = reinterpret_cast<double*>(smem + lay.off_pz);
@@ -1511,7 +1632,14 @@ __device__ __forceinline__ void kernel_body(const KHand& H, const KObj& O, const
         radius = P.iters > 1 ? P.r0 * (1.0 - static_cast<double>(k) / static_cast<double>(P.iters - 1)) : 0.0;
       // 1. FK. Split execution: the forward kernel stores the link transforms
       // and world points per candidate; the adjoint kernel reloads them.
-      double* fkb = Phase != kPhaseFused && record ? buf.fk + static_cast<size_t>(b) * (12 * L + 3 * N) : nullptr;
+      double* fkb = Phase != kPhaseFused && (record || PtsG) ? buf.fk + static_cast<size_t>(b) * (12 * L + 3 * N)
+                                                               : nullptr;
+      if constexpr (PtsG) {
+        px = fkb + 12 * L;
+        py = fkb + 12 * L + N;
+        pz = fkb + 12 * L + 2 * N;
+        e.px = px; e.py = py; e.pz = pz;
+      }
       for (int t = tid; t < 6 * L * M; t += blockDim.x) ft_all[t] = 0.0;
       for (int t = tid; t <= M; t += blockDim.x) sflag[t] = kOk;
       if constexpr (Phase == kPhaseAdj) {
@@ -1532,8 +1660,8 @@ __device__ __forceinline__ void kernel_body(const KHand& H, const KObj& O, const
           for (int m = 0; m < 9; ++m) R.m[m] = Rl[m];
           const V3 s{H.samples[3 * i], H.samples[3 * i + 1], H.samples[3 * i + 2]};
           const V3 p = mul(R, s) + V3{Rl[9], Rl[10], Rl[11]};
-          px[i] = p.x; py[i] = p.y; pz[i] = p.z;
-          if (fkb) {
+          px[i] = p.x; py[i] = p.y; pz[i] = p.z;  // PtsG: plain stores into buf.fk (read back via L1)
+          if (fkb && !PtsG) {
             __stcg(fkb + 12 * L + i, p.x);
             __stcg(fkb + 12 * L + N + i, p.y);
             __stcg(fkb + 12 * L + 2 * N + i, p.z);
@@ -1596,104 +1724,8 @@ __device__ __forceinline__ void kernel_body(const KHand& H, const KObj& O, const
 
       // 4. losses, gradient, optimizer (warp 0)
       if (warp == 0) {
-        for (int m = 0; m < M; ++m)
-          if (sflag[m] != kOk) cand_status = sflag[m];
-        // stability loss: losses.cpp:43-45 (record) / losses.hpp:60-67 (eval)
-        double stable = 0.0;
-        for (int m = 0; m < M; ++m) stable = stable + sres[m];
-        if (record) stable = stable * (1.0 / static_cast<double>(M));
-        else stable = stable / static_cast<double>(M);
-        // qrange / qlimit (losses.hpp:70-93)
-        double qr = 0.0, ql = 0.0;
-        for (int j = 0; j < J; ++j) {
-          const double d = sq[7 + j] - 0.5 * (H.lower[j] + H.upper[j]);
-          qr = qr + d * d;
-        }
-        qr = sqrt(qr);
-        for (int j = 0; j < J; ++j) {
-          const double a = sq[7 + j] - H.upper[j];
-          ql = ql + (a >= 0.0 ? a : 0.0);
-          const double c = H.lower[j] - sq[7 + j];
-          ql = ql + (c >= 0.0 ? c : 0.0);
-        }
-        if (record) {
-          // link sums over the sims (losses.cpp:32-41 order, per entry), lanes over entries
-          for (int t = lane; t < 6 * L; t += 32) {
-            double s = 0.0;
-            for (int m = 0; m < M; ++m) s += ft_all[m * 6 * L + t];
-            stage_all[t] = s;
-          }
-          __syncwarp();
-          fk_adjoint(H, sq, link, stage_all, sg, lane);
-          __syncwarp();
-          if (lane < D) {
-            const double inv_m = 1.0 / static_cast<double>(M);
-            double ds = sg[lane] * inv_m;
-            double dr = 0.0, dl = 0.0;
-            if (lane >= 6) {
-              const int j = lane - 6;
-              const double d = sq[7 + j] - 0.5 * (H.lower[j] + H.upper[j]);
-              dr = qr > 0.0 ? 2.0 * ((0.5 / qr) * d) : 0.0;
-              dl = (sq[7 + j] - H.upper[j] >= 0.0 ? 1.0 : 0.0) + (H.lower[j] - sq[7 + j] >= 0.0 ? -1.0 : 0.0);
-            }
-            sg[lane] = ds;
-            sg[32 + lane] = dr;
-            sg[64 + lane] = dl;
-          }
-          __syncwarp();
-        }
-        const bool finite_loss = isfinite(stable) && isfinite(qr) && isfinite(ql);
-        if (!finite_loss && cand_status == kOk) cand_status = kNonFiniteLoss;
-        if (mode == kModeGrad || mode == kModeEval) {
-          if (lane == 0 && buf.losses) {
-            double* lo = buf.losses + static_cast<size_t>(b) * 3;
-            lo[0] = stable; lo[1] = qr; lo[2] = ql;
-          }
-          if (mode == kModeGrad && lane < D && buf.grads) {
-            double* go = buf.grads + static_cast<size_t>(b) * 3 * D;
-            go[lane] = sg[lane];
-            go[D + lane] = sg[32 + lane];
-            go[2 * D + lane] = sg[64 + lane];
-            if (!isfinite(sg[lane]) && cand_status == kOk) cand_status = kNonFiniteGrad;
-          }
-        } else {
-          // App. C: weighted gradient, Adam, apply_gradient_step
-          double gw = 0.0;
-          if (lane < D) gw = S.w_stable * sg[lane] + S.w_qrange * sg[32 + lane] + S.w_qlimit * sg[64 + lane];
-          if (buf.egrad && lane < D) gw = gw + buf.egrad[static_cast<size_t>(b) * D + lane];  // grasp energies
-          const bool bad = __any_sync(kFull, lane < D && !isfinite(gw));
-          if (bad && cand_status == kOk) cand_status = kNonFiniteGrad;
-          if (buf.traj) {
-            double* tr = buf.traj + (static_cast<size_t>(b) * P.traj_rows + (k - P.traj_k0)) * (3 + D);
-            if (lane == 0) { tr[0] = stable; tr[1] = qr; tr[2] = ql; }
-            if (lane < D) tr[3 + lane] = gw;
-          }
-          b1t = b1t * P.beta1;
-          b2t = b2t * P.beta2;
-          double dir = 0.0;
-          if (lane < D) {
-            const double c1 = 1.0 - P.beta1, c2 = 1.0 - P.beta2;
-            am = P.beta1 * am + c1 * gw;
-            av = P.beta2 * av + c2 * (gw * gw);
-            const double mhat = am / (1.0 - b1t);
-            const double vhat = av / (1.0 - b2t);
-            dir = mhat / (sqrt(vhat) + P.eps);
-          }
-          __syncwarp();
-          if (lane < D) sg[lane] = dir;  // sg now holds the step direction
-          __syncwarp();
-          if (lane == 0 && cand_status == kOk) {
-            // apply_gradient_step (losses.cpp:92-102)
-            const double lr = P.lr;
-            sq[0] = sq[0] - lr * sg[0];
-            sq[1] = sq[1] - lr * sg[1];
-            sq[2] = sq[2] - lr * sg[2];
-            const V3 tangent{-lr * sg[3], -lr * sg[4], -lr * sg[5]};
-            const Q4 qn = qnormalized(qmul(quat_exp(tangent), Q4{sq[3], sq[4], sq[5], sq[6]}));
-            sq[3] = qn.w; sq[4] = qn.x; sq[5] = qn.y; sq[6] = qn.z;
-            for (int j = 0; j < J; ++j) sq[7 + j] = sq[7 + j] - lr * sg[6 + j];
-          }
-        }
+        candidate_epilogue(H, S, P, buf, mode, b, k, lane, sflag, sres, ft_all, link, stage_all, sg, sq, am, av, b1t,
+                           b2t, cand_status);
         if (lane == 0) sflag[M] = cand_status;
       }
       __syncthreads();
@@ -1731,10 +1763,161 @@ __global__ void __launch_bounds__(224, Occ) fused_kernel(KHand H, const __grid_c
 // register file is split per SM sub-partition (16384 each), so 14 warps on 4
 // sub-partitions allow 4096 / 32 = 128 registers per thread; __maxnreg__(144)
 // leaves one CTA per SM (90k vs 101k cand-iter/s)
-template <class Sdf>
+template <class Sdf, bool PtsG = false>
 __global__ void __launch_bounds__(224, kFwdCtasPerSm) fwd_kernel(KHand H, const __grid_constant__ KObj O, Sdf sdf,
                                                                  KSim S, KOpt P, KBuf buf, int mode) {
-  kernel_body<Sdf, kPhaseFwd>(H, O, sdf, S, P, buf, mode);
+  kernel_body<Sdf, kPhaseFwd, PtsG>(H, O, sdf, S, P, buf, mode);
+}
+
+// ---------------------------------------------------------------------------
+// Split adjoint as independent warp tasks (kPhaseAdjTask). A task is one
+// (candidate, sim) pair claimed from the launch's ticket counter; the warp
+// reads the forward's link transforms and world points from global memory
+// (buf.fk, L2-resident), replays the sim's logs in reverse (run_sim), folds
+// its link force / torque sums and writes them with its residual and status
+// per (candidate, sim). The warp that completes a candidate's last sim (a
+// per-candidate counter, release / acquire through __threadfence) runs the
+// candidate's epilogue (candidate_epilogue: loss reductions in sim order, FK
+// adjoint, Adam, step) from __ldcg copies of those rows. No warp waits for
+// another, so sims of uneven cost do not idle the SM at a barrier, and the
+// CTA size is not tied to M.
+template <class Sdf>
+__device__ __forceinline__ void adj_task_body(const KHand& H, const KObj& O, const Sdf& sdf, const KSim& S,
+                                              const KOpt& P, const KBuf& buf, int mode) {
+  extern __shared__ __align__(16) unsigned char smem[];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int M = S.M, N = H.N, L = H.L, J = H.J, D = 6 + J, Qd = 7 + J;
+  const TaskLayout lay(L, M, S.seg_max);
+  double* wb = reinterpret_cast<double*>(smem) + static_cast<size_t>(warp) * lay.per_warp;
+  double* stage = wb;
+  double* ftw = wb + lay.off_ft;
+  double* sq = wb + lay.off_sq;
+  double* sg = wb + lay.off_sg;
+  const int gwarp = static_cast<int>(blockIdx.x) * kTaskWarps + warp;
+  const int nwarps = static_cast<int>(gridDim.x) * kTaskWarps;
+
+  SimEnv e;
+  e.lane = lane;
+  e.N = N;
+  e.gs = S.gs;
+  e.sample_link = H.sample_link;
+  e.bitmap = nullptr;
+  e.stage = stage;
+  e.seg_max = S.seg_max;
+  e.ft = ftw;
+  e.gft = buf.ft_global + static_cast<size_t>(gwarp) * 6 * L;
+  e.cmat = buf.cmat + static_cast<size_t>(gwarp) * buf.cap_corr * kCorrMat;
+  e.L = L;
+  e.cap_corr = buf.cap_corr;
+  e.O = &O;
+  e.alpha = S.alpha;
+  e.mu = S.mu;
+  e.dt = S.dt;
+  e.mcache = nullptr;
+  e.mcert = nullptr;
+  e.mcf = nullptr;
+  e.fold = S.fold;
+  const int k = mode == kModeOpt ? P.k_begin : 0;
+  e.radius = S.radius;
+  if (mode == kModeOpt)
+    e.radius = P.iters > 1 ? P.r0 * (1.0 - static_cast<double>(k) / static_cast<double>(P.iters - 1)) : 0.0;
+  const long long ntask = static_cast<long long>(buf.B) * M;
+  long long t = gwarp;
+  while (t < ntask) {
+    const int b = static_cast<int>(t / M), m = static_cast<int>(t - static_cast<long long>(b) * M);
+    const size_t bm = static_cast<size_t>(b) * M + m;
+    const bool skip = mode == kModeOpt && P.k_begin > P.traj_k0 && buf.status[b] != kOk;
+    if (!skip) {
+      e.corr = buf.corr + bm * buf.cap_corr;
+      e.slots = buf.slots + bm * buf.slot_stride;
+      e.slot_of_point = buf.slot_of_point + bm * N;
+      e.fric_order = buf.fric_order + bm * buf.slot_stride;
+      const double* fkb = buf.fk + static_cast<size_t>(b) * (12 * L + 3 * N);
+      e.px = fkb + 12 * L;
+      e.py = fkb + 12 * L + N;
+      e.pz = fkb + 12 * L + 2 * N;
+      e.point_grads = buf.point_grads ? buf.point_grads + bm * N * 3 : nullptr;
+      for (int i = lane; i < 6 * L; i += 32) ftw[i] = 0.0;
+      __syncwarp();
+      SimStats st;
+      int status = kOk;
+      FtAcc acc;
+      const double* vv = m < kMaxSims ? S.vel[m] : S.vel_dev + 3 * m;
+      const V3 vm{vv[0], vv[1], vv[2]};
+      const double res = run_sim<kPhaseAdjTask>(sdf, e, vm, true, false, st, status, acc, buf.fwd + bm);
+      ft_flush_warp(acc, ftw, lane);
+      __syncwarp();
+      for (int i = lane; i < 6 * L; i += 32) __stcg(buf.task_ft + bm * 6 * L + i, ftw[i]);
+      if (lane == 0) {
+        __stcg(buf.task_res + bm, res);
+        __stcg(buf.task_stat + bm, status);
+        if (buf.sim_res) buf.sim_res[bm] = res;
+      }
+      if (buf.sim_grads) {  // debug: per-perturbation gradient via the FK adjoint
+        if (lane < Qd) sq[lane] = buf.q[static_cast<size_t>(b) * Qd + lane];
+        double* ftc = stage;
+        for (int i = lane; i < 6 * L; i += 32) ftc[i] = ftw[i];
+        __syncwarp();
+        fk_adjoint(H, sq, fkb, ftc, sg, lane);
+        for (int i = lane; i < D; i += 32) buf.sim_grads[bm * D + i] = sg[i];
+        __syncwarp();
+      }
+    }
+    // publish this sim, then count it; the candidate's last sim runs its epilogue
+    __threadfence();
+    __syncwarp();
+    int prev = 0;
+    if (lane == 0) prev = atomicAdd(buf.task_done + b, 1);
+    prev = __shfl_sync(kFull, prev, 0);
+    if (prev == M - 1 && !skip) {
+      __threadfence();  // acquire: the other sims' rows are visible
+      const size_t b0 = static_cast<size_t>(b) * M;
+      double* ft_all = stage;                        // [M][6L]
+      double* sres = stage + M * 6 * L;              // [M]
+      int* sflag = reinterpret_cast<int*>(sres + M); // [M]
+      double* scratch = sres + M + (M + 1) / 2 + 1;  // [6L]
+      for (int i = lane; i < M * 6 * L; i += 32) ft_all[i] = __ldcg(buf.task_ft + b0 * 6 * L + i);
+      for (int i = lane; i < M; i += 32) {
+        sres[i] = __ldcg(buf.task_res + b0 + i);
+        sflag[i] = __ldcg(buf.task_stat + b0 + i);
+      }
+      if (lane < Qd) sq[lane] = buf.q[static_cast<size_t>(b) * Qd + lane];
+      double am = 0.0, av = 0.0, b1t = 1.0, b2t = 1.0;
+      if (mode == kModeOpt) {
+        if (lane < D) {
+          am = buf.adam_m[static_cast<size_t>(b) * D + lane];
+          av = buf.adam_v[static_cast<size_t>(b) * D + lane];
+        }
+        for (int kk = 0; kk < P.k_begin; ++kk) { b1t = b1t * P.beta1; b2t = b2t * P.beta2; }
+      }
+      __syncwarp();
+      int cand_status = kOk;
+      const double* link = buf.fk + static_cast<size_t>(b) * (12 * L + 3 * N);
+      candidate_epilogue(H, S, P, buf, mode, b, k, lane, sflag, sres, ft_all, link, scratch, sg, sq, am, av, b1t, b2t,
+                         cand_status);
+      __syncwarp();
+      if (mode == kModeOpt) {
+        if (lane < Qd) buf.q[static_cast<size_t>(b) * Qd + lane] = sq[lane];
+        if (lane < D) {
+          buf.adam_m[static_cast<size_t>(b) * D + lane] = am;
+          buf.adam_v[static_cast<size_t>(b) * D + lane] = av;
+        }
+      }
+      if (lane == 0) buf.status[b] = cand_status;
+      __syncwarp();
+    }
+    // next task
+    long long nt = 0;
+    if (lane == 0) nt = buf.claim ? static_cast<long long>(atomicAdd(buf.claim, 1ull)) + nwarps : t + nwarps;
+    t = __shfl_sync(kFull, nt, 0);
+  }
+}
+
+template <class Sdf, int MinBlocks>
+__global__ void __launch_bounds__(32 * kTaskWarps, MinBlocks) adj_task_kernel(KHand H, const __grid_constant__ KObj O,
+                                                                              Sdf sdf, KSim S, KOpt P, KBuf buf,
+                                                                              int mode) {
+  adj_task_body<Sdf>(H, O, sdf, S, P, buf, mode);
 }
 }  // namespace dgx
 
@@ -2083,11 +2266,12 @@ static cudaError_t allow_smem() {
   return e;
 }
 
-template <class Sdf>
+template <class Sdf, bool PtsG>
 static cudaError_t allow_smem_fwd() {
   static bool configured = false;
   if (configured) return cudaSuccess;
-  cudaError_t e = cudaFuncSetAttribute(fwd_kernel<Sdf>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+  cudaError_t e =
+      cudaFuncSetAttribute(fwd_kernel<Sdf, PtsG>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
   if (e == cudaSuccess) configured = true;
   return e;
 }
@@ -2104,8 +2288,13 @@ static cudaError_t launch_fused_t(const KHand& H, const KObj& O, const Sdf& sdf,
   cudaError_t e = cudaSuccess;
   if constexpr (kSplitCapable<Sdf>) {
     if (phase == kPhaseFwd) {
-      if ((e = allow_smem_fwd<Sdf>()) != cudaSuccess) return e;
-      fwd_kernel<Sdf><<<grid, 32 * S.warps(), smem, st>>>(H, O, sdf, S, P, buf, mode);
+      if (S.pts_global) {
+        if ((e = allow_smem_fwd<Sdf, true>()) != cudaSuccess) return e;
+        fwd_kernel<Sdf, true><<<grid, 32 * S.warps(), smem, st>>>(H, O, sdf, S, P, buf, mode);
+      } else {
+        if ((e = allow_smem_fwd<Sdf, false>()) != cudaSuccess) return e;
+        fwd_kernel<Sdf, false><<<grid, 32 * S.warps(), smem, st>>>(H, O, sdf, S, P, buf, mode);
+      }
       return cudaGetLastError();
     }
     if (phase == kPhaseAdj) {
@@ -2118,6 +2307,66 @@ static cudaError_t launch_fused_t(const KHand& H, const KObj& O, const Sdf& sdf,
   if ((e = allow_smem<Sdf, occ, kPhaseFused>()) != cudaSuccess) return e;
   fused_kernel<Sdf, occ, kPhaseFused><<<grid, 32 * S.warps(), smem, st>>>(H, O, sdf, S, P, buf, mode);
   return cudaGetLastError();
+}
+
+// warp-task adjoint instances: kTaskMinBlocks CTAs of kTaskWarps warps per SM
+// sets the register budget (2 -> 8 warps/SM at <= 255 registers; 3 -> 12
+// warps at <= 168)
+#ifndef DGX_TASK_MINBLOCKS
+#define DGX_TASK_MINBLOCKS 2
+#endif
+constexpr int kTaskMinBlocks = DGX_TASK_MINBLOCKS;
+
+template <class Sdf>
+static cudaError_t task_attr() {
+  static bool configured = false;
+  if (configured) return cudaSuccess;
+  cudaError_t e = cudaFuncSetAttribute(adj_task_kernel<Sdf, kTaskMinBlocks>,
+                                       cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+  if (e == cudaSuccess) configured = true;
+  return e;
+}
+
+template <class Sdf>
+static cudaError_t launch_task_t(const KHand& H, const KObj& O, const Sdf& sdf, const KSim& S, const KOpt& P,
+                                 const KBuf& buf, int mode, int grid, int smem, cudaStream_t st) {
+  if constexpr (kSplitCapable<Sdf>) {
+    cudaError_t e = task_attr<Sdf>();
+    if (e != cudaSuccess) return e;
+    adj_task_kernel<Sdf, kTaskMinBlocks><<<grid, 32 * kTaskWarps, smem, st>>>(H, O, sdf, S, P, buf, mode);
+    return cudaGetLastError();
+  }
+  return cudaErrorInvalidValue;
+}
+
+cudaError_t launch_adj_task(const KHand& H, const KObj& O, const SdfSet& sdf, const KSim& S, const KOpt& P,
+                            const KBuf& buf, int mode, int grid, int smem, cudaStream_t st) {
+  switch (sdf.kind) {
+    case kSdfSphere: return launch_task_t(H, O, sdf.sph, S, P, buf, mode, grid, smem, st);
+    case kSdfBox: return launch_task_t(H, O, sdf.box, S, P, buf, mode, grid, smem, st);
+    case kSdfGrid: return launch_task_t(H, O, sdf.grd, S, P, buf, mode, grid, smem, st);
+    default: return cudaErrorInvalidValue;
+  }
+}
+
+template <class Sdf>
+static cudaError_t task_occ_t(int smem, int* per_sm) {
+  if constexpr (kSplitCapable<Sdf>) {
+    cudaError_t e = task_attr<Sdf>();
+    if (e != cudaSuccess) return e;
+    return cudaOccupancyMaxActiveBlocksPerMultiprocessor(per_sm, adj_task_kernel<Sdf, kTaskMinBlocks>,
+                                                         32 * kTaskWarps, smem);
+  }
+  return cudaErrorInvalidValue;
+}
+
+cudaError_t adj_task_occupancy(int kind, int smem, int* per_sm) {
+  switch (kind) {
+    case kSdfSphere: return task_occ_t<SphereSdf>(smem, per_sm);
+    case kSdfBox: return task_occ_t<BoxSdf>(smem, per_sm);
+    case kSdfGrid: return task_occ_t<GridSdf>(smem, per_sm);
+    default: return cudaErrorInvalidValue;
+  }
 }
 
 cudaError_t launch_fused(const KHand& H, const KObj& O, const SdfSet& sdf, const KSim& S, const KOpt& P,
@@ -2135,17 +2384,20 @@ template <class Sdf, int Occ, int Phase>
 static cudaError_t occupancy_i(int M, int smem, int* blocks_per_sm) {
   cudaError_t e = allow_smem<Sdf, Occ, Phase>();
   if (e != cudaSuccess) return e;
-  return cudaOccupancyMaxActiveBlocksPerMultiprocessor(blocks_per_sm, fused_kernel<Sdf, Occ, Phase>, 32 * M, smem);
+  return cudaOccupancyMaxActiveBlocksPerMultiprocessor(blocks_per_sm, fused_kernel<Sdf, Occ, Phase>,
+                                                       32 * (M < kMaxWarps ? M : kMaxWarps), smem);
 }
 
 template <class Sdf>
 static cudaError_t occupancy_t(int M, int smem, int phase, int* blocks_per_sm) {
   constexpr int occ = CtasPerSm<Sdf>::value;
   if constexpr (kSplitCapable<Sdf>) {
-    if (phase == kPhaseFwd) {
-      cudaError_t e = allow_smem_fwd<Sdf>();
+    if (phase == kPhaseFwd || phase == kPhaseFwdPtsG) {
+      const bool g = phase == kPhaseFwdPtsG;
+      cudaError_t e = g ? allow_smem_fwd<Sdf, true>() : allow_smem_fwd<Sdf, false>();
       if (e != cudaSuccess) return e;
-      return cudaOccupancyMaxActiveBlocksPerMultiprocessor(blocks_per_sm, fwd_kernel<Sdf>, 32 * M, smem);
+      return cudaOccupancyMaxActiveBlocksPerMultiprocessor(blocks_per_sm, g ? fwd_kernel<Sdf, true> : fwd_kernel<Sdf, false>,
+                                                           32 * (M < kMaxWarps ? M : kMaxWarps), smem);
     }
     if (phase == kPhaseAdj) return occupancy_i<Sdf, occ, kPhaseAdj>(M, smem, blocks_per_sm);
   }

@@ -269,13 +269,14 @@ struct SplitGrid {
   bool task;  // adjoint as warp tasks (adj_task_kernel) instead of one CTA per candidate
 };
 
-// Split adjoint as warp tasks (default; DGX_ADJ_CTA=1 keeps the CTA-per-
-// candidate adjoint for A/B measurements). Its staging length: DGX_TASK_SEG
-// (default 8 points per lane: 8 warps x 11.5 KB leave most of the SM's
-// 256 KB as L1 for the points and SDF cells the tasks read from L2).
+// Split adjoint as warp tasks (DGX_ADJ_TASK=1; measured equal to the CTA-per-
+// candidate adjoint on configs 2 and 3, so the CTA adjoint,
+// bit-identical to the fused kernel, stays the default). Its staging length:
+// DGX_TASK_SEG (default 8 points per lane: 8 warps x 11.5 KB leave most of the
+// SM's 256 KB as L1 for the points and SDF cells the tasks read from L2).
 bool use_task_adjoint() {
-  static const bool cta = std::getenv("DGX_ADJ_CTA") != nullptr;
-  return !cta;
+  static const bool task = std::getenv("DGX_ADJ_TASK") != nullptr;
+  return task;
 }
 int task_seg() {
   static const int seg = [] {
@@ -296,6 +297,7 @@ SplitGrid prepare_split(dgx_ctx* c, Scratch& sc, const dgx_hand* h, const dgx_ob
     g.smem_a = TaskLayout(L, M, S.seg_max).bytes();
   } else {
     g.smem_a = choose_staging(h, o, S);
+    S.fold = std::getenv("DGX_CTA_FOLD") ? 1 : 0;
   }
   g.smem_f = SmemLayout(N, L, M, 0, !S.pts_global).total;
   int per_f = 0, per_a = 1;

@@ -163,7 +163,11 @@ struct KBuf {
 // warp-task adjoint: warps per CTA and the per-warp shared memory (doubles):
 // adjoint staging (also the epilogue's copy of the candidate's per-sim link
 // sums + scratch), link sums of the running sim, configuration, gradients
-constexpr int kTaskWarps = 4;
+#ifndef DGX_TASK_WARPS
+#define DGX_TASK_WARPS 8
+#endif
+constexpr int kTaskWarps = DGX_TASK_WARPS;
+constexpr int kTaskRing = 8;  // candidate slots a task CTA can have in flight
 struct TaskLayout {
   int stage, off_ft, off_sq, off_sg, per_warp;
   __host__ __device__ TaskLayout(int L, int M, int seg_max) {
@@ -174,7 +178,8 @@ struct TaskLayout {
     off_sg = off_sq + 40;
     per_warp = off_sg + 3 * 32;
   }
-  __host__ __device__ int bytes() const { return 8 * per_warp * kTaskWarps; }
+  // + the CTA's task queue: next task, ring of (slot tag | candidate), per-slot resolved counts
+  __host__ __device__ int bytes() const { return 8 * per_warp * kTaskWarps + 16 + 8 * kTaskRing + 4 * kTaskRing; }
 };
 
 // dynamic shared memory layout (bytes), identical on host and device. Per

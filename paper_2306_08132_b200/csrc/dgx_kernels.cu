@@ -35,7 +35,7 @@
 
 #ifdef DGX_PROFILE_REGIONS
 namespace dgx {
-__device__ unsigned long long g_prof[32];
+__device__ unsigned long long g_prof[48];
 }
 // mesh traversal counters (lane 0 of each warp): 23 nearest queries, 24
 // nearest node pops, 25 ray casts, 26 ray node pops, 27 exact queries
@@ -435,6 +435,7 @@ __device__ void process_run(const Sdf& sdf, SimEnv& e, int lo, int hi, V3 xk, Q4
   // run fed with sum_k X_k and c0scale = K emits the sum over K identical runs.
   const int lane = e.lane, N = e.N;
   double* stg = e.stage;
+  PROF_CNT(35, map_out ? 0 : hi - lo);
   // H . k == ([0,k] (x) q_k) . aQ ; G = Iw^T H  (theta-axpy coefficient)
   const V3 H{-qk.x * aQ.w + qk.w * aQ.x - qk.z * aQ.y + qk.y * aQ.z,
              -qk.y * aQ.w + qk.z * aQ.x + qk.w * aQ.y - qk.x * aQ.z,
@@ -1050,6 +1051,8 @@ __device__ double run_sim(const Sdf& sdf, SimEnv& e, V3 v_m, bool record, bool m
     return residual;
   }
   if (!record || !touched) return residual;  // untouched: constant loss, zero gradient
+  PROF_CNT(32, 1);
+  PROF_CNT(36, ncorr);
 
   for (int t = lane; t < 6 * e.L; t += 32) e.gft[t] = 0.0;
   __syncwarp();
@@ -1149,12 +1152,14 @@ __device__ double run_sim(const Sdf& sdf, SimEnv& e, V3 v_m, bool record, bool m
   const int lo_f = ncorr > 0 ? e.corr[ncorr - 1].f + 1 : 0;
   const int Kc = (hi - lo_f) / N;
   const int rhead = (hi - lo_f) - Kc * N;
+  PROF_CNT(33, Kc >= 2 ? 1 : 0);
+  PROF_CNT(34, Kc);
 #ifdef DGX_QUIET
   int stage = Kc >= 2 ? 0 : 3;
 #else
   // the warp-task adjoint folds (its warps do not wait on each other, so the
   // saved work is not lost to a barrier); DESIGN.md §3
-  int stage = (Phase == kPhaseAdjTask && e.fold && Kc >= 2) ? 0 : 3;
+  int stage = ((Phase == kPhaseAdjTask || Phase == kPhaseAdj) && e.fold && Kc >= 2) ? 0 : 3;
 #endif
   int k = ncorr - 1;
   V3 Xk_fold{0.0, 0.0, 0.0};
@@ -1601,6 +1606,7 @@ __device__ __forceinline__ void kernel_body(const KHand& H, const KObj& O, const
   e.mu = S.mu;
   e.dt = S.dt;
   e.point_grads = nullptr;
+  e.fold = S.fold;
   e.mcache = buf.mesh_cache ? buf.mesh_cache + wslot * static_cast<size_t>(S.gs) * N : nullptr;
   e.mcert = buf.mesh_cert ? buf.mesh_cert + wslot * 4 * static_cast<size_t>(N) : nullptr;
   e.mcf = buf.mesh_cf ? buf.mesh_cf + wslot * static_cast<size_t>(kCertFaces + 1) * N : nullptr;
@@ -1794,7 +1800,18 @@ __device__ __forceinline__ void adj_task_body(const KHand& H, const KObj& O, con
   double* sq = wb + lay.off_sq;
   double* sg = wb + lay.off_sg;
   const int gwarp = static_cast<int>(blockIdx.x) * kTaskWarps + warp;
-  const int nwarps = static_cast<int>(gridDim.x) * kTaskWarps;
+  // CTA task queue (after the warps' areas): the CTA's warps take the sims of
+  // the same few candidates, so those candidates' points stay in the SM's L1
+  unsigned char* qbase = smem + 8 * static_cast<size_t>(lay.per_warp) * kTaskWarps;
+  int* q_next = reinterpret_cast<int*>(qbase);
+  unsigned long long* q_ring = reinterpret_cast<unsigned long long*>(qbase + 16);
+  int* q_done = reinterpret_cast<int*>(qbase + 16 + 8 * kTaskRing);
+  if (threadIdx.x == 0) *q_next = 0;
+  if (threadIdx.x < kTaskRing) {
+    q_ring[threadIdx.x] = 0ull;
+    q_done[threadIdx.x] = M;  // slot never used: free
+  }
+  __syncthreads();
 
   SimEnv e;
   e.lane = lane;
@@ -1821,10 +1838,44 @@ __device__ __forceinline__ void adj_task_body(const KHand& H, const KObj& O, con
   e.radius = S.radius;
   if (mode == kModeOpt)
     e.radius = P.iters > 1 ? P.r0 * (1.0 - static_cast<double>(k) / static_cast<double>(P.iters - 1)) : 0.0;
-  const long long ntask = static_cast<long long>(buf.B) * M;
-  long long t = gwarp;
-  while (t < ntask) {
-    const int b = static_cast<int>(t / M), m = static_cast<int>(t - static_cast<long long>(b) * M);
+  // next task of this warp: task j of the CTA is sim j % M of its candidate
+  // slot j / M. The warp that takes sim 0 claims the slot's candidate (the
+  // CTA's first slot: blockIdx.x; later ones: a launch ticket + gridDim.x) and
+  // publishes it tagged with the slot; the other sims' warps read it. A ring
+  // entry is reused only after all M sims of its previous slot read it.
+  auto next_task = [&](int& b, int& m) {
+    int cb = 0, cm = 0;
+    if (lane == 0) {
+      const int j = atomicAdd(q_next, 1);
+      const int c = j / M;
+      cm = j - c * M;
+      const int r = c % kTaskRing;
+      volatile unsigned long long* ring = q_ring;
+      volatile int* done = q_done;
+      if (cm == 0) {
+        while (done[r] < M) {
+        }
+        int cand = static_cast<int>(blockIdx.x) + c * static_cast<int>(gridDim.x);  // static (no counter)
+        if (c > 0 && buf.claim)
+          cand = static_cast<int>(min(atomicAdd(buf.claim, 1ull), static_cast<unsigned long long>(INT_MAX / 2))) +
+                 static_cast<int>(gridDim.x);
+        done[r] = 0;
+        __threadfence_block();
+        ring[r] = (static_cast<unsigned long long>(c + 1) << 32) | static_cast<unsigned int>(cand);
+      }
+      unsigned long long v;
+      do {
+        v = ring[r];
+      } while (static_cast<int>(v >> 32) != c + 1);
+      cb = static_cast<int>(v & 0xffffffffull);
+      atomicAdd(q_done + r, 1);
+    }
+    b = __shfl_sync(kFull, cb, 0);
+    m = __shfl_sync(kFull, cm, 0);
+  };
+  int b = 0, m = 0;
+  next_task(b, m);
+  while (b < buf.B) {
     const size_t bm = static_cast<size_t>(b) * M + m;
     const bool skip = mode == kModeOpt && P.k_begin > P.traj_k0 && buf.status[b] != kOk;
     if (!skip) {
@@ -1906,10 +1957,7 @@ __device__ __forceinline__ void adj_task_body(const KHand& H, const KObj& O, con
       if (lane == 0) buf.status[b] = cand_status;
       __syncwarp();
     }
-    // next task
-    long long nt = 0;
-    if (lane == 0) nt = buf.claim ? static_cast<long long>(atomicAdd(buf.claim, 1ull)) + nwarps : t + nwarps;
-    t = __shfl_sync(kFull, nt, 0);
+    next_task(b, m);
   }
 }
 
@@ -2313,7 +2361,7 @@ static cudaError_t launch_fused_t(const KHand& H, const KObj& O, const Sdf& sdf,
 // sets the register budget (2 -> 8 warps/SM at <= 255 registers; 3 -> 12
 // warps at <= 168)
 #ifndef DGX_TASK_MINBLOCKS
-#define DGX_TASK_MINBLOCKS 2
+#define DGX_TASK_MINBLOCKS 1
 #endif
 constexpr int kTaskMinBlocks = DGX_TASK_MINBLOCKS;
 
@@ -2464,10 +2512,10 @@ cudaError_t launch_step(int J, const double* q, const double* g, double lr, doub
 
 #ifdef DGX_PROFILE_REGIONS
 extern "C" int dgx_prof_read(unsigned long long* out, int n, int reset) {
-  if (n > 32) n = 32;
+  if (n > 48) n = 48;
   cudaMemcpyFromSymbol(out, dgx::g_prof, sizeof(unsigned long long) * n);
   if (reset) {
-    unsigned long long z[32] = {0};
+    unsigned long long z[48] = {0};
     cudaMemcpyToSymbol(dgx::g_prof, z, sizeof z);
   }
   return cudaGetLastError() == cudaSuccess ? 0 : 101;

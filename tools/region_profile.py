@@ -24,30 +24,35 @@ COUNTS = {16: "forward chunk iterations", 17: "forward candidate lanes", 18: "ad
           23: "mesh nearest queries (lane 0)", 24: "mesh nearest node pops (lane 0)",
           25: "mesh ray casts (lane 0)", 26: "mesh ray node pops (lane 0)", 27: "mesh exact queries (lane 0)",
           28: "mesh certified queries (lane 0)", 29: "mesh cycles: certified argmin (lane 0)",
-          30: "mesh cycles: re-certification (lane 0)", 31: "mesh cycles: phong + ray-cast sign (lane 0)"}
+          30: "mesh cycles: re-certification (lane 0)", 31: "mesh cycles: phong + ray-cast sign (lane 0)",
+          32: "sims entering the adjoint (touched)", 33: "  of which fold-eligible (>= 2 final cycles)",
+          34: "  final-run cycles Kc (sum)", 35: "adjoint emitted positions (point-sweeps)",
+          36: "  corrections in adjoint sims"}
 
 
 def main():
     hand_name = sys.argv[1] if len(sys.argv) > 1 else "allegro16"
     B = int(sys.argv[2]) if len(sys.argv) > 2 else 512
     obj_name = sys.argv[3] if len(sys.argv) > 3 else "boxgrid64"
+    K0 = int(sys.argv[4]) if len(sys.argv) > 4 else 2  # profiled iterate
     L = capi.load()
     L.dgx_prof_read.argtypes = [C.POINTER(C.c_ulonglong), C.c_int, C.c_int]
     ctx = api.Context(0)
     hd = model.HandDesc.asset(hand_name)
     od = {"boxgrid64": lambda: model.box_grid(res=64),
           "ico3": lambda: model.mesh_object(*model.icosphere_mesh(0.025, 3)),
+          "blob128": lambda: model.blob_grid(seed=3, res=128),
           "sphere": lambda: model.sphere(0.025)}[obj_name]()
     hand, obj = api.Hand(ctx, hd), api.GraspObject(ctx, od)
-    q = init.approach_init(od, hd, B, seed=17)
+    q = init.approach_init(od, hd, B, seed=3 if obj_name == "blob128" else 17)
     proto, w = api.StabilityProtocol.standard(), api.LossWeights()
     opt = api.OptConfig(iterations=500)
-    buf = (C.c_ulonglong * 32)()
-    out = api.optimize(ctx, obj, hand, q, proto, api.SimParams(), w, opt, k_begin=0, k_end=2)
-    L.dgx_prof_read(buf, 32, 1)
-    out = api.optimize(ctx, obj, hand, out["q"], proto, api.SimParams(), w, opt, k_begin=2, k_end=3,
+    buf = (C.c_ulonglong * 48)()
+    out = api.optimize(ctx, obj, hand, q, proto, api.SimParams(), w, opt, k_begin=0, k_end=K0)
+    L.dgx_prof_read(buf, 48, 1)
+    out = api.optimize(ctx, obj, hand, out["q"], proto, api.SimParams(), w, opt, k_begin=K0, k_end=K0 + 1,
                        adam_m=out["m"], adam_v=out["v"])
-    L.dgx_prof_read(buf, 32, 1)
+    L.dgx_prof_read(buf, 48, 1)
     v = np.array(list(buf), dtype=np.float64)
     ci = B * 1
     tot = v[12]

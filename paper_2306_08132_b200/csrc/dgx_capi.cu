@@ -134,8 +134,6 @@ void set_device(dgx_ctx* c) { cuda_check(cudaSetDevice(c->device), "cudaSetDevic
 KSim make_sim(const dgx_params* p, bool eval) {
   if (!p) throw DgxError(DGX_E_INVALID, "params is NULL");
   if (p->steps < 1) throw DgxError(DGX_E_INVALID, "StabilityProtocol::steps must be >= 1");
-  if (p->steps != 1)
-    throw DgxError(DGX_E_UNSUPPORTED, "StabilityProtocol::steps != 1 is not supported by this build");
   if (p->num_velocities < 1) throw DgxError(DGX_E_INVALID, "protocol must have >= 1 velocities");
   if (p->num_velocities > kMaxSims && !p->velocity_list)
     throw DgxError(DGX_E_INVALID, "more than 8 velocities need params->velocity_list");
@@ -220,12 +218,20 @@ int prepare(dgx_ctx* c, Scratch& sc, const dgx_hand* h, const dgx_object* o, KSi
   const size_t nws = static_cast<size_t>(grid) * M;
   sc.corr.ensure(nws * c->cap_corr * sizeof(CorrRec));
   const size_t per = nws * static_cast<size_t>(h->N);
-  sc.slots.ensure(per * (sizeof(SlotRec) + 2 * sizeof(int)));
+  // contact slots: one per hand point per solve (sim.hpp:155); a multi-step
+  // protocol keeps every step's slots (nslot <= ncorr + T overall)
+  const int T = S.steps;
+  const size_t ss = T > 1 ? std::max<size_t>(h->N, static_cast<size_t>(c->cap_corr) + T) : h->N;
+  const size_t steps_bytes = T > 1 ? nws * T * sizeof(StepRec) + 256 : 0;
+  sc.slots.ensure(nws * ss * (sizeof(SlotRec) + sizeof(int)) + per * sizeof(int) + steps_bytes + 256);
   buf.corr = static_cast<CorrRec*>(sc.corr.p);
   buf.slots = static_cast<SlotRec*>(sc.slots.p);
-  buf.slot_of_point = reinterpret_cast<int*>(buf.slots + per);
+  buf.slot_of_point = reinterpret_cast<int*>(buf.slots + nws * ss);
   buf.fric_order = buf.slot_of_point + per;
-  buf.slot_stride = h->N;
+  buf.slot_stride = static_cast<int>(ss);
+  buf.steps = T > 1 ? reinterpret_cast<StepRec*>((reinterpret_cast<uintptr_t>(buf.fric_order + nws * ss) + 255) &
+                                                 ~static_cast<uintptr_t>(255))
+                    : nullptr;
   buf.fwd = nullptr;
   buf.fk = nullptr;
   sc.ftg.ensure(nws * (6 * static_cast<size_t>(h->L) + static_cast<size_t>(c->cap_corr) * kCorrMatDoubles) *
@@ -238,7 +244,8 @@ int prepare(dgx_ctx* c, Scratch& sc, const dgx_hand* h, const dgx_object* o, KSi
   if (o->kind == DGX_SDF_MESH) {
     // per point-sweep (face, sign) of the forward, read by the adjoint; per
     // point nearest-face certificates (4 doubles + 1 + kCertFaces ints)
-    const size_t b_cache = (per * static_cast<size_t>(std::max(S.gs, 1)) * sizeof(int) + 255) & ~size_t(255);
+    const size_t b_cache =
+        (per * static_cast<size_t>(std::max(S.gs, 1)) * static_cast<size_t>(T) * sizeof(int) + 255) & ~size_t(255);
     const size_t b_cert = (per * 4 * sizeof(double) + 255) & ~size_t(255);
     sc.mcache.ensure(b_cache + b_cert + per * (kCertFaces + 1) * sizeof(int));
     char* base = static_cast<char*>(sc.mcache.p);
@@ -428,7 +435,8 @@ void launch_range(dgx_ctx* c, Scratch& sc, const dgx_hand* h, const dgx_object* 
   // Large hands (forward shared memory with the points > kSplitMaxFwdSmem,
   // N >~ 3000) run the forward with its points in global memory (L1 / L2)
   // so it keeps two CTAs per SM (fwd_kernel<Sdf, true>).
-  const bool split = use_split(o) && B > c->num_sms && !(mode == kModeOpt && P.k_end == P.k_begin);
+  const bool split = use_split(o) && B > c->num_sms && !(mode == kModeOpt && P.k_end == P.k_begin) &&
+                     S.steps == 1;  // multi-step protocols run the fused kernel
   S.pts_global = SmemLayout(N, h->L, M, 0).total > kSplitMaxFwdSmem ? 1 : 0;
   // grasp-energy terms (optimizer only): their weighted gradient depends on
   // the iterate's q, so it is computed per iterate right before the

@@ -79,6 +79,16 @@ struct FwdRec {
   int ncorr, nslot, nfric, touched, status, pad;
 };
 
+// Per (warp slot, step) record of a multi-step perturbation sim
+// (StabilityProtocol::steps > 1): the step's handover plus its prev / pred
+// states and log offsets, for the reverse over the steps.
+struct StepRec {
+  FwdRec rec;
+  double prev[13];  // x 3, q 4, xdot 3, thetadot 3
+  double pred[13];
+  int c_off, s_off, f_off, pad;
+};
+
 struct KHand {
   int L, J, N;
   const int* topo;
@@ -140,6 +150,7 @@ struct KBuf {
   double* task_res;     // [B, M]
   int* task_stat;       // [B, M]
   int* task_done;       // [B]
+  StepRec* steps;       // [grid, W, T] multi-step sims (fused kernel, T > 1)
   CorrRec* corr;        // [grid, M, cap_corr]
   SlotRec* slots;       // [grid, M, N]  contact slots (one per hand point at most)
   int* slot_of_point;   // [grid, M, N]

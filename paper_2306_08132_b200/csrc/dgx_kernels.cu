@@ -296,7 +296,8 @@ __device__ __forceinline__ bool friction_fwd(const SimEnv& e, V3 prev_x, Q4 prev
 // Reverse of friction_fwd for one applied slot; aX/aQ: adjoints of the state
 // after it (in) and before it (out). Accumulates the slot's a_lam / a_n.
 __device__ __forceinline__ void friction_adj(const SimEnv& e, V3 prev_x, Q4 prev_q, const SlotRec& s, V3& aX, Q4& aQ,
-                                             double& a_lam_slot, V3& a_n_slot) {
+                                             double& a_lam_slot, V3& a_n_slot, V3* a_prev_x = nullptr,
+                                             Q4* a_prev_q = nullptr) {
   V3 rb{s.rb[0], s.rb[1], s.rb[2]};
   V3 n{s.n[0], s.n[1], s.n[2]};
   V3 fx{s.fx[0], s.fx[1], s.fx[2]};
@@ -350,6 +351,11 @@ __device__ __forceinline__ void friction_adj(const SimEnv& e, V3 prev_x, Q4 prev
   a_arm = a_arm + a_u;
   Q4 r = rotate_adj_q(fq, rb, a_arm);
   aQ = qadd(aQ_in, r);
+  if (a_prev_x) {  // before = prev.x + rotate(prev.theta, r_body) (sim.hpp:250): a_before = -a_u
+    const V3 ab = a_u * -1.0;
+    *a_prev_x = *a_prev_x + ab;
+    *a_prev_q = qadd(*a_prev_q, rotate_adj_q(prev_q, rb, ab));
+  }
 }
 
 // Warp-wide all-reduce of a per-lane 3x3 accumulator.
@@ -824,17 +830,38 @@ __device__ __forceinline__ void correction_matrices(const SimEnv& e, int ncorr, 
 // in the same warp; kPhaseFwd runs the forward only and stores the state the
 // adjoint needs in *rec (its logs stay in the per-(candidate, sim) scratch);
 // kPhaseAdj skips the forward, reloads *rec and runs the adjoint.
-template <int Phase, class Sdf>
+// One step of a StabilityProtocol with steps > 1 (losses.hpp:54-55): the
+// state before the step (prev) and after predict (pred), set by run_sim_steps;
+// the forward returns the state after the step, the adjoint takes the adjoint
+// of that state and returns the adjoints of pred and of prev's pose (friction's
+// "before" point and finalize read prev, sim.hpp:250, 284-285).
+struct StepCtx {
+  V3 prev_x, prev_xd, prev_w, pred_x, pred_xd, pred_w;
+  Q4 prev_q, pred_q;
+  // forward out: state after the step, its log sizes
+  V3 out_x, out_xd, out_w;
+  Q4 out_q;
+  int out_ncorr, out_nslot, out_nfric;
+  // adjoint in: adjoint of the state after the step
+  V3 aX_out, aXd_out, aW_out;
+  Q4 aQ_out;
+  // adjoint out
+  V3 a_pred_x, a_pred_xd, a_pred_w, a_prev_x;
+  Q4 a_pred_q, a_prev_q;
+};
+
+template <int Phase, class Sdf, bool Multi = false>
 __device__ double run_sim(const Sdf& sdf, SimEnv& e, V3 v_m, bool record, bool measure_residual, SimStats& st,
-                          int& status, FtAcc& acc, FwdRec* rec) {
+                          int& status, FtAcc& acc, FwdRec* rec, StepCtx* sc = nullptr) {
   const int lane = e.lane, N = e.N;
   // canonical_state (rigid.hpp:29-33) with xdot = v_m; predict (sim.hpp:74-83)
-  const V3 prev_x = e.O->com;
-  const Q4 prev_q{1.0, 0.0, 0.0, 0.0};
-  const V3 prev_thd{0.0, 0.0, 0.0};
-  const V3 pred_xdot = v_m + V3{0.0 * e.dt, 0.0 * e.dt, 0.0 * e.dt};
-  const V3 pred_x = prev_x + pred_xdot * e.dt;
-  const Q4 pred_q = qnormalized(qmul(quat_exp(prev_thd * e.dt), prev_q));
+  // (Multi: the step's prev / pred states from run_sim_steps)
+  const V3 prev_x = Multi ? sc->prev_x : e.O->com;
+  const Q4 prev_q = Multi ? sc->prev_q : Q4{1.0, 0.0, 0.0, 0.0};
+  const V3 prev_thd = Multi ? sc->prev_w : V3{0.0, 0.0, 0.0};
+  const V3 pred_xdot = Multi ? sc->pred_xd : v_m + V3{0.0 * e.dt, 0.0 * e.dt, 0.0 * e.dt};
+  const V3 pred_x = Multi ? sc->pred_x : prev_x + pred_xdot * e.dt;
+  const Q4 pred_q = Multi ? sc->pred_q : qnormalized(qmul(quat_exp(prev_thd * e.dt), prev_q));
   // world_inertia_inv at the predicted orientation (sim.hpp:96-100, 142) is
   // KObj::Iw, evaluated once on the host with the same formula (the canonical
   // state has thetadot = 0, so every perturbation predicts the same pose)
@@ -1037,7 +1064,17 @@ __device__ double run_sim(const Sdf& sdf, SimEnv& e, V3 v_m, bool record, bool m
       double rho = qq.rho - e.radius;
       if (rho < 0.0) mp = mp < -rho ? -rho : mp;
     }
-    st.max_pen = warp_max(mp);
+    const double wm = warp_max(mp);
+    st.max_pen = Multi ? (st.max_pen < wm ? wm : st.max_pen) : wm;  // one SolveStats over the steps
+  }
+  if constexpr (Multi && Phase == kPhaseFwd) {
+    sc->out_x = x;
+    sc->out_q = q;
+    sc->out_xd = xdot;
+    sc->out_w = thd;
+    sc->out_ncorr = ncorr;
+    sc->out_nslot = nslot;
+    sc->out_nfric = nfric;
   }
   if constexpr (Phase == kPhaseFwd) {  // the adjoint kernel resumes from here
     if (lane == 0) {
@@ -1050,17 +1087,47 @@ __device__ double run_sim(const Sdf& sdf, SimEnv& e, V3 v_m, bool record, bool m
     }
     return residual;
   }
-  if (!record || !touched) return residual;  // untouched: constant loss, zero gradient
+  V3 aX;
+  Q4 aQ;
+  if constexpr (Multi) {
+    // finalize (sim.hpp:276-287) reverse with the adjoint of the step's output
+    sc->a_pred_xd = V3{0.0, 0.0, 0.0};
+    sc->a_pred_w = V3{0.0, 0.0, 0.0};
+    sc->a_prev_x = V3{0.0, 0.0, 0.0};
+    sc->a_prev_q = Q4{0.0, 0.0, 0.0, 0.0};
+    aX = sc->aX_out;
+    aQ = sc->aQ_out;
+    if (!touched) {  // xdot / thetadot pass through from predict; x / q carry only the leak
+      sc->a_pred_xd = sc->aXd_out;
+      sc->a_pred_w = sc->aW_out;
+    } else {
+      const Q4 a_qd = quat_log_adj(qd, sc->aW_out * inv_dt);
+      aQ = qadd(aQ, qmul_adj_a(a_qd, qconj(prev_q)));
+      const Q4 ac = qmul_adj_b(a_qd, q);
+      sc->a_prev_q = Q4{ac.w, -ac.x, -ac.y, -ac.z};
+      aX = aX + sc->aXd_out * inv_dt;
+      sc->a_prev_x = sc->aXd_out * -inv_dt;
+    }
+    const bool zero = aX.x == 0.0 && aX.y == 0.0 && aX.z == 0.0 && aQ.w == 0.0 && aQ.x == 0.0 && aQ.y == 0.0 &&
+                      aQ.z == 0.0;
+    sc->a_pred_x = aX;
+    sc->a_pred_q = aQ;
+    if (!record || zero) return residual;  // the tape skips zero adjoints (tape.cpp:33)
+  } else {
+    if (!record || !touched) return residual;  // untouched: constant loss, zero gradient
+  }
   PROF_CNT(32, 1);
   PROF_CNT(36, ncorr);
 
   for (int t = lane; t < 6 * e.L; t += 32) e.gft[t] = 0.0;
   __syncwarp();
   // ---- adjoint: residual -> finalize ---------------------------------------
-  const V3 a_xdot = n1 > 0.0 ? xdot / n1 : V3{0.0, 0.0, 0.0};
-  const V3 a_thd = n2 > 0.0 ? thd / n2 : V3{0.0, 0.0, 0.0};
-  Q4 aQ = qmul_adj_a(quat_log_adj(qd, a_thd * inv_dt), qconj(prev_q));
-  V3 aX = a_xdot * inv_dt;
+  if constexpr (!Multi) {
+    const V3 a_xdot = n1 > 0.0 ? xdot / n1 : V3{0.0, 0.0, 0.0};
+    const V3 a_thd = n2 > 0.0 ? thd / n2 : V3{0.0, 0.0, 0.0};
+    aQ = qmul_adj_a(quat_log_adj(qd, a_thd * inv_dt), qconj(prev_q));
+    aX = a_xdot * inv_dt;
+  }
 
   PROF_T(tfa);
   // ---- friction, reverse --------------------------------------------------
@@ -1075,13 +1142,14 @@ __device__ double run_sim(const Sdf& sdf, SimEnv& e, V3 v_m, bool record, bool m
     const int nb_max = min(32, (e.seg_max * 5 * 32) / kFr);
     int hi = nfric;
     while (hi > 0) {
-      const int cnt = nb_max >= 2 ? min(nb_max, hi) : 1;
-      if (cnt == 1) {  // serial reverse step (short tails / tiny staging)
+      const int cnt = (!Multi && nb_max >= 2) ? min(nb_max, hi) : 1;
+      if (cnt == 1) {  // serial reverse step (short tails / tiny staging; Multi: with prev's adjoint)
         const int slot = e.fric_order[hi - 1];
         SlotRec s = e.slots[slot];
         double a_lam = s.a_lam;
         V3 a_n{s.a_n[0], s.a_n[1], s.a_n[2]};
-        friction_adj(e, prev_x, prev_q, s, aX, aQ, a_lam, a_n);
+        friction_adj(e, prev_x, prev_q, s, aX, aQ, a_lam, a_n, Multi ? &sc->a_prev_x : nullptr,
+                     Multi ? &sc->a_prev_q : nullptr);
         __syncwarp();
         if (lane == 0) {
           SlotRec& sw = e.slots[slot];
@@ -1258,6 +1326,10 @@ __device__ double run_sim(const Sdf& sdf, SimEnv& e, V3 v_m, bool record, bool m
     hi = e.corr[k].f;
     --k;
   }
+  if constexpr (Multi) {  // the sweeps started from pred (st = predicted, sim.hpp:144)
+    sc->a_pred_x = aX;
+    sc->a_pred_q = aQ;
+  }
   // fold the global spill buffer into the warp's shared link sums
   PROF_T(tf);
   acc.spill_if_any(e.gft);
@@ -1266,6 +1338,112 @@ __device__ double run_sim(const Sdf& sdf, SimEnv& e, V3 v_m, bool record, bool m
   for (int t = lane; t < 6 * e.L; t += 32) e.ft[t] += __ldcg(e.gft + t);
   __syncwarp();
   PROF_ACC(10, tf);
+  return residual;
+}
+
+
+__device__ __forceinline__ void put3(double* d, V3 v) { d[0] = v.x; d[1] = v.y; d[2] = v.z; }
+__device__ __forceinline__ void put4(double* d, Q4 v) { d[0] = v.w; d[1] = v.x; d[2] = v.y; d[3] = v.z; }
+__device__ __forceinline__ V3 get3(const double* d) { return V3{d[0], d[1], d[2]}; }
+__device__ __forceinline__ Q4 get4(const double* d) { return Q4{d[0], d[1], d[2], d[3]}; }
+
+// perturbation_residual with StabilityProtocol::steps = T > 1 (losses.hpp:47-57):
+// T steps of predict + solve (sim.hpp:310-316) from the canonical state, the
+// residual of the last, and (record) the reverse over the steps: each step's
+// adjoint (run_sim<kPhaseAdj, Multi>) followed by predict's reverse
+// (sim.hpp:74-83: pred.x = x + dt pred.xdot, pred.theta = normalized(
+// quat_exp(dt thetadot) (x) theta)). The world inverse inertia is frozen per
+// step at its predicted orientation (sim.hpp:142). Logs of all T solves are
+// kept (corrections / slots / frictions at per-step offsets); link sums
+// accumulate over the steps (the hand points are shared).
+template <class Sdf>
+__device__ double run_sim_steps(const Sdf& sdf, SimEnv& e, V3 v_m, bool record, bool meas, SimStats& st,
+                                int& status, FtAcc& acc, StepRec* steps, int T) {
+  const int lane = e.lane;
+  CorrRec* corr0 = e.corr;
+  SlotRec* slots0 = e.slots;
+  int* fo0 = e.fric_order;
+  int* mc0 = e.mcache;
+  const int cap0 = e.cap_corr;
+  const KObj* O0 = e.O;
+  KObj Ot = *O0;  // Iw at each step's predicted orientation
+  e.O = &Ot;
+  auto bind_step = [&](int c_off, int s_off, int f_off, int t) {
+    e.corr = corr0 + c_off;
+    e.slots = slots0 + s_off;
+    e.fric_order = fo0 + f_off;
+    e.cap_corr = cap0 - c_off;
+    if (mc0) e.mcache = mc0 + static_cast<size_t>(t) * e.gs * e.N;
+  };
+  auto set_iw = [&](Q4 pq) {
+    const M3 Rp = rotation_matrix(pq);
+    Ot.Iw = mul(mul(Rp, O0->inertia_body_inv), transposed(Rp));  // sim.hpp:96-100
+  };
+  V3 x = O0->com, xd = v_m, w{0.0, 0.0, 0.0};  // canonical_state with xdot = v (losses.hpp:52-53)
+  Q4 q{1.0, 0.0, 0.0, 0.0};
+  int c_off = 0, s_off = 0, f_off = 0;
+  double residual = 0.0;
+  for (int t = 0; t < T; ++t) {
+    StepCtx sc;
+    sc.prev_x = x; sc.prev_q = q; sc.prev_xd = xd; sc.prev_w = w;
+    sc.pred_xd = xd + V3{0.0 * e.dt, 0.0 * e.dt, 0.0 * e.dt};  // gravity zeroed (losses.hpp:51)
+    sc.pred_x = x + sc.pred_xd * e.dt;
+    sc.pred_q = qnormalized(qmul(quat_exp(w * e.dt), q));
+    sc.pred_w = w;
+    set_iw(sc.pred_q);
+    bind_step(c_off, s_off, f_off, t);
+    StepRec& sr = steps[t];
+    residual = run_sim<kPhaseFwd, Sdf, true>(sdf, e, v_m, record, meas, st, status, acc, &sr.rec, &sc);
+    if (lane == 0) {
+      sr.rec.status = status;
+      sr.rec.residual = residual;
+      put3(sr.prev, x); put4(sr.prev + 3, q); put3(sr.prev + 7, xd); put3(sr.prev + 10, w);
+      put3(sr.pred, sc.pred_x); put4(sr.pred + 3, sc.pred_q); put3(sr.pred + 7, sc.pred_xd); put3(sr.pred + 10, sc.pred_w);
+      sr.c_off = c_off; sr.s_off = s_off; sr.f_off = f_off;
+    }
+    __syncwarp();
+    if (status != kOk) {
+      e.O = O0;
+      return residual;
+    }
+    c_off += sc.out_ncorr;
+    s_off += sc.out_nslot;
+    f_off += sc.out_nfric;
+    x = sc.out_x; q = sc.out_q; xd = sc.out_xd; w = sc.out_w;
+  }
+  if (record) {
+    const double n1 = norm(xd), n2 = norm(w);
+    V3 aX{0.0, 0.0, 0.0}, aXd = n1 > 0.0 ? xd / n1 : V3{0.0, 0.0, 0.0}, aW = n2 > 0.0 ? w / n2 : V3{0.0, 0.0, 0.0};
+    Q4 aQ{0.0, 0.0, 0.0, 0.0};
+    for (int t = T - 1; t >= 0; --t) {
+      const StepRec& sr = steps[t];
+      StepCtx sc;
+      sc.prev_x = get3(sr.prev); sc.prev_q = get4(sr.prev + 3); sc.prev_xd = get3(sr.prev + 7); sc.prev_w = get3(sr.prev + 10);
+      sc.pred_x = get3(sr.pred); sc.pred_q = get4(sr.pred + 3); sc.pred_xd = get3(sr.pred + 7); sc.pred_w = get3(sr.pred + 10);
+      sc.aX_out = aX; sc.aQ_out = aQ; sc.aXd_out = aXd; sc.aW_out = aW;
+      set_iw(sc.pred_q);
+      bind_step(sr.c_off, sr.s_off, sr.f_off, t);
+      SimStats st2;
+      int s2 = kOk;
+      run_sim<kPhaseAdj, Sdf, true>(sdf, e, v_m, true, false, st2, s2, acc, const_cast<FwdRec*>(&sr.rec), &sc);
+      if (s2 != kOk) status = s2;
+      // predict, reverse (sim.hpp:74-83)
+      aXd = fma3(e.dt, sc.a_pred_x, sc.a_pred_xd);
+      aX = sc.a_pred_x + sc.a_prev_x;
+      double sh;
+      const Q4 E = quat_exp_sin(sc.prev_w * e.dt, sh);
+      const Q4 aP = qnormalize_adj(qmul(E, sc.prev_q), sc.a_pred_q);
+      aQ = qadd(qmul_adj_b(aP, E), sc.a_prev_q);
+      const V3 aom = quat_exp_adj_sc(sc.prev_w * e.dt, qmul_adj_a(aP, sc.prev_q), sh, E.w);
+      aW = fma3(e.dt, aom, sc.a_pred_w);
+    }
+  }
+  e.O = O0;
+  e.corr = corr0;
+  e.slots = slots0;
+  e.fric_order = fo0;
+  e.cap_corr = cap0;
+  e.mcache = mc0;
   return residual;
 }
 
@@ -1551,7 +1729,7 @@ __device__ __forceinline__ void candidate_epilogue(const KHand& H, const KSim& S
 // PtsG (split forward only): the world points live in the candidate's global
 // FK record (buf.fk, read through L1 / L2) instead of shared memory, for hands
 // whose 24 N bytes of points would cap the forward at one CTA per SM.
-template <class Sdf, int Phase, bool PtsG = false>
+template <class Sdf, int Phase, bool PtsG = false, bool Multi = false>
 __device__ __forceinline__ void kernel_body(const KHand& H, const KObj& O, const Sdf& sdf, const KSim& S,
                                             const KOpt& P, const KBuf& buf, int mode) {
   extern __shared__ __align__(16) unsigned char smem[];
@@ -1607,7 +1785,7 @@ __device__ __forceinline__ void kernel_body(const KHand& H, const KObj& O, const
   e.dt = S.dt;
   e.point_grads = nullptr;
   e.fold = S.fold;
-  e.mcache = buf.mesh_cache ? buf.mesh_cache + wslot * static_cast<size_t>(S.gs) * N : nullptr;
+  e.mcache = buf.mesh_cache ? buf.mesh_cache + wslot * static_cast<size_t>(S.gs) * N * S.steps : nullptr;
   e.mcert = buf.mesh_cert ? buf.mesh_cert + wslot * 4 * static_cast<size_t>(N) : nullptr;
   e.mcf = buf.mesh_cf ? buf.mesh_cf + wslot * static_cast<size_t>(kCertFaces + 1) * N : nullptr;
 
@@ -1692,7 +1870,12 @@ __device__ __forceinline__ void kernel_body(const KHand& H, const KObj& O, const
         const bool meas = mode == kModeEval && S.measure_residual;
         PROF_T(tsim);
         FwdRec* rec = Phase != kPhaseFused ? buf.fwd + static_cast<size_t>(b) * M + m : nullptr;
-        const double res = run_sim<Phase>(sdf, e, vm, record, meas, st, status, acc, rec);
+        double res;
+        if constexpr (Multi)  // StabilityProtocol::steps > 1 (fused kernel only)
+          res = run_sim_steps(sdf, e, vm, record, meas, st, status, acc,
+                              buf.steps + wslot * static_cast<size_t>(S.steps), S.steps);
+        else
+          res = run_sim<Phase>(sdf, e, vm, record, meas, st, status, acc, rec);
         PROF_ACC(12, tsim);
         if constexpr (Phase == kPhaseFwd) {
           if (lane == 0) {
@@ -1759,10 +1942,10 @@ __device__ __forceinline__ void kernel_body(const KHand& H, const KObj& O, const
 
 
 // fused / adjoint instances: the register budget follows CTAs per SM
-template <class Sdf, int Occ = CtasPerSm<Sdf>::value, int Phase = kPhaseFused>
+template <class Sdf, int Occ = CtasPerSm<Sdf>::value, int Phase = kPhaseFused, bool Multi = false>
 __global__ void __launch_bounds__(224, Occ) fused_kernel(KHand H, const __grid_constant__ KObj O, Sdf sdf, KSim S,
                                                          KOpt P, KBuf buf, int mode) {
-  kernel_body<Sdf, Phase>(H, O, sdf, S, P, buf, mode);
+  kernel_body<Sdf, Phase, false, Multi>(H, O, sdf, S, P, buf, mode);
 }
 
 // forward instance of split execution: kFwdCtasPerSm CTAs per SM. The
@@ -2352,6 +2535,17 @@ static cudaError_t launch_fused_t(const KHand& H, const KObj& O, const Sdf& sdf,
     }
   }
   if (phase != kPhaseFused) return cudaErrorInvalidValue;
+  if (S.steps > 1) {  // multi-step protocol instance
+    static bool configured = false;
+    if (!configured) {
+      if ((e = cudaFuncSetAttribute(fused_kernel<Sdf, occ, kPhaseFused, true>,
+                                    cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024)) != cudaSuccess)
+        return e;
+      configured = true;
+    }
+    fused_kernel<Sdf, occ, kPhaseFused, true><<<grid, 32 * S.warps(), smem, st>>>(H, O, sdf, S, P, buf, mode);
+    return cudaGetLastError();
+  }
   if ((e = allow_smem<Sdf, occ, kPhaseFused>()) != cudaSuccess) return e;
   fused_kernel<Sdf, occ, kPhaseFused><<<grid, 32 * S.warps(), smem, st>>>(H, O, sdf, S, P, buf, mode);
   return cudaGetLastError();

@@ -229,8 +229,8 @@ def test_invalid_arguments(ctx, oracle):
         api.loss_gradient(ctx, c.obj, c.hand, c.q, api.StabilityProtocol.standard(),
                           api.SimParams(dilation_radius=-0.1))
     with pytest.raises(capi.DgxError) as e:
-        api.loss_gradient(ctx, c.obj, c.hand, c.q, api.StabilityProtocol.standard(steps=2), api.SimParams())
-    assert e.value.code == 102
+        api.loss_gradient(ctx, c.obj, c.hand, c.q, api.StabilityProtocol.standard(steps=0), api.SimParams())
+    assert e.value.code == 100
     # NaN configuration: like the reference, every SDF gate sees NaN (inactive),
     # the sim is untouched, the loss is the free-flight constant, gradient 0
     bad = c.q.copy()

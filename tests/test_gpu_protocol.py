@@ -66,3 +66,56 @@ def test_protocol_optimizer_m9(ctx, oracle):
     assert np.array_equal(out["traj"][rows, :, :3], r["losses"])
     assert relerr(out["traj"][rows, :, 3:], r["grads"]) < GRAD_RTOL
     assert relerr(out["q"][rows], r["q"]) < GRAD_RTOL
+
+
+@pytest.mark.parametrize("T", [2, 3])
+@pytest.mark.parametrize("hand_name,obj_name,B", [("barrett3", "sphere25", 2), ("allegro16", "boxgrid64", 160),
+                                                  ("barrett3", "ico25", 2), ("pincher2", "box40", 2)])
+def test_protocol_steps(ctx, oracle, T, hand_name, obj_name, B):
+    """StabilityProtocol::steps = T > 1 (losses.hpp:54-55): T predict + solve
+    steps per perturbation sim, the reverse through every step's solve, its
+    friction's and finalize's dependence on the previous state, and predict
+    (quat_exp of the carried angular velocity). Residuals / losses / stats
+    bit-exact, gradients within GRAD_RTOL of the reference tape."""
+    from paper_2306_08132_b200 import api
+    c = Case(ctx, oracle, hand_name, obj_name, B=B, seed=29 + T)
+    proto = api.StabilityProtocol.standard(steps=T)
+    params = api.SimParams(dilation_radius=0.015)
+    p = oracle.default_params(dilation_radius=0.015, steps=T)
+    losses, grads, st = api.loss_gradient(ctx, c.obj, c.hand, c.q, proto, params)
+    el, stats, st2 = api.evaluate_losses(ctx, c.obj, c.hand, c.q, proto, params)
+    rows = [0, 1] if B == 2 else [0, 99, 159]
+    res, g, _, st3 = api.debug_sims(ctx, c.obj, c.hand, c.q[rows], proto, params)
+    assert not np.any(st) and not np.any(st2) and not np.any(st3)
+    active = 0
+    for i, b in enumerate(rows):
+        rl, ds, dr, dl = oracle.loss_gradient(c.ro, c.rh, c.q[b], p)
+        assert np.array_equal(losses[b], rl), (b, losses[b], rl)
+        assert relerr(grads[b, 0], ds) < GRAD_RTOL, (b, relerr(grads[b, 0], ds))
+        assert np.array_equal(el[b], oracle.evaluate_losses(c.ro, c.rh, c.q[b], p))
+        for m in range(7):
+            rres, rg, _, log = oracle.sim_record(c.ro, c.rh, c.q[b], m, p)
+            active += int(np.sum(log < 0))
+            assert res[i, m] == rres, (b, m)
+            assert relerr(g[i, m], rg) < GRAD_RTOL, (b, m, relerr(g[i, m], rg))
+            _, rst, _ = oracle.sim_forward(c.ro, c.rh, c.q[b], m, p)
+            assert np.array_equal(stats[b, m], rst), (b, m, stats[b, m], rst)
+    assert active > 0
+
+
+def test_protocol_steps_optimizer(ctx, oracle):
+    """Teacher-forced optimizer steps with T = 2."""
+    from paper_2306_08132_b200 import api
+    c = Case(ctx, oracle, "allegro16", "boxgrid64", B=3, seed=8, pull=0.3)
+    q, m, v = c.q, None, None
+    for k in range(2):
+        g = api.optimize(ctx, c.obj, c.hand, q, api.StabilityProtocol.standard(steps=2), api.SimParams(),
+                         api.LossWeights(), api.OptConfig(iterations=6), k_begin=k, k_end=k + 1, adam_m=m, adam_v=v,
+                         record=True)
+        r = oracle.optimize(c.ro, c.rh, q, oracle.default_params(steps=2), iters=6, k_begin=k, k_end=k + 1, adam_m=m,
+                            adam_v=v, record=True)
+        assert not np.any(g["status"]) and not np.any(r["status"])
+        assert np.array_equal(g["traj"][:, :, :3], r["losses"])
+        assert relerr(g["traj"][:, :, 3:], r["grads"]) < GRAD_RTOL
+        assert relerr(g["q"], r["q"]) < GRAD_RTOL
+        q, m, v = r["q"], r["m"], r["v"]

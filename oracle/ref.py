@@ -97,6 +97,7 @@ def lib(variant: str = "sm") -> C.CDLL:
     L.dgr_drop.argtypes = [vp, _dp, C.c_double, C.c_double, C.c_int, _dp, C.c_int, C.c_int, C.c_double, C.c_int,
                            _dp, _ip, _dp, _dp, _dp, C.c_int, C.c_int]
     L.dgr_set_protocol.argtypes = [C.c_int, _dp]
+    L.dgr_debug_step_adjoint.argtypes = [vp, vp, _dp, C.c_int, C.POINTER(Params), _dp]
     L.dgr_object_use_sphere.argtypes = [vp, C.c_double, C.c_double, C.c_double, C.c_double]
     L.dgr_object_use_box.argtypes = [vp, _dp, _dp]
     L.dgr_object_use_grid.argtypes = [vp, _ip, _dp, C.c_double, C.c_double, _fp]

@@ -501,6 +501,48 @@ int dgr_apply_gradient_step(void* hp, const double* q, const double* g, double l
 // One recorded perturbation sim (losses.cpp:32-42): residual, its tape
 // gradient (6+J), optional d residual / d p_i (points as tape inputs, N*3),
 // and the rho_d of every SDF call in call order (sweep-major, point-minor).
+// debug (multi-step protocols): d residual / d (state after step 1) of a
+// two-step perturbation sim, the reference tape with the step-1 state
+// re-registered as 13 inputs (x 3, theta w,x,y,z 4, xdot 3, thetadot 3)
+int dgr_debug_step_adjoint(void* o, void* hp, const double* q, int m, const Params* p, double* out) {
+  try {
+    auto* h = static_cast<HandModel*>(hp);
+    const auto& obj = *static_cast<GraspObject*>(o);
+    StabilityProtocol proto = protocol(*p);
+    SimParams sim = sim_params(*p);
+    sim.gravity = Vec3{};
+    HandConfig cfg = unpack_q(*h, q);
+    std::vector<Vec3> pts = h->forward(cfg);
+    // step 1 on values
+    BodyStateT<double> s0 = to_body_state<double>(canonical_state(obj.inertial));
+    s0.xdot = proto.velocities[m];
+    BodyStateT<double> s1 = step(s0, pts, obj.sdf, obj.inertial, sim);
+    Tape tape;
+    Tape::Scope scope(tape);
+    std::vector<Vec3T<Rec>> rp;
+    for (const Vec3& v : pts) rp.push_back({Rec(v.x), Rec(v.y), Rec(v.z)});
+    BodyStateT<Rec> r1;
+    r1.x = {tape.input(s1.x.x), tape.input(s1.x.y), tape.input(s1.x.z)};
+    r1.theta = {tape.input(s1.theta.w), tape.input(s1.theta.x), tape.input(s1.theta.y), tape.input(s1.theta.z)};
+    r1.xdot = {tape.input(s1.xdot.x), tape.input(s1.xdot.y), tape.input(s1.xdot.z)};
+    r1.thetadot = {tape.input(s1.thetadot.x), tape.input(s1.thetadot.y), tape.input(s1.thetadot.z)};
+    BodyStateT<double> pd = predict(s1, sim);
+    BodyStateT<Rec> rpd;  // the predicted state as separate inputs (13 more)
+    rpd.x = {tape.input(pd.x.x), tape.input(pd.x.y), tape.input(pd.x.z)};
+    rpd.theta = {tape.input(pd.theta.w), tape.input(pd.theta.x), tape.input(pd.theta.y), tape.input(pd.theta.z)};
+    rpd.xdot = {tape.input(pd.xdot.x), tape.input(pd.xdot.y), tape.input(pd.xdot.z)};
+    rpd.thetadot = {tape.input(pd.thetadot.x), tape.input(pd.thetadot.y), tape.input(pd.thetadot.z)};
+    BodyStateT<Rec> r2 = solve_contacts(r1, rpd, rp, obj.sdf, obj.inertial, sim);
+    Rec res = norm(r2.xdot) + norm(r2.thetadot);
+    tape.set_output(res);
+    std::vector<double> g = tape.gradient();
+    std::copy(g.begin(), g.begin() + 26, out);  // d/d prev (13), d/d pred (13)
+    return 0;
+  } catch (const std::exception& e) {
+    return fail(e);
+  }
+}
+
 int dgr_sim_record(void* o, void* hp, const double* q, int m, const Params* p, double* residual,
                    double* grad, double* grad_points, double* rho_log, int rho_cap, int* n_calls) {
   try {

@@ -1327,6 +1327,9 @@ __device__ double run_sim(const Sdf& sdf, SimEnv& e, V3 v_m, bool record, bool m
     --k;
   }
   if constexpr (Multi) {  // the sweeps started from pred (st = predicted, sim.hpp:144)
+    // the solve's first R node, rotation_matrix(pred.theta) (sim.hpp:145), read
+    // by the run before the first correction (a constant when T = 1)
+    aQ = qadd(aQ, rotmat_adj(pred_q, warp_sum(aR)));
     sc->a_pred_x = aX;
     sc->a_pred_q = aQ;
   }

@@ -225,6 +225,11 @@ int dgx_evaluate_losses_batch(dgx_ctx* ctx, const dgx_hand* hand, const dgx_obje
 int dgx_apply_gradient_step_batch(dgx_ctx* ctx, const dgx_hand* hand, int32_t B, const double* q,
                                   const double* g, double lr, double* q_out, uint32_t flags);
 
+/* the same without a hand handle (dg::apply_gradient_step takes no hand,
+   losses.hpp:136): num_joints = J of the configurations */
+int dgx_apply_gradient_step_joints(dgx_ctx* ctx, int32_t num_joints, int32_t B, const double* q, const double* g,
+                                   double lr, double* q_out, uint32_t flags);
+
 /* Fused synthesis loop: q [B,7+J], adam_m / adam_v [B,6+J] updated in place;
    traj [B, k_end-k_begin, 3+6+J] (losses, weighted gradient) when opt->record;
    rows of iterates after a candidate's failure are zero. */

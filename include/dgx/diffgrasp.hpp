@@ -11,6 +11,12 @@
 //   dg::apply_gradient_step(q, grad, lr)           losses.hpp:136   -> dgx::apply_gradient_step
 // plus batched overloads over std::span<const dg::HandConfig> and the fused
 // synthesis loop dgx::optimize (the reference has none).
+// The reference's exact signatures (no Runtime / handles: a per-thread
+// runtime and upload cache) are at the end of this header:
+//   dgx::loss_gradient(obj, hand, q, proto, params)   == dg::loss_gradient
+//   dgx::evaluate_losses(obj, hand, q, proto, params) == dg::evaluate_losses
+//   dgx::apply_gradient_step(q, grad, lr)             == dg::apply_gradient_step
+//   dgx::forward(hand, q)                             == hand.forward(q)
 //
 // The object: dgx::Object(rt, const dg::GraspObject&) takes the reference's
 // own object (losses.hpp:38-44) unchanged: its TriMesh (vertices, faces,
@@ -21,7 +27,9 @@
 #pragma once
 
 #include <cstdint>
+#include <cstdlib>
 #include <limits>
+#include <memory>
 #include <optional>
 #include <span>
 #include <stdexcept>
@@ -333,6 +341,124 @@ inline std::vector<dg::HandConfig> optimize(Runtime& rt, const Object& obj, cons
     out.push_back(detail::unpack(q.data() + static_cast<std::size_t>(b) * (7 + J), J));
   }
   return out;
+}
+
+// ---- true drop-in: the reference's own signatures ---------------------------
+// Same argument lists as dg::loss_gradient / dg::evaluate_losses
+// (losses.hpp:119-127), dg::apply_gradient_step (losses.hpp:136) and
+// HandModel::forward (hand.hpp:86): a call site switches namespace
+// (dg:: -> dgx::) and nothing else. The device runtime is per host thread
+// (device DGX_DEVICE, default 0; the reference's tape is per thread too,
+// tape.hpp:124), and uploads are cached per thread keyed on the object's /
+// hand's address plus a content fingerprint, so a destroyed-and-rebuilt
+// object at the same address is uploaded again.
+namespace detail {
+inline Runtime& thread_runtime() {
+  thread_local Runtime rt([] {
+    const char* ev = std::getenv("DGX_DEVICE");
+    return ev ? std::atoi(ev) : 0;
+  }());
+  return rt;
+}
+inline uint64_t fnv(uint64_t h, const void* p, std::size_t n) {
+  const unsigned char* c = static_cast<const unsigned char*>(p);
+  for (std::size_t i = 0; i < n; ++i) h = (h ^ c[i]) * 1099511628211ull;
+  return h;
+}
+inline uint64_t fingerprint(const dg::HandModel& h) {
+  uint64_t f = 1469598103934665603ull;
+  const int ints[3] = {h.num_links(), h.num_joints(), h.total_samples()};
+  f = fnv(f, ints, sizeof ints);
+  for (const auto& l : h.links())
+    if (!l.samples.empty()) f = fnv(f, l.samples.data(), l.samples.size() * sizeof(dg::Vec3));
+  for (const auto& j : h.joints()) {
+    f = fnv(f, &j.axis, sizeof j.axis);
+    f = fnv(f, &j.origin_t, sizeof j.origin_t);
+    f = fnv(f, j.origin_R.m.data(), sizeof(double) * 9);
+    f = fnv(f, &j.lower, sizeof j.lower);
+    f = fnv(f, &j.upper, sizeof j.upper);
+  }
+  return f;
+}
+inline uint64_t fingerprint(const dg::GraspObject& o) {
+  uint64_t f = 1469598103934665603ull;
+  const dg::TriMesh& m = o.sdf.mesh();
+  f = fnv(f, m.vertices.data(), m.vertices.size() * sizeof(dg::Vec3));
+  f = fnv(f, m.faces.data(), m.faces.size() * sizeof(m.faces[0]));
+  const double a = o.sdf.alpha_phong();
+  f = fnv(f, &a, sizeof a);
+  f = fnv(f, &o.inertial.mass, sizeof o.inertial.mass);
+  f = fnv(f, &o.inertial.com, sizeof o.inertial.com);
+  f = fnv(f, o.inertial.inertia_body_inv.m.data(), sizeof(double) * 9);
+  return f;
+}
+template <class Dev, class Src>
+struct UploadCache {
+  struct Entry {
+    const Src* key;
+    uint64_t fp;
+    std::unique_ptr<Dev> dev;
+  };
+  std::vector<Entry> entries;
+  const Dev& get(const Src& s) {
+    const uint64_t fp = fingerprint(s);
+    for (auto& e : entries)
+      if (e.key == &s) {
+        if (e.fp != fp) {
+          e.dev = std::make_unique<Dev>(thread_runtime(), s);
+          e.fp = fp;
+        }
+        return *e.dev;
+      }
+    if (entries.size() >= 64) entries.erase(entries.begin());
+    entries.push_back({&s, fp, std::make_unique<Dev>(thread_runtime(), s)});
+    return *entries.back().dev;
+  }
+};
+inline const Hand& cached(const dg::HandModel& h) {
+  thread_local UploadCache<Hand, dg::HandModel> c;
+  return c.get(h);
+}
+inline const Object& cached(const dg::GraspObject& o) {
+  thread_local UploadCache<Object, dg::GraspObject> c;
+  return c.get(o);
+}
+}  // namespace detail
+
+// dg::loss_gradient (losses.hpp:126-127)
+inline dg::LossGradient loss_gradient(const dg::GraspObject& object, const dg::HandModel& hand,
+                                      const dg::HandConfig& q, const dg::StabilityProtocol& protocol,
+                                      const dg::SimParams& params) {
+  if (static_cast<int>(q.joint_angles.size()) != hand.num_joints())
+    throw std::runtime_error("hand: expected " + std::to_string(hand.num_joints()) + " joint angles, got " +
+                             std::to_string(q.joint_angles.size()));
+  return loss_gradient(detail::thread_runtime(), detail::cached(object), detail::cached(hand), q, protocol, params);
+}
+
+// dg::evaluate_losses (losses.hpp:119-121)
+inline dg::LossBreakdown evaluate_losses(const dg::GraspObject& object, const dg::HandModel& hand,
+                                         const dg::HandConfig& q, const dg::StabilityProtocol& protocol,
+                                         const dg::SimParams& params) {
+  if (static_cast<int>(q.joint_angles.size()) != hand.num_joints())
+    throw std::runtime_error("hand: expected " + std::to_string(hand.num_joints()) + " joint angles, got " +
+                             std::to_string(q.joint_angles.size()));
+  return evaluate_losses(detail::thread_runtime(), detail::cached(object), detail::cached(hand), q, protocol,
+                         params);
+}
+
+// dg::apply_gradient_step (losses.hpp:136; losses.cpp:92-102)
+inline dg::HandConfig apply_gradient_step(const dg::HandConfig& q, const std::vector<double>& grad, double lr) {
+  const int J = static_cast<int>(q.joint_angles.size());
+  if (static_cast<int>(grad.size()) != 6 + J) throw std::runtime_error("gradient size mismatch");
+  std::vector<double> qv = detail::pack(q), out(qv.size());
+  detail::check(dgx_apply_gradient_step_joints(detail::thread_runtime().get(), J, 1, qv.data(), grad.data(), lr,
+                                               out.data(), 0));
+  return detail::unpack(out.data(), J);
+}
+
+// HandModel::forward(const HandConfig&) (hand.hpp:86) as a free function
+inline std::vector<dg::Vec3> forward(const dg::HandModel& hand, const dg::HandConfig& q) {
+  return forward(detail::thread_runtime(), detail::cached(hand), q);
 }
 
 }  // namespace dgx

@@ -68,6 +68,56 @@ int main() {
       EXPECT(aw.has_value() == bw.has_value() && (!aw || aw->rho == bw->rho), "dilated_within differs");
     }
   }
+  // ---- the reference's own signatures, call sites unchanged but for the
+  // namespace (dg:: -> dgx::): standard protocol, T = 2 steps, M = 9 velocities
+  dg::StabilityProtocol t2 = dg::StabilityProtocol::standard(0.5, 2);
+  dg::StabilityProtocol m9 = dg::StabilityProtocol::standard();
+  m9.velocities.push_back({0.3, 0.3, 0.0});
+  m9.velocities.push_back({0.0, 0.2, -0.4});
+  dg::GraspObject cube(dg::make_box(0.04, 0.04, 0.04), 1000.0, 0.75);
+  int nonzero = 0;
+  for (const dg::GraspObject* obj : {&go, &cube, &go}) {  // two objects through the per-thread upload cache
+    for (const dg::StabilityProtocol* pr : {&proto, &t2, &m9}) {
+      dg::SimParams sp;
+      sp.dilation_radius = 0.01;
+      for (std::size_t b = 0; b < qs.size(); ++b) {
+        dg::LossGradient a = dgx::loss_gradient(*obj, hand, qs[b], *pr, sp);
+        dg::LossGradient r = dg::loss_gradient(*obj, hand, qs[b], *pr, sp);
+        EXPECT(a.losses.stable == r.losses.stable && a.losses.qrange == r.losses.qrange &&
+                   a.losses.qlimit == r.losses.qlimit,
+               "ref-signature losses differ (M=%d T=%d b=%zu): %.17g vs %.17g", pr->m(), pr->steps, b,
+               a.losses.stable, r.losses.stable);
+        double mx = 0, err = 0;
+        for (std::size_t i = 0; i < r.d_stable.size(); ++i) {
+          mx = std::fmax(mx, std::fabs(r.d_stable[i]));
+          err = std::fmax(err, std::fabs(a.d_stable[i] - r.d_stable[i]));
+        }
+        EXPECT(err <= 1e-8 * mx, "ref-signature gradient rel err %.3e (M=%d T=%d)", mx > 0 ? err / mx : err, pr->m(),
+               pr->steps);
+        nonzero += mx > 0;
+        dg::LossBreakdown ea = dgx::evaluate_losses(*obj, hand, qs[b], *pr, sp);
+        dg::LossBreakdown er = dg::evaluate_losses(*obj, hand, qs[b], *pr, sp);
+        EXPECT(ea.stable == er.stable && ea.qrange == er.qrange && ea.qlimit == er.qlimit,
+               "ref-signature evaluate_losses differs (M=%d T=%d)", pr->m(), pr->steps);
+      }
+    }
+  }
+  EXPECT(nonzero > 0, "no reference-signature case produced a gradient");
+  {
+    auto g = dg::loss_gradient(go, hand, qs[1], proto, dg::SimParams{}).weighted(dg::LossWeights{});
+    for (double& x : g) x = std::tanh(x);
+    dg::HandConfig a = dgx::apply_gradient_step(qs[1], g, 1e-3);
+    dg::HandConfig r = dg::apply_gradient_step(qs[1], g, 1e-3);
+    EXPECT(a.base_position.x == r.base_position.x && a.base_position.z == r.base_position.z &&
+               a.base_orientation.w == r.base_orientation.w && a.base_orientation.y == r.base_orientation.y &&
+               a.joint_angles == r.joint_angles,
+           "ref-signature apply_gradient_step differs");
+    auto pa = dgx::forward(hand, qs[2]);
+    auto pb = hand.forward(qs[2]);
+    bool same = pa.size() == pb.size();
+    for (std::size_t i = 0; same && i < pa.size(); ++i) same = pa[i].x == pb[i].x && pa[i].y == pb[i].y && pa[i].z == pb[i].z;
+    EXPECT(same, "ref-signature forward differs");
+  }
   if (failures == 0) std::printf("DROPIN MESH OK\n");
   return failures == 0 ? 0 : 1;
 }

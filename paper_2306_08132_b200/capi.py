@@ -87,6 +87,7 @@ EXPORTS = [
     "dgx_evaluate_losses_batch", "dgx_apply_gradient_step_batch", "dgx_optimize_batch", "dgx_debug_sims",
     "dgx_fp64_peak", "dgx_optimize_multi", "dgx_sdf_query_batch", "dgx_mesh_inertia",
     "dgx_mesh_bvh", "dgx_drop_batch", "dgx_contacts_batch", "dgx_grasp_energy_batch",
+    "dgx_apply_gradient_step_joints",
 ]
 
 _lib: C.CDLL | None = None

@@ -1190,16 +1190,27 @@ int dgx_grasp_energy_batch(dgx_ctx* c, const dgx_hand* h, const dgx_object* o, i
 
 int dgx_apply_gradient_step_batch(dgx_ctx* c, const dgx_hand* h, int32_t B, const double* q, const double* g,
                                   double lr, double* q_out, uint32_t flags) {
+  if (!h) {
+    g_err = "NULL hand";
+    return DGX_E_INVALID;
+  }
+  return dgx_apply_gradient_step_joints(c, h->J, B, q, g, lr, q_out, flags);
+}
+
+int dgx_apply_gradient_step_joints(dgx_ctx* c, int32_t J, int32_t B, const double* q, const double* g, double lr,
+                                   double* q_out, uint32_t flags) {
   return guarded([&] {
+    if (!c) throw DgxError(DGX_E_INVALID, "NULL context");
+    if (J < 0 || J + 6 > kMaxDim) throw DgxError(DGX_E_INVALID, "num_joints out of range");
     if (B <= 0) return;
     set_device(c);
     const bool dev = flags & DGX_DEVICE_PTRS;
-    const int Qd = 7 + h->J, D = 6 + h->J;
+    const int Qd = 7 + J, D = 6 + J;
     Staging s(c, dev, 2 * bytes_round(8ull * B * Qd) + bytes_round(8ull * B * D));
     const double* dq = s.in(q, static_cast<size_t>(B) * Qd);
     const double* dg = s.in(g, static_cast<size_t>(B) * D);
     double* dout = s.out(q_out, static_cast<size_t>(B) * Qd);
-    cuda_check(launch_step(h->J, dq, dg, lr, dout, B, c->stream), "step_kernel");
+    cuda_check(launch_step(J, dq, dg, lr, dout, B, c->stream), "step_kernel");
     ++c->launches;
     s.finish(flags);
   });

@@ -154,6 +154,7 @@ KSim make_sim(const dgx_params* p, bool eval) {
   for (int m = 0; m < s.M && m < kMaxSims; ++m)
     for (int c = 0; c < 3; ++c) s.vel[m][c] = p->velocity_list ? p->velocity_list[3 * m + c] : p->velocities[m][c];
   s.vel_dev = nullptr;  // set by upload_velocities when M > kMaxSims
+  s.discard = std::getenv("DGX_NO_DISCARD") ? 0 : 1;
   s.w_stable = p->w_stable;
   s.w_qrange = p->w_qrange;
   s.w_qlimit = p->w_qlimit;

@@ -116,7 +116,8 @@ struct KSim {
   double dt, mu, alpha, radius;
   int gs, M, measure_residual, seg_max;
   int steps, fold;         // fold: warp-task adjoint folds the identical final sweeps (exact)
-  int pts_global, pad2;    // split forward: world points in buf.fk instead of shared memory
+  int pts_global;          // split forward: world points in buf.fk instead of shared memory
+  int discard;             // drop consumed scratch lines from L2 without write-back (discard.global.L2)
   double vel[kMaxSims][3];
   const double* vel_dev;  // [M,3] device copy when M > kMaxSims
   double w_stable, w_qrange, w_qlimit;

@@ -78,6 +78,18 @@ __device__ __forceinline__ double warp_max(double v) {
   return v;
 }
 
+// Scratch that has been consumed (correction logs / matrices, contact slots,
+// the forward's FK record) is dead until rewritten: drop its L2 lines without
+// write-back (PTX discard.global.L2, sm_80+) so it never costs HBM writes nor
+// evicts the SDF cells. Only whole 128 B lines inside [p, p + bytes) are
+// discarded; callers have finished every read of the range.
+__device__ __forceinline__ void l2_discard(const void* p, size_t bytes, int part, int nparts) {
+  const uintptr_t a = (reinterpret_cast<uintptr_t>(p) + 127) & ~static_cast<uintptr_t>(127);
+  const uintptr_t e = (reinterpret_cast<uintptr_t>(p) + bytes) & ~static_cast<uintptr_t>(127);
+  for (uintptr_t l = a + 128 * static_cast<uintptr_t>(part); l < e; l += 128 * static_cast<uintptr_t>(nparts))
+    asm volatile("discard.global.L2 [%0], 128;" ::"l"(l) : "memory");
+}
+
 struct SimEnv {
   int lane, N, gs, seg_max;
   const double *px, *py, *pz;
@@ -100,6 +112,7 @@ struct SimEnv {
   double* mcert;          // mesh: [N,4] nearest-face certificates (reset per sim)
   int* mcf;               // mesh: [N, 1 + kCertFaces]
   int fold;               // warp-task adjoint: fold the identical final sweeps
+  int discard;            // KSim::discard
 };
 
 // Forward classification of grids through the FP32 pre-filter (see
@@ -1341,6 +1354,11 @@ __device__ double run_sim(const Sdf& sdf, SimEnv& e, V3 v_m, bool record, bool m
   for (int t = lane; t < 6 * e.L; t += 32) e.ft[t] += __ldcg(e.gft + t);
   __syncwarp();
   PROF_ACC(10, tf);
+  if (e.discard) {  // this sim's logs and correction matrices are consumed
+    l2_discard(e.cmat, static_cast<size_t>(ncorr) * kCorrMat * sizeof(double), lane, 32);
+    l2_discard(e.corr, static_cast<size_t>(ncorr) * sizeof(CorrRec), lane, 32);
+    l2_discard(e.slots, static_cast<size_t>(nslot) * sizeof(SlotRec), lane, 32);
+  }
   return residual;
 }
 
@@ -1788,6 +1806,7 @@ __device__ __forceinline__ void kernel_body(const KHand& H, const KObj& O, const
   e.dt = S.dt;
   e.point_grads = nullptr;
   e.fold = S.fold;
+  e.discard = S.discard;
   e.mcache = buf.mesh_cache ? buf.mesh_cache + wslot * static_cast<size_t>(S.gs) * N * S.steps : nullptr;
   e.mcert = buf.mesh_cert ? buf.mesh_cert + wslot * 4 * static_cast<size_t>(N) : nullptr;
   e.mcf = buf.mesh_cf ? buf.mesh_cf + wslot * static_cast<size_t>(kCertFaces + 1) * N : nullptr;
@@ -1930,6 +1949,11 @@ __device__ __forceinline__ void kernel_body(const KHand& H, const KObj& O, const
         continue;
       }
     }
+    if constexpr (Phase == kPhaseAdj) {  // the forward's FK record of this candidate is consumed
+      if (S.discard && record)
+        l2_discard(buf.fk + static_cast<size_t>(b) * (12 * L + 3 * N), sizeof(double) * (12 * L + 3 * N), tid,
+                   blockDim.x);
+    }
     // write back
     if (mode == kModeOpt) {
       if (tid < Qd) buf.q[static_cast<size_t>(b) * Qd + tid] = sq[tid];
@@ -2020,6 +2044,7 @@ __device__ __forceinline__ void adj_task_body(const KHand& H, const KObj& O, con
   e.mcert = nullptr;
   e.mcf = nullptr;
   e.fold = S.fold;
+  e.discard = S.discard;
   const int k = mode == kModeOpt ? P.k_begin : 0;
   e.radius = S.radius;
   if (mode == kModeOpt)
@@ -2142,6 +2167,10 @@ __device__ __forceinline__ void adj_task_body(const KHand& H, const KObj& O, con
       }
       if (lane == 0) buf.status[b] = cand_status;
       __syncwarp();
+      if (S.discard) {  // every sim of the candidate has read its FK record; the task rows are consumed
+        l2_discard(link, sizeof(double) * (12 * L + 3 * N), lane, 32);
+        l2_discard(buf.task_ft + b0 * 6 * L, sizeof(double) * M * 6 * L, lane, 32);
+      }
     }
     next_task(b, m);
   }

@@ -305,7 +305,6 @@ SplitGrid prepare_split(dgx_ctx* c, Scratch& sc, const dgx_hand* h, const dgx_ob
     g.smem_a = TaskLayout(L, M, S.seg_max).bytes();
   } else {
     g.smem_a = choose_staging(h, o, S);
-    S.fold = std::getenv("DGX_CTA_FOLD") ? 1 : 0;
   }
   g.smem_f = SmemLayout(N, L, M, 0, !S.pts_global).total;
   int per_f = 0, per_a = 1;

@@ -1240,7 +1240,9 @@ __device__ double run_sim(const Sdf& sdf, SimEnv& e, V3 v_m, bool record, bool m
 #else
   // the warp-task adjoint folds (its warps do not wait on each other, so the
   // saved work is not lost to a barrier); DESIGN.md §3
-  int stage = ((Phase == kPhaseAdjTask || Phase == kPhaseAdj) && e.fold && Kc >= 2) ? 0 : 3;
+  // (the CTA-per-candidate adjoint measured slower with it: its warps wait at
+  // the candidate barrier, and the fold's code alone costs it issue slots)
+  int stage = (Phase == kPhaseAdjTask && e.fold && Kc >= 2) ? 0 : 3;
 #endif
   int k = ncorr - 1;
   V3 Xk_fold{0.0, 0.0, 0.0};

@@ -365,7 +365,7 @@ void dgr_object_use_box(void* o, const double* c, const double* h) {
   static_cast<GraspObject*>(o)->sdf.use_box(dgx::BoxSdf{{c[0], c[1], c[2]}, {h[0], h[1], h[2]}});
 }
 void dgr_object_use_grid(void* o, const int* dims, const double* origin, double h, double inv_h, const float* vals) {
-  dgx::GridSdf g{dims[0], dims[1], dims[2], {origin[0], origin[1], origin[2]}, h, inv_h, nullptr, nullptr,
+  dgx::GridSdf g{dims[0], dims[1], dims[2], {origin[0], origin[1], origin[2]}, h, inv_h, nullptr, nullptr, 0,
                  0.0f, 0.0f, 0.0f, 0.0f, 0.0f};
   std::vector<float> v(vals, vals + static_cast<std::size_t>(dims[0]) * dims[1] * dims[2]);
   static_cast<GraspObject*>(o)->sdf.use_grid(g, std::move(v));

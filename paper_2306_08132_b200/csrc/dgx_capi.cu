@@ -768,26 +768,36 @@ int dgx_object_upload(dgx_ctx* c, const dgx_object_desc* d, dgx_object** out) {
         const size_t nc = static_cast<size_t>(nx - 1) * (ny - 1) * (nz - 1);
         if (8 * nc >= (size_t(1) << 31) || n >= (size_t(1) << 31))
           throw DgxError(DGX_E_UNSUPPORTED, "grid: more than 2^28 cells (32-bit cell offsets)");
-        // node values (host-layout copy) + the corner-packed cells the kernels read
+        // node values (host-layout copy) + the packed cells the kernels read
+        // (GridSdf::cells): corner-packed (8 values per cell, one sector per
+        // lookup) while that copy stays well inside L2, else xy-quads (4 per
+        // cell per plane, half the footprint, two sectors per lookup).
+        // DGX_GRID_LAYOUT=8|4 forces one (A/B measurements).
         const size_t vbytes = (n * sizeof(float) + 255) & ~size_t(255);
-        o->vals.ensure(vbytes + nc * 8 * sizeof(float));
+        int pairs = 8 * nc * sizeof(float) > (size_t(32) << 20) ? 1 : 0;
+        if (const char* ev = std::getenv("DGX_GRID_LAYOUT")) pairs = std::atoi(ev) == 4 ? 1 : 0;
+        const size_t ncp = pairs ? static_cast<size_t>(nx - 1) * (ny - 1) * nz : nc;  // packed units
+        const int per = pairs ? 4 : 8;
+        o->vals.ensure(vbytes + ncp * per * sizeof(float));
         cuda_check(cudaMemcpy(o->vals.p, d->values, n * sizeof(float), cudaMemcpyHostToDevice), "grid upload");
-        std::vector<float> packed(nc * 8);
+        std::vector<float> packed(ncp * per);
         const float* v = d->values;
         auto at = [&](int i, int j, int k) { return v[(static_cast<size_t>(k) * ny + j) * nx + i]; };
-        for (int k = 0; k < nz - 1; ++k)
+        for (int k = 0; k < (pairs ? nz : nz - 1); ++k)
           for (int j = 0; j < ny - 1; ++j)
             for (int i = 0; i < nx - 1; ++i) {
-              float* c = packed.data() + 8 * ((static_cast<size_t>(k) * (ny - 1) + j) * (nx - 1) + i);
+              float* c = packed.data() + per * ((static_cast<size_t>(k) * (ny - 1) + j) * (nx - 1) + i);
               c[0] = at(i, j, k); c[1] = at(i + 1, j, k); c[2] = at(i, j + 1, k); c[3] = at(i + 1, j + 1, k);
-              c[4] = at(i, j, k + 1); c[5] = at(i + 1, j, k + 1); c[6] = at(i, j + 1, k + 1);
-              c[7] = at(i + 1, j + 1, k + 1);
+              if (!pairs) {
+                c[4] = at(i, j, k + 1); c[5] = at(i + 1, j, k + 1); c[6] = at(i, j + 1, k + 1);
+                c[7] = at(i + 1, j + 1, k + 1);
+              }
             }
         float* dcells = reinterpret_cast<float*>(static_cast<char*>(o->vals.p) + vbytes);
         cuda_check(cudaMemcpy(dcells, packed.data(), packed.size() * sizeof(float), cudaMemcpyHostToDevice),
                    "grid cells upload");
         o->sdf.grd = GridSdf{nx, ny, nz, V3{d->origin[0], d->origin[1], d->origin[2]}, d->spacing, d->inv_spacing,
-                             static_cast<const float*>(o->vals.p), dcells, static_cast<float>(d->origin[0]),
+                             static_cast<const float*>(o->vals.p), dcells, pairs, static_cast<float>(d->origin[0]),
                              static_cast<float>(d->origin[1]), static_cast<float>(d->origin[2]),
                              static_cast<float>(d->spacing), static_cast<float>(d->inv_spacing)};
       } else if (d->kind == DGX_SDF_MESH) {

@@ -261,10 +261,17 @@ struct GridSdf {
   V3 origin;
   double h, inv_h;
   const float* vals;
-  // device only (may be null): corner-packed copy, the 8 node values of cell
-  // (i,j,k) at cells[8 * ((k*(ny-1) + j)*(nx-1) + i)] in the order
-  // c000 c100 c010 c110 c001 c101 c011 c111 (one 32 B sector per lookup)
+  // device only (may be null): packed copy of the node values, read as two
+  // float4 per lookup (c000 c100 c010 c110 | c001 c101 c011 c111):
+  //   pairs == 0: corner-packed, the 8 values of cell (i,j,k) at
+  //     cells[8 * ((k*(ny-1) + j)*(nx-1) + i)] (one 32 B sector per lookup;
+  //     8x the node footprint);
+  //   pairs == 1: xy-quads, the 4 values (i..i+1, j..j+1) of plane k at
+  //     cells[4 * ((k*(ny-1) + j)*(nx-1) + i)], the lookup reads planes k and
+  //     k+1 (two sectors; 4x the node footprint, for grids whose corner-packed
+  //     copy would not stay L2-resident)
   const float* cells;
+  int pairs;
   // FP32 copies of origin / h / 1/h for the forward's FP32 pre-filter
   float ofx, ofy, ofz, hf, inv_hf;
 
@@ -296,9 +303,9 @@ struct GridSdf {
     double c000, c100, c010, c110, c001, c101, c011, c111;
 #if defined(__CUDA_ARCH__)
     if (cells) {
-      const float4* cp = reinterpret_cast<const float4*>(
-          cells + 8 * ((static_cast<long long>(ci[2]) * (ny - 1) + ci[1]) * (nx - 1) + ci[0]));
-      const float4 lo = __ldg(cp), hi = __ldg(cp + 1);
+      const long long cell = (static_cast<long long>(ci[2]) * (ny - 1) + ci[1]) * (nx - 1) + ci[0];
+      const float4* cp = reinterpret_cast<const float4*>(cells + (pairs ? 4 : 8) * cell);
+      const float4 lo = __ldg(cp), hi = __ldg(cp + (pairs ? static_cast<long long>(nx - 1) * (ny - 1) : 1));
       c000 = lo.x; c100 = lo.y; c010 = lo.z; c110 = lo.w;
       c001 = hi.x; c101 = hi.y; c011 = hi.z; c111 = hi.w;
     } else

@@ -4,6 +4,25 @@
 
 #include "dgx_mesh.h"
 
+// Device-side bounds checks for the checked build (-DDGX_CHECKS, tools/
+// build_checked.sh): every scratch / log / staging index against its
+// capacity; a violation prints the site and traps. Compiled out otherwise.
+#ifdef DGX_CHECKS
+#include <cstdio>
+#define DGX_ASSERT(c)                                                              \
+  do {                                                                             \
+    if (!(c)) {                                                                    \
+      printf("DGX_ASSERT failed %s:%d: %s (block %d thread %d)\n", __FILE__, __LINE__, #c, \
+             static_cast<int>(blockIdx.x), static_cast<int>(threadIdx.x));          \
+      __trap();                                                                    \
+    }                                                                              \
+  } while (0)
+#else
+#define DGX_ASSERT(c) \
+  do {                \
+  } while (0)
+#endif
+
 namespace dgx {
 
 constexpr int kMaxSims = 8;        // protocol velocities held inline in KSim (standard: 7); more: KSim::vel_dev

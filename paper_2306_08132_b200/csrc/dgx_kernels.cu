@@ -113,6 +113,7 @@ struct SimEnv {
   int* mcf;               // mesh: [N, 1 + kCertFaces]
   int fold;               // warp-task adjoint: fold the identical final sweeps
   int discard;            // KSim::discard
+  int slot_cap;           // contact-slot / friction-order entries of this sim's logs
 };
 
 // Forward classification of grids through the FP32 pre-filter (see
@@ -159,6 +160,7 @@ struct PointEval {
 template <class Sdf>
 __device__ __forceinline__ void eval_point(const Sdf& sdf, const SimEnv& e, int i, V3 x, const M3& R,
                                            bool record, PointEval& pe) {
+  DGX_ASSERT(i >= 0 && i < e.N);
   pe.p = V3{e.px[i], e.py[i], e.pz[i]};
   pe.rel = pe.p - x;
   pe.rl = tmul(R, pe.rel) + e.O->com;
@@ -193,6 +195,7 @@ struct FtAcc {
     T = V3{0.0, 0.0, 0.0};
   }
   __device__ __forceinline__ void spill(double* ft) {
+    DGX_ASSERT(link >= 0 && link < 32);
     double* d = ft + 6 * link;
     atomicAdd(d + 0, F.x); atomicAdd(d + 1, F.y); atomicAdd(d + 2, F.z);
     atomicAdd(d + 3, T.x); atomicAdd(d + 4, T.y); atomicAdd(d + 5, T.z);
@@ -402,6 +405,7 @@ struct LeakGeo {
 template <class Sdf>
 __device__ __forceinline__ void leak_geo(const Sdf& sdf, const SimEnv& e, int i, int fpos, V3 xk, const M3& Rk,
                                          LeakGeo& L) {
+  DGX_ASSERT(i >= 0 && i < e.N);
   L.p = V3{e.px[i], e.py[i], e.pz[i]};
   L.rel = L.p - xk;
   const V3 rl = ftmul_add(Rk, L.rel, e.O->com);
@@ -468,6 +472,7 @@ __device__ void process_run(const Sdf& sdf, SimEnv& e, int lo, int hi, V3 xk, Q4
     // segment length adapts to the run: short runs keep all lanes busy, long
     // runs amortise the scan over up to seg_max points per lane
     const int S = min(e.seg_max, (top - lo + 31) / 32);
+    DGX_ASSERT(S >= 1 && S <= e.seg_max && lo >= 0 && top <= e.gs * N);
     const int shi = top - lane * S;
     const int slo = max(top - (lane + 1) * S, lo);
     const int cnt = shi - slo;
@@ -681,8 +686,10 @@ __device__ __forceinline__ CorrOut apply_correction(const SimEnv& e, const CorrI
   const bool was = (e.bitmap[ij >> 5] & bit) != 0u;
   int slot;
   double lambda_n;
+  DGX_ASSERT(ij >= 0 && ij < e.N);
   if (!was) {
     slot = in.nslot;  // slots are sized N (sim.hpp:155): never overflows
+    DGX_ASSERT(slot < e.slot_cap);
     out.nslot = in.nslot + 1;
     lambda_n = 0.0 + lam;
     if (e.lane == 0) {
@@ -701,6 +708,7 @@ __device__ __forceinline__ CorrOut apply_correction(const SimEnv& e, const CorrI
     lambda_n = e.slots[slot].lambda_n + lam;
   }
   if (in.ncorr >= e.cap_corr) { out.status = kCorrOverflow; return out; }
+  DGX_ASSERT(slot >= 0 && slot < e.slot_cap && in.ncorr >= 0);
   if (e.lane == 0) {
     SlotRec& s = e.slots[slot];
     s.lambda_n = lambda_n;
@@ -806,7 +814,9 @@ __device__ __forceinline__ void correction_matrices(const SimEnv& e, int ncorr, 
 #pragma unroll 1
   for (int t = e.lane; t < ncorr * kCorrCols; t += 32) {
     const int k = t / kCorrCols, cb = t - k * kCorrCols;
+    DGX_ASSERT(k < e.cap_corr);
     const CorrRec c = e.corr[k];
+    DGX_ASSERT(c.slot >= 0 && c.slot < e.slot_cap);
     V3 xb = pred_x;
     Q4 qb = pred_q;
     if (k >= 1) {
@@ -1042,6 +1052,7 @@ __device__ double run_sim(const Sdf& sdf, SimEnv& e, V3 v_m, bool record, bool m
               e.fric_order[nfric] = slot;
             }
             ++nfric;
+            DGX_ASSERT(nfric <= e.slot_cap && slot < e.slot_cap);
           }
           __syncwarp();
         }
@@ -1387,7 +1398,7 @@ __device__ double run_sim_steps(const Sdf& sdf, SimEnv& e, V3 v_m, bool record, 
   SlotRec* slots0 = e.slots;
   int* fo0 = e.fric_order;
   int* mc0 = e.mcache;
-  const int cap0 = e.cap_corr;
+  const int cap0 = e.cap_corr, scap0 = e.slot_cap;
   const KObj* O0 = e.O;
   KObj Ot = *O0;  // Iw at each step's predicted orientation
   e.O = &Ot;
@@ -1396,6 +1407,7 @@ __device__ double run_sim_steps(const Sdf& sdf, SimEnv& e, V3 v_m, bool record, 
     e.slots = slots0 + s_off;
     e.fric_order = fo0 + f_off;
     e.cap_corr = cap0 - c_off;
+    e.slot_cap = scap0 - s_off;
     if (mc0) e.mcache = mc0 + static_cast<size_t>(t) * e.gs * e.N;
   };
   auto set_iw = [&](Q4 pq) {
@@ -1466,6 +1478,7 @@ __device__ double run_sim_steps(const Sdf& sdf, SimEnv& e, V3 v_m, bool record, 
   e.slots = slots0;
   e.fric_order = fo0;
   e.cap_corr = cap0;
+  e.slot_cap = scap0;
   e.mcache = mc0;
   return residual;
 }
@@ -1791,6 +1804,7 @@ __device__ __forceinline__ void kernel_body(const KHand& H, const KObj& O, const
   const size_t wslot = static_cast<size_t>(blockIdx.x) * W + warp;  // fused scratch: per (CTA, warp)
   // logs: per resident (CTA, warp) when fused; per (candidate, sim) when split
   // (bound per candidate below)
+  e.slot_cap = buf.slot_stride;
   auto bind_logs = [&](size_t ws) {
     e.corr = buf.corr + ws * buf.cap_corr;
     e.slots = buf.slots + ws * buf.slot_stride;
@@ -1817,6 +1831,7 @@ __device__ __forceinline__ void kernel_body(const KHand& H, const KObj& O, const
   const int k1 = mode == kModeOpt ? P.k_end : 1;
 
   for (int b = blockIdx.x; b < buf.B; b = next_candidate(buf, b, snext)) {
+    DGX_ASSERT(b >= 0);
     // a candidate that failed at an earlier iterate of this call stays there
     // (a multi-iterate launch's loop stops at its first failure)
     if (mode == kModeOpt && P.k_begin > P.traj_k0 && buf.status[b] != kOk) continue;
@@ -2038,6 +2053,7 @@ __device__ __forceinline__ void adj_task_body(const KHand& H, const KObj& O, con
   e.cmat = buf.cmat + static_cast<size_t>(gwarp) * buf.cap_corr * kCorrMat;
   e.L = L;
   e.cap_corr = buf.cap_corr;
+  e.slot_cap = buf.slot_stride;
   e.O = &O;
   e.alpha = S.alpha;
   e.mu = S.mu;

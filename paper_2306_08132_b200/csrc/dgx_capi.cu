@@ -235,7 +235,7 @@ int prepare(dgx_ctx* c, Scratch& sc, const dgx_hand* h, const dgx_object* o, KSi
                     : nullptr;
   buf.fwd = nullptr;
   buf.fk = nullptr;
-  sc.ftg.ensure(nws * (6 * static_cast<size_t>(h->L) + static_cast<size_t>(c->cap_corr) * kCorrMatDoubles) *
+  sc.ftg.ensure(nws * (6 * static_cast<size_t>(h->L) + static_cast<size_t>(kCorrBatch) * kCorrMatDoubles) *
                 sizeof(double));
   buf.ft_global = static_cast<double*>(sc.ftg.p);
   buf.cmat = buf.ft_global + nws * 6 * static_cast<size_t>(h->L);
@@ -361,7 +361,7 @@ SplitGrid prepare_split(dgx_ctx* c, Scratch& sc, const dgx_hand* h, const dgx_ob
   }
   // adjoint spill / correction-matrix buffers per resident warp
   const size_t nwa = g.task ? static_cast<size_t>(g.grid_a) * kTaskWarps : static_cast<size_t>(g.grid_a) * M;
-  sc.ftg.ensure(nwa * (6 * static_cast<size_t>(h->L) + static_cast<size_t>(c->cap_corr) * kCorrMatDoubles) *
+  sc.ftg.ensure(nwa * (6 * static_cast<size_t>(h->L) + static_cast<size_t>(kCorrBatch) * kCorrMatDoubles) *
                 sizeof(double));
   buf.ft_global = static_cast<double*>(sc.ftg.p);
   buf.cmat = buf.ft_global + nwa * 6 * static_cast<size_t>(h->L);

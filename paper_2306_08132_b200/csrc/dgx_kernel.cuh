@@ -29,7 +29,13 @@ constexpr int kMaxSims = 8;        // protocol velocities held inline in KSim (s
 constexpr int kMaxWarps = 7;       // warps per grasp-search CTA: warp w runs sims w, w + W, ... (W = min(M, 7))
 constexpr int kMaxDim = 32;        // 6 + J gradient coordinates (J <= 26)
 constexpr int kSegMaxCap = 16;
-constexpr int kCorrMatDoubles = 19 * 8 + 1;  // dgx_kernels.cu kCorrMat    // max points per lane segment in the adjoint
+constexpr int kCorrMatDoubles = 19 * 8 + 1;  // dgx_kernels.cu kCorrMat
+// correction-reverse matrices are built kCorrBatch at a time, just before the
+// reverse sweep reaches them, into a per-warp ring (L1 / L2-resident)
+#ifndef DGX_CORR_BATCH
+#define DGX_CORR_BATCH 16
+#endif
+constexpr int kCorrBatch = DGX_CORR_BATCH;
 
 enum Mode : int { kModeGrad = 0, kModeEval = 1, kModeOpt = 2 };
 

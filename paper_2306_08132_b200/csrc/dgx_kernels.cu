@@ -810,10 +810,11 @@ static_assert(kCorrMat == kCorrMatDoubles, "host scratch sizing");
 // All corrections' matrices, (correction, column) tasks spread over the warp.
 // Column 7 is the constant part: v = 0 with the slot's final a_lam / a_n
 // (set by the friction reverse; correction adjoints only read them).
-__device__ __forceinline__ void correction_matrices(const SimEnv& e, int ncorr, V3 pred_x, Q4 pred_q) {
+// Corrections [k_lo, k_hi] go to ring entries k % kCorrBatch.
+__device__ __forceinline__ void correction_matrices(const SimEnv& e, int k_lo, int k_hi, V3 pred_x, Q4 pred_q) {
 #pragma unroll 1
-  for (int t = e.lane; t < ncorr * kCorrCols; t += 32) {
-    const int k = t / kCorrCols, cb = t - k * kCorrCols;
+  for (int t = e.lane; t < (k_hi - k_lo + 1) * kCorrCols; t += 32) {
+    const int k = k_lo + t / kCorrCols, cb = t % kCorrCols;
     DGX_ASSERT(k < e.cap_corr);
     const CorrRec c = e.corr[k];
     DGX_ASSERT(c.slot >= 0 && c.slot < e.slot_cap);
@@ -835,7 +836,7 @@ __device__ __forceinline__ void correction_matrices(const SimEnv& e, int ncorr, 
     }
     bool ok = true;
     const CorrLin o = correction_linear(e, c, xb, qb, vx, vq, a_lam, a_nw, ok);
-    double* Mk = e.cmat + static_cast<size_t>(k) * kCorrMat;
+    double* Mk = e.cmat + static_cast<size_t>(k % kCorrBatch) * kCorrMat;
     const double col[kCorrRows] = {o.aX.x, o.aX.y, o.aX.z, o.aQ.w, o.aQ.x, o.aQ.y, o.aQ.z,
                                    o.aR.m[0], o.aR.m[1], o.aR.m[2], o.aR.m[3], o.aR.m[4], o.aR.m[5],
                                    o.aR.m[6], o.aR.m[7], o.aR.m[8], o.a_rel.x, o.a_rel.y, o.a_rel.z};
@@ -1225,7 +1226,7 @@ __device__ double run_sim(const Sdf& sdf, SimEnv& e, V3 v_m, bool record, bool m
 
   PROF_ACC(4, tfa);
   PROF_T(tcm);
-  correction_matrices(e, ncorr, pred_x, pred_q);
+  int built_lo = ncorr;  // matrices of corrections [built_lo, ...] are in the ring
   PROF_ACC(11, tcm);
   // ---- sweeps, reverse ----------------------------------------------------
   M3 aR;  // per-lane partial adjoint of the current R node
@@ -1319,8 +1320,12 @@ __device__ double run_sim(const Sdf& sdf, SimEnv& e, V3 v_m, bool record, bool m
     const M3 aRk = warp_sum(aR);
     aQ = qadd(aQ, rotmat_adj(qk, aRk));
     for (int t = 0; t < 9; ++t) aR.m[t] = 0.0;
+    if (k < built_lo) {  // next batch of correction matrices, built in parallel
+      built_lo = max(0, k - kCorrBatch + 1);
+      correction_matrices(e, built_lo, k, pred_x, pred_q);
+    }
     {  // the precomputed affine map of correction k: one 19 x 8 mat-vec (lanes = rows)
-      const double* Mk = e.cmat + static_cast<size_t>(k) * kCorrMat;
+      const double* Mk = e.cmat + static_cast<size_t>(k % kCorrBatch) * kCorrMat;
       const double v[kCorrCols] = {aX.x, aX.y, aX.z, aQ.w, aQ.x, aQ.y, aQ.z, 1.0};
       double r = 0.0;
       if (lane < kCorrRows) {
@@ -1368,7 +1373,7 @@ __device__ double run_sim(const Sdf& sdf, SimEnv& e, V3 v_m, bool record, bool m
   __syncwarp();
   PROF_ACC(10, tf);
   if (e.discard) {  // this sim's logs and correction matrices are consumed
-    l2_discard(e.cmat, static_cast<size_t>(ncorr) * kCorrMat * sizeof(double), lane, 32);
+    l2_discard(e.cmat, static_cast<size_t>(min(ncorr, kCorrBatch)) * kCorrMat * sizeof(double), lane, 32);
     l2_discard(e.corr, static_cast<size_t>(ncorr) * sizeof(CorrRec), lane, 32);
     l2_discard(e.slots, static_cast<size_t>(nslot) * sizeof(SlotRec), lane, 32);
   }
@@ -1813,7 +1818,7 @@ __device__ __forceinline__ void kernel_body(const KHand& H, const KObj& O, const
   };
   bind_logs(wslot);
   e.gft = buf.ft_global + wslot * 6 * L;
-  e.cmat = buf.cmat + wslot * static_cast<size_t>(buf.cap_corr) * kCorrMat;
+  e.cmat = buf.cmat + wslot * static_cast<size_t>(kCorrBatch) * kCorrMat;
   e.L = L;
   e.cap_corr = buf.cap_corr;
   e.O = &O;
@@ -2050,7 +2055,7 @@ __device__ __forceinline__ void adj_task_body(const KHand& H, const KObj& O, con
   e.seg_max = S.seg_max;
   e.ft = ftw;
   e.gft = buf.ft_global + static_cast<size_t>(gwarp) * 6 * L;
-  e.cmat = buf.cmat + static_cast<size_t>(gwarp) * buf.cap_corr * kCorrMat;
+  e.cmat = buf.cmat + static_cast<size_t>(gwarp) * kCorrBatch * kCorrMat;
   e.L = L;
   e.cap_corr = buf.cap_corr;
   e.slot_cap = buf.slot_stride;

@@ -399,9 +399,10 @@ def run_dgx(args, rank, world, local_rank):
     ctx.set_stream(stream.cuda_stream)
     n0 = int(counts[0])
     sub = {k: st[k][:n0] for k in ("q", "m", "v", "status")}
+    ksteps = max(3, min(args.steps, 10))
     for phase in ("warm", "timed"):
         ctx.set_kernel_timing(phase == "timed")
-        for s in range(3 if phase == "warm" else max(3, min(args.steps, 10))):
+        for s in range(3 if phase == "warm" else ksteps):
             flush.zero_()
             ks = (k0 + s) % ITERS
             api.optimize(ctx, objs[0], hand, sub["q"], proto, params, weights, opt, k_begin=ks, k_end=ks + 1,
@@ -423,10 +424,14 @@ def run_dgx(args, rank, world, local_rank):
                              ("fused", FLOP_PER_POINT_SWEEP)):
             ms_tot, cnt = ktimes[kind]
             if cnt:
+                # a step's n0 candidates may be split over several launches (scratch
+                # chunks): a launch processes n0 * steps / launches candidates on average
                 ms = ms_tot / cnt
-                kern[kind] = {"avg_launch_ms": ms, "launches": cnt, "candidates_per_launch": n0,
+                per_launch = n0 * ksteps / cnt
+                kern[kind] = {"avg_launch_ms": ms, "launches": cnt, "steps": ksteps,
+                              "candidates_per_launch": per_launch,
                               "flop_per_candidate_iteration": pts_sweeps * per_ps,
-                              "achieved_tflops": pts_sweeps * per_ps * n0 / (ms * 1e-3) / 1e12}
+                              "achieved_tflops": pts_sweeps * per_ps * per_launch / (ms * 1e-3) / 1e12}
         dom = max(kern, key=lambda k: kern[k]["avg_launch_ms"] * kern[k]["launches"])
         step_kernel_ms = sum(v["avg_launch_ms"] * v["launches"] for v in kern.values())
         for v in kern.values():

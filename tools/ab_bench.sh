@@ -9,7 +9,7 @@ for cfg in $cfgs; do
       python -c "import json,sys
 t=sys.stdin.read()
 try:
-  d=json.loads(t); print(round(d['value']), {k:(round(v['avg_launch_ms'],3), v['launches']) for k,v in d['roofline']['kernels'].items()}, round(d['roofline']['frac'],4))
+  d=json.loads(t); print(round(d['value']), {k:(round(v['avg_launch_ms'],3), v['launches']) for k,v in d['roofline']['kernels'].items()}, round(d['roofline']['frac'],4), d['clocks']['sm_mhz'])
 except Exception: print('FAILED', t[-300:])"
   done
 done

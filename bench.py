@@ -363,6 +363,10 @@ def run_dgx(args, rank, world, local_rank):
     ctx.set_stream(None)
     k0 = args.warmup + args.steps
     h2d = d2h = 0
+    # one untimed call first: the host path runs on the context's side stream,
+    # whose scratch is allocated on first use
+    api.optimize_multi(ctx, objs, hand, host["q"].copy(), counts, proto, params, weights, opt, k_begin=k0 % ITERS,
+                       k_end=k0 % ITERS + 1, adam_m=host["m"].copy(), adam_v=host["v"].copy(), record=True)
     torch.cuda.synchronize()
     if world > 1:
         dist.barrier()

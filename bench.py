@@ -200,16 +200,21 @@ class ClockSampler:
                 "reasons": reasons, "samples": len(sm), "window_s": (self.t1 - self.t0) if self.t0 else None}
 
 
-def traffic_from_profiles(name: str, kernel: str):
-    """DRAM bytes per launch of the dominant kernel from the committed ncu
-    capture of THIS workload (profiles/roofline_traffic.json, keyed by
-    workload and kernel kind); None when that capture does not exist."""
+def traffic_from_profiles(name: str, kernel: str, candidates_per_launch: float):
+    """DRAM bytes (read + write) per launch of the dominant kernel from the
+    committed ncu --set full capture of THIS workload (profiles/
+    roofline_traffic.json, keyed by workload and kernel kind), scaled from the
+    captured launch's candidate count to this run's average launch; None when
+    that capture does not exist."""
     p = os.path.join(ROOT, "profiles", "roofline_traffic.json")
     if not os.path.exists(p):
         return None, None
     with open(p) as f:
         d = json.load(f).get(name, {}).get(kernel)
-    return (d["dram_bytes_per_launch"], d["source"]) if d else (None, None)
+    if not d:
+        return None, None
+    per = d["dram_bytes_per_launch"] / d["candidates_per_launch"]
+    return per * candidates_per_launch, d["source"]
 
 
 # ---------------------------------------------------------------------------
@@ -441,7 +446,7 @@ def run_dgx(args, rank, world, local_rank):
         for v in kern.values():
             v["share_of_serialised_step"] = v["avg_launch_ms"] * v["launches"] / step_kernel_ms
         achieved = kern[dom]["achieved_tflops"]
-        traffic, traffic_src = traffic_from_profiles(args.workload, dom)
+        traffic, traffic_src = traffic_from_profiles(args.workload, dom, kern[dom]["candidates_per_launch"])
         result = {
             "metric": "candidate-iterations/sec", "value": value, "unit": "candidate-iterations/s",
             "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": max_ms / args.steps,

@@ -330,6 +330,10 @@ SplitGrid prepare_split(dgx_ctx* c, Scratch& sc, const dgx_hand* h, const dgx_ob
   const size_t by_mem = std::max<size_t>(1, budget / per_cand);
   g.chunk = static_cast<int>(std::max<size_t>(
       1, std::min<size_t>(B, std::max<size_t>(4 * static_cast<size_t>(std::max(g.grid_f, g.grid_a)), by_mem))));
+  {  // equal chunks (4096 -> 2 x 2048, not 2973 + 1123): the same launch count, balanced launches
+    const int n = (B + g.chunk - 1) / g.chunk;
+    g.chunk = (B + n - 1) / n;
+  }
   g.grid_f = std::min(g.grid_f, g.chunk);
   g.grid_a = std::min(g.grid_a, g.chunk);
   const size_t nws = static_cast<size_t>(g.chunk) * M;

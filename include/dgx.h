@@ -179,6 +179,14 @@ int64_t dgx_ctx_launch_count(const dgx_ctx* ctx);
  * (0 fused, 1 split forward, 2 split adjoint), the summed milliseconds and the
  * launch count since the last enable; ms / count may be NULL. */
 int dgx_ctx_set_kernel_timing(dgx_ctx* ctx, int enable);
+/* Split-execution adjoint kernel (measurement / testing; no reference
+ * counterpart). DGX_ADJOINT_AUTO (default): the lane adjoint (one thread per
+ * (candidate, sim)) when the batch gives it >= 4 warps per SM, else the CTA
+ * adjoint (one CTA per candidate, bit-identical to the fused kernel).
+ * Gradients of the two agree to rounding. The DGX_ADJ
+ * environment variable (lane | cta | task) overrides AUTO. */
+enum { DGX_ADJOINT_AUTO = 0, DGX_ADJOINT_CTA = 1, DGX_ADJOINT_LANE = 2 };
+int dgx_ctx_set_adjoint(dgx_ctx* ctx, int variant);
 int dgx_ctx_kernel_times(dgx_ctx* ctx, double ms[3], int64_t count[3]);
 
 int dgx_hand_upload(dgx_ctx* ctx, const dgx_hand_desc* desc, dgx_hand** out);

@@ -125,6 +125,12 @@ class Context:
         (resets the record)."""
         capi.check(self.L.dgx_ctx_set_kernel_timing(self.h, int(enable)))
 
+    def set_adjoint(self, variant: str) -> None:
+        """Split-execution adjoint kernel: "auto" (default), "cta" or "lane"
+        (include/dgx.h dgx_ctx_set_adjoint)."""
+        v = {"auto": 0, "cta": 1, "lane": 2}[variant]
+        capi.check(self.L.dgx_ctx_set_adjoint(self.h, v))
+
     def kernel_times(self) -> dict:
         """{kind: (total ms, launches)} for kinds fused / forward / adjoint since
         set_kernel_timing(True); synchronizes on the recorded events."""

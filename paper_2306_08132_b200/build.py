@@ -13,7 +13,7 @@ PKG = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(PKG, "csrc")
 OUT = os.path.join(PKG, "libdgx_cuda.so")
 SOURCES = ["dgx_kernels.cu", "dgx_capi.cu", "dgx_peak.cu", "dgx_mesh_host.cu", "dgx_drop.cu"]
-HEADERS = ["dgx_math.h", "dgx_geom.h", "dgx_mesh.h", "dgx_mesh_host.h", "dgx_adjoint.cuh", "dgx_kernel.cuh", "dgx_sdf_fast.cuh", "dgx_drop.cuh"]
+HEADERS = ["dgx_math.h", "dgx_geom.h", "dgx_mesh.h", "dgx_mesh_host.h", "dgx_adjoint.cuh", "dgx_kernel.cuh", "dgx_sdf_fast.cuh", "dgx_drop.cuh", "dgx_lane_adj.cuh"]
 NVCC_FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "--fmad=false", "-std=c++17",
               "-Xcompiler", "-fPIC", "-shared"]
 

@@ -81,7 +81,7 @@ class OptC(C.Structure):
 
 EXPORTS = [
     "dgx_last_error", "dgx_abi_version", "dgx_ctx_create", "dgx_ctx_destroy", "dgx_ctx_set_stream",
-    "dgx_ctx_set_correction_capacity", "dgx_ctx_launch_count", "dgx_ctx_set_kernel_timing",
+    "dgx_ctx_set_correction_capacity", "dgx_ctx_launch_count", "dgx_ctx_set_kernel_timing", "dgx_ctx_set_adjoint",
     "dgx_ctx_kernel_times", "dgx_hand_upload", "dgx_hand_free",
     "dgx_object_upload", "dgx_object_free", "dgx_forward_batch", "dgx_loss_gradient_batch",
     "dgx_evaluate_losses_batch", "dgx_apply_gradient_step_batch", "dgx_optimize_batch", "dgx_debug_sims",
@@ -117,6 +117,7 @@ def load() -> C.CDLL:
     L.dgx_ctx_launch_count.argtypes = [vp]
     L.dgx_ctx_launch_count.restype = C.c_int64
     L.dgx_ctx_set_kernel_timing.argtypes = [vp, C.c_int]
+    L.dgx_ctx_set_adjoint.argtypes = [vp, C.c_int]
     L.dgx_ctx_kernel_times.argtypes = [vp, C.POINTER(C.c_double), C.POINTER(C.c_int64)]
     L.dgx_hand_upload.argtypes = [vp, C.POINTER(HandDescC), C.POINTER(vp)]
     L.dgx_hand_free.argtypes = [vp]

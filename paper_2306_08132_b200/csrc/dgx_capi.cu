@@ -96,6 +96,7 @@ struct dgx_ctx {
   cudaStream_t stream = nullptr;
   cudaEvent_t fork = nullptr;
   int cap_corr = 1024;
+  int adjoint = DGX_ADJOINT_AUTO;  // dgx_ctx_set_adjoint
   int64_t launches = 0;
   // kernel timing (dgx_ctx_set_kernel_timing): event pairs per launch
   bool timing = false;
@@ -270,22 +271,42 @@ bool use_split(const dgx_object* o) {
 }
 
 constexpr size_t kSplitScratchBytes = size_t(8) << 30;  // per stream
+constexpr size_t kLaneScratchBytes = size_t(24) << 30;  // per stream, lane adjoint
 constexpr int kSplitMaxFwdSmem = 96 * 1024;
 
 struct SplitGrid {
   int chunk, grid_f, grid_a, smem_f, smem_a;
   bool task;  // adjoint as warp tasks (adj_task_kernel) instead of one CTA per candidate
+  bool lane;  // adjoint with one thread per (candidate, sim) + the epilogue kernel (the default)
 };
+
+// Split adjoint variant. Default (auto): the lane adjoint
+// (lane_adj_kernel, one thread per (candidate, sim), dgx_lane_adj.cuh) when the
+// batch gives it at least kLaneMinWarpsPerSm warps per SM, else the CTA-per-
+// candidate adjoint (bit-identical to the fused kernel). The lane adjoint's
+// parallelism is its task count: config 3 (4096 x 7 tasks, 6 warps / SM)
+// 30.9 vs 52.3 ms per step; 2048 x 7 tasks (3 warps / SM) 31.8 vs 26.1 ms per
+// 2048 (U = 4 build). DGX_ADJ=lane|cta|task forces one (A/B measurements);
+// DGX_ADJ_TASK=1 is the warp-task adjoint (kept for A/B, never faster).
+constexpr int kLaneMinWarpsPerSm = 4;
+int adjoint_variant() {  // 0 cta, 1 task, 2 lane, 3 auto
+  static const int v = [] {
+    const char* ev = std::getenv("DGX_ADJ");
+    if (std::getenv("DGX_ADJ_TASK")) return 1;
+    if (!ev) return 3;
+    if (std::strcmp(ev, "cta") == 0) return 0;
+    if (std::strcmp(ev, "task") == 0) return 1;
+    if (std::strcmp(ev, "lane") == 0) return 2;
+    return 3;
+  }();
+  return v;
+}
 
 // Split adjoint as warp tasks (DGX_ADJ_TASK=1; measured equal to the CTA-per-
 // candidate adjoint on configs 2 and 3, so the CTA adjoint,
 // bit-identical to the fused kernel, stays the default). Its staging length:
 // DGX_TASK_SEG (default 8 points per lane: 8 warps x 11.5 KB leave most of the
 // SM's 256 KB as L1 for the points and SDF cells the tasks read from L2).
-bool use_task_adjoint() {
-  static const bool task = std::getenv("DGX_ADJ_TASK") != nullptr;
-  return task;
-}
 int task_seg() {
   static const int seg = [] {
     const char* ev = std::getenv("DGX_TASK_SEG");
@@ -298,8 +319,15 @@ SplitGrid prepare_split(dgx_ctx* c, Scratch& sc, const dgx_hand* h, const dgx_ob
                         bool record, KBuf& buf) {
   const int M = S.M, N = h->N, L = h->L;
   SplitGrid g{};
-  g.task = record && use_task_adjoint();
-  if (g.task) {
+  int av = adjoint_variant();
+  if (av == 3 && c->adjoint != DGX_ADJOINT_AUTO) av = c->adjoint == DGX_ADJOINT_LANE ? 2 : 0;
+  g.task = record && av == 1;
+  g.lane = record && N >= kLaneU &&
+           (av == 2 || (av == 3 && static_cast<long long>(B) * M >=
+                                       static_cast<long long>(kLaneMinWarpsPerSm) * 32 * c->num_sms));
+  if (g.lane) {
+    g.smem_a = 0;
+  } else if (g.task) {
     S.seg_max = task_seg();
     S.fold = std::getenv("DGX_NOFOLD") ? 0 : 1;
     g.smem_a = TaskLayout(L, M, S.seg_max).bytes();
@@ -310,7 +338,8 @@ SplitGrid prepare_split(dgx_ctx* c, Scratch& sc, const dgx_hand* h, const dgx_ob
   int per_f = 0, per_a = 1;
   cuda_check(fused_occupancy(o->kind, M, g.smem_f, S.pts_global ? kPhaseFwdPtsG : kPhaseFwd, &per_f), "occupancy");
   if (record) {
-    if (g.task) cuda_check(adj_task_occupancy(o->kind, g.smem_a, &per_a), "occupancy");
+    if (g.lane) per_a = 1;
+    else if (g.task) cuda_check(adj_task_occupancy(o->kind, g.smem_a, &per_a), "occupancy");
     else cuda_check(fused_occupancy(o->kind, M, g.smem_a, kPhaseAdj, &per_a), "occupancy");
   }
   if (per_f < 1 || per_a < 1) throw DgxError(DGX_E_UNSUPPORTED, "split kernels cannot be resident (registers/smem)");
@@ -324,7 +353,11 @@ SplitGrid prepare_split(dgx_ctx* c, Scratch& sc, const dgx_hand* h, const dgx_ob
                                                     sizeof(FwdRec) + static_cast<size_t>(N) * sizeof(int) +
                                                     (6 * static_cast<size_t>(L) + 2) * sizeof(double)) +
                           (12 * static_cast<size_t>(h->L) + 3 * static_cast<size_t>(N)) * sizeof(double) + 8;
-  size_t budget = kSplitScratchBytes;
+  // the lane adjoint's parallelism is its task count (one thread per (candidate,
+  // sim)): it takes the whole batch in one chunk when kLaneScratchBytes allows
+  size_t budget = g.lane ? kLaneScratchBytes : kSplitScratchBytes;
+  if (const char* ev = std::getenv("DGX_LANE_SCRATCH_MB"); ev && g.lane)
+    budget = static_cast<size_t>(std::max(1, std::atoi(ev))) << 20;
   if (const char* ev = std::getenv("DGX_SPLIT_SCRATCH_MB"))  // tests: force several chunks
     budget = static_cast<size_t>(std::max(1, std::atoi(ev))) << 20;
   const size_t by_mem = std::max<size_t>(1, budget / per_cand);
@@ -512,7 +545,14 @@ void launch_range(dgx_ctx* c, Scratch& sc, const dgx_hand* h, const dgx_object* 
       });
       if (!record) continue;
       bind_claim(sc, cb, nb, st);
-      if (g.task) {
+      if (g.lane) {
+        counted_launch(c, kPhaseAdj, st, "lane adjoint kernels", [&] {
+          cudaError_t e = launch_lane_adj(h->k, o->k, o->sdf, S, Pk, cb, mode, st);
+          if (e != cudaSuccess) return e;
+          ++c->launches;  // + the epilogue kernel
+          return launch_lane_epi(h->k, S, Pk, cb, mode, st);
+        });
+      } else if (g.task) {
         cuda_check(cudaMemsetAsync(cb.task_done, 0, sizeof(int) * nb, st), "cudaMemsetAsync");
         const int grid_t = std::max(1, std::min(g.grid_a, (nb * M + kTaskWarps - 1) / kTaskWarps));
         counted_launch(c, kPhaseAdj, st, "adjoint task kernel", [&] {
@@ -636,6 +676,15 @@ int dgx_ctx_set_correction_capacity(dgx_ctx* c, int32_t cap) {
 }
 
 int64_t dgx_ctx_launch_count(const dgx_ctx* c) { return c ? c->launches : 0; }
+
+int dgx_ctx_set_adjoint(dgx_ctx* c, int variant) {
+  return guarded([&] {
+    if (!c) throw DgxError(DGX_E_INVALID, "NULL context");
+    if (variant != DGX_ADJOINT_AUTO && variant != DGX_ADJOINT_CTA && variant != DGX_ADJOINT_LANE)
+      throw DgxError(DGX_E_INVALID, "unknown adjoint variant");
+    c->adjoint = variant;
+  });
+}
 
 int dgx_ctx_set_kernel_timing(dgx_ctx* c, int enable) {
   return guarded([&] {

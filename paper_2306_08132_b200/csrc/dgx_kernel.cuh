@@ -36,6 +36,12 @@ constexpr int kCorrMatDoubles = 19 * 8 + 1;  // dgx_kernels.cu kCorrMat
 #define DGX_CORR_BATCH 16
 #endif
 constexpr int kCorrBatch = DGX_CORR_BATCH;
+// lane adjoint (dgx_lane_adj.cuh): positions per step of a thread's reverse walk
+// (independent geometry, then the serial recurrence); needs N >= kLaneU
+#ifndef DGX_LANE_U
+#define DGX_LANE_U 2  // config 3 (adjoint ms per 4096-candidate step): U 1 43.8, 2 30.9, 4 36.6, 8 85.3
+#endif
+constexpr int kLaneU = DGX_LANE_U;
 
 enum Mode : int { kModeGrad = 0, kModeEval = 1, kModeOpt = 2 };
 
@@ -101,7 +107,8 @@ struct FwdRec {
   double x[3];
   double q[4];
   double residual;
-  int ncorr, nslot, nfric, touched, status, pad;
+  int ncorr, nslot, nfric, touched, status;
+  int fwd_end;  // first position the forward's quiet-window exit left unclassified (gs N: none)
 };
 
 // Per (warp slot, step) record of a multi-step perturbation sim
@@ -271,6 +278,11 @@ cudaError_t fused_occupancy(int kind, int M, int smem, int phase, int* blocks_pe
 cudaError_t launch_adj_task(const KHand& H, const KObj& O, const SdfSet& sdf, const KSim& S, const KOpt& P,
                             const KBuf& buf, int mode, int grid, int smem, cudaStream_t st);
 cudaError_t adj_task_occupancy(int kind, int smem, int* per_sm);
+// split adjoint with one thread per (candidate, sim) (dgx_lane_adj.cuh), then
+// the per-candidate epilogue kernel (one warp per candidate)
+cudaError_t launch_lane_adj(const KHand& H, const KObj& O, const SdfSet& sdf, const KSim& S, const KOpt& P,
+                            const KBuf& buf, int mode, cudaStream_t st);
+cudaError_t launch_lane_epi(const KHand& H, const KSim& S, const KOpt& P, const KBuf& buf, int mode, cudaStream_t st);
 inline bool split_capable(int kind) { return kind != kSdfMesh; }
 // out[n, 8] = rho - radius, grad (3), proxy (3), sign per point (MeshSdf::dilated,
 // sdf.cpp:62-67); within != 0: dilated_within (sdf.cpp:69-81), culled points

@@ -893,6 +893,7 @@ __device__ double run_sim(const Sdf& sdf, SimEnv& e, V3 v_m, bool record, bool m
   Q4 q = pred_q;
   bool touched = false;
   int ncorr = 0, nslot = 0, nfric = 0;
+  int fwd_end = e.gs * N;  // forward: quiet-window exit position (recorded for the lane adjoint)
   const int nwords = (N + 31) / 32;
   if constexpr (Phase == kPhaseAdj || Phase == kPhaseAdjTask) {
     x = V3{rec->x[0], rec->x[1], rec->x[2]};
@@ -932,10 +933,10 @@ __device__ double run_sim(const Sdf& sdf, SimEnv& e, V3 v_m, bool record, bool m
     int f_last = -1, singular_since = 0;
     while (sweep < e.gs) {
   #if defined(DGX_QUIET) || defined(DGX_QUIET_FWD)  // exact
-      if (sweep * N + pos - f_last - 1 >= N && singular_since == 0) break;
+      if (sweep * N + pos - f_last - 1 >= N && singular_since == 0) { fwd_end = sweep * N + pos; break; }
   #else
       if constexpr (kQuietExit) {
-        if (sweep * N + pos - f_last - 1 >= N && singular_since == 0) break;
+        if (sweep * N + pos - f_last - 1 >= N && singular_since == 0) { fwd_end = sweep * N + pos; break; }
       }
   #endif
       int cls[2];
@@ -1109,6 +1110,7 @@ __device__ double run_sim(const Sdf& sdf, SimEnv& e, V3 v_m, bool record, bool m
       rec->ncorr = ncorr;
       rec->nslot = nslot;
       rec->nfric = nfric;
+      rec->fwd_end = fwd_end;
     }
     return residual;
   }
@@ -2205,6 +2207,8 @@ __global__ void __launch_bounds__(32 * kTaskWarps, MinBlocks) adj_task_kernel(KH
                                                                               int mode) {
   adj_task_body<Sdf>(H, O, sdf, S, P, buf, mode);
 }
+
+#include "dgx_lane_adj.cuh"
 }  // namespace dgx
 
 // ---------------------------------------------------------------------------
@@ -2664,6 +2668,43 @@ cudaError_t adj_task_occupancy(int kind, int smem, int* per_sm) {
     case kSdfGrid: return task_occ_t<GridSdf>(smem, per_sm);
     default: return cudaErrorInvalidValue;
   }
+}
+
+// lane adjoint (dgx_lane_adj.cuh): one thread per (candidate, sim), then one
+// warp per candidate for the epilogue
+template <class Sdf>
+static cudaError_t launch_lane_t(const KHand& H, const KObj& O, const Sdf& sdf, const KSim& S, const KOpt& P,
+                                 const KBuf& buf, int mode, cudaStream_t st) {
+  if constexpr (kSplitCapable<Sdf>) {
+    const long long nt = static_cast<long long>(buf.B) * S.M;
+    const int grid = static_cast<int>((nt + kLaneAdjThreads - 1) / kLaneAdjThreads);
+    lane_adj_kernel<Sdf><<<grid, kLaneAdjThreads, 0, st>>>(H, O, sdf, S, P, buf, mode);
+    return cudaGetLastError();
+  }
+  return cudaErrorInvalidValue;
+}
+
+cudaError_t launch_lane_adj(const KHand& H, const KObj& O, const SdfSet& sdf, const KSim& S, const KOpt& P,
+                            const KBuf& buf, int mode, cudaStream_t st) {
+  switch (sdf.kind) {
+    case kSdfSphere: return launch_lane_t(H, O, sdf.sph, S, P, buf, mode, st);
+    case kSdfBox: return launch_lane_t(H, O, sdf.box, S, P, buf, mode, st);
+    case kSdfGrid: return launch_lane_t(H, O, sdf.grd, S, P, buf, mode, st);
+    default: return cudaErrorInvalidValue;
+  }
+}
+
+cudaError_t launch_lane_epi(const KHand& H, const KSim& S, const KOpt& P, const KBuf& buf, int mode, cudaStream_t st) {
+  static bool configured = false;
+  const int smem = 8 * kEpiWarps * lane_epi_doubles(S.M, H.L);
+  if (!configured) {
+    cudaError_t e = cudaFuncSetAttribute(lane_epi_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+    if (e != cudaSuccess) return e;
+    configured = true;
+  }
+  if (smem > 227 * 1024) return cudaErrorInvalidValue;
+  lane_epi_kernel<<<(buf.B + kEpiWarps - 1) / kEpiWarps, 32 * kEpiWarps, smem, st>>>(H, S, P, buf, mode);
+  return cudaGetLastError();
 }
 
 cudaError_t launch_fused(const KHand& H, const KObj& O, const SdfSet& sdf, const KSim& S, const KOpt& P,

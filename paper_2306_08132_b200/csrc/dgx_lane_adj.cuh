@@ -1,0 +1,379 @@
+// dgx_lane_adj.cuh — the split adjoint with one THREAD per (candidate, sim).
+// Included by dgx_kernels.cu inside namespace dgx (uses its device helpers).
+//
+// The CTA adjoint (kernel_body<Sdf, kPhaseAdj>) gives each perturbation sim a
+// warp and parallelises the leak recurrence over lanes: every block of 32 S
+// positions is staged, composed into per-lane 3x3 affine maps, scanned across
+// lanes (Kogge-Stone) and re-walked. That parallel prefix costs more than the
+// recurrence itself (ncu, config 3: ~560 thread-instructions per point-sweep,
+// 7 warps / SM at 255 registers, FP64 pipe 28%).
+//
+// Here a thread walks its sim's whole reverse sweep serially, exactly in the
+// reference tape's order (tape.cpp:27-114): per position, the leak geometry of
+// the frozen state (sim.hpp:105-125; the same leak_geo / leak_coef as the CTA
+// adjoint), then adj_x <- adj_x - s n and the point adjoint folded into the
+// per-link force / torque sums. No staging, no map composition, no scan and no
+// shuffles. The 32 lanes of a warp are 32 (candidate, sim) tasks walking the
+// SAME position sequence (sweep * N + i, descending) in lockstep, so the point
+// index, its link and the link-change flushes are warp-uniform; only a lane's
+// logged corrections (its run boundaries) diverge. U positions are processed
+// per step: their geometry is independent (issued together: ILP), the
+// recurrence then applies them in order.
+//
+// Logged corrections and frictions are reversed with the same closed forms as
+// the CTA adjoint (correction_linear, friction_adj; dgx_adjoint.cuh), one
+// thread each. Per-link sums go to task_ft transposed ([6L][tasks]: the
+// warp-uniform flushes are coalesced). lane_epi_kernel then runs each
+// candidate's epilogue (candidate_epilogue: sim-order reductions, FK adjoint,
+// Adam, step) with one warp per candidate.
+//
+// Parity: forward values are untouched (the forward kernel is unchanged);
+// gradients follow the tape's sequential order and match it to rounding
+// (tests/test_gpu_parity.py bars), as the CTA adjoint does.
+#pragma once
+
+constexpr int kLaneAdjThreads = 32;  // one warp per CTA: tasks spread over all SMs' schedulers
+constexpr int kEpiWarps = 4;
+#ifndef DGX_LANE_PREFETCH
+#define DGX_LANE_PREFETCH 16
+#endif
+constexpr int kLanePrefetch = DGX_LANE_PREFETCH;  // points prefetched this many positions ahead
+
+// Geometry prefetch split: grids issue their cell loads for all U positions
+// before finishing any (grid_fetch / grid_finish); other backends classify in
+// one go.
+template <class Sdf>
+struct GeoPre {
+  __device__ __forceinline__ void fetch(const Sdf&, V3) {}
+  __device__ __forceinline__ FastEval finish(const Sdf& s, V3 r, double radius) const { return classify(s, r, radius); }
+};
+template <>
+struct GeoPre<GridSdf> {
+  GridFetch f;
+  __device__ __forceinline__ void fetch(const GridSdf& s, V3 r) { grid_fetch(s, r, f); }
+  __device__ __forceinline__ FastEval finish(const GridSdf& s, V3 r, double radius) const {
+    return grid_finish(s, r, f, radius);
+  }
+};
+
+// Per-thread link accumulator: F_l = sum a_p, T_l = sum p x a_p over the
+// current link, added into the task's transposed row on a link change.
+struct LaneFt {
+  int link = -1;
+  V3 F{0.0, 0.0, 0.0}, T{0.0, 0.0, 0.0};
+  __device__ __forceinline__ void flush(double* ftT, size_t nt) {
+    if (link < 0) return;
+    double* d = ftT + static_cast<size_t>(6 * link) * nt;
+    d[0] += F.x; d[nt] += F.y; d[2 * nt] += F.z;
+    d[3 * nt] += T.x; d[4 * nt] += T.y; d[5 * nt] += T.z;
+    link = -1;
+    F = V3{0.0, 0.0, 0.0};
+    T = V3{0.0, 0.0, 0.0};
+  }
+  __device__ __forceinline__ void add(double* ftT, size_t nt, int l, V3 ap, V3 p) {
+    if (l != link) {
+      flush(ftT, nt);
+      link = l;
+    }
+    F = F + ap;
+    T = T + fcross(p, ap);
+  }
+};
+
+// The leak steps of U consecutive descending positions pos, pos-1, ... (point
+// indices i, i-1, ... wrapping at N) with the frozen state (xk, Rk); slot u
+// takes part iff pos - u > lim (above the lane's next correction). The points
+// kLanePrefetch positions further down are prefetched into L1 (they do not
+// depend on the state; lanes of one candidate share the lines).
+template <int U, bool Prefetch, class Sdf>
+__device__ __forceinline__ void lane_leak_steps(const Sdf& sdf, const SimEnv& e, int pos, int i, int lim, V3 xk,
+                                                const M3& Rk, V3 G, V3& a, M3& aR, LaneFt& acc, double* ftT,
+                                                size_t nt) {
+  if (Prefetch && kLanePrefetch > 0) {
+    int ip = i - kLanePrefetch;
+    if (ip < 0) ip += e.N;
+    asm volatile("prefetch.global.L1 [%0];" ::"l"(e.px + ip));
+    asm volatile("prefetch.global.L1 [%0];" ::"l"(e.py + ip));
+    asm volatile("prefetch.global.L1 [%0];" ::"l"(e.pz + ip));
+  }
+  V3 p[U], rel[U], rl[U];
+  int ii[U];
+  GeoPre<Sdf> pre[U];
+#pragma unroll
+  for (int u = 0; u < U; ++u) {
+    ii[u] = i - u < 0 ? i - u + e.N : i - u;
+    p[u] = V3{e.px[ii[u]], e.py[ii[u]], e.pz[ii[u]]};
+    rel[u] = p[u] - xk;
+    rl[u] = ftmul_add(Rk, rel[u], e.O->com);
+    pre[u].fetch(sdf, rl[u]);
+  }
+  double c1[U], c0[U];
+  V3 n[U], g[U];
+  bool on[U];
+#pragma unroll
+  for (int u = 0; u < U; ++u) {
+    FastEval fe = pre[u].finish(sdf, rl[u], e.radius);
+    double sg = 1.0;
+    g[u] = fe.g;
+    on[u] = pos - u > lim && fe.cls > 0;
+    if (pos - u > lim && fe.cls == 0) {  // near the decision boundary: the exact (bit-exact) query decides
+      // (inline: an out-of-line call here measured 25% slower, its ABI spills)
+      PointEval pe;
+      eval_point(sdf, e, ii[u], xk, Rk, true, pe);
+      on[u] = !(pe.rho_d < 0.0);
+      if (on[u]) {
+        g[u] = pe.q.grad;
+        sg = pe.fb ? static_cast<double>(pe.q.sign) : 1.0;
+      }
+    }
+    n[u] = fmul(Rk, g[u]);
+    // leak_coef (sim.hpp:107-124): s = c1 (n . a) + c0
+    const V3 aa = fcross(rel[u], n[u]);
+    const V3 Ia = fmul(e.O->Iw, aa);
+    const double w = e.O->inv_mass + fdot(aa, Ia);
+    on[u] = on[u] && w >= 1e-12;
+    const double lpc = rcp_fast(w);
+    c1[u] = e.alpha * e.O->inv_mass * lpc * sg;
+    c0[u] = 0.5 * e.alpha * lpc * fdot(aa, G) * sg;
+  }
+#pragma unroll
+  for (int u = 0; u < U; ++u) {
+    if (on[u]) {
+      const double s = fma(c1[u], fdot(n[u], a), c0[u]);
+      a = fma3(-s, n[u], a);
+      const V3 a_rel = n[u] * s;
+      outer_acc(aR, rel[u], g[u] * s);
+      acc.add(ftT, nt, e.sample_link[ii[u]], a_rel, p[u]);
+      add_point_grad(e, ii[u], a_rel);
+    }
+  }
+}
+
+template <class Sdf>
+__global__ void __launch_bounds__(kLaneAdjThreads) lane_adj_kernel(KHand H, const __grid_constant__ KObj O, Sdf sdf,
+                                                                   KSim S, KOpt P, KBuf buf, int mode) {
+  const int M = S.M, N = H.N, L = H.L;
+  const size_t nt = static_cast<size_t>(buf.B) * M;
+  const size_t t = static_cast<size_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (t >= nt) return;  // no warp-collective operations below
+  const int b = static_cast<int>(t / M), m = static_cast<int>(t % M);
+  // a candidate that failed at an earlier iterate of this call stays there
+  if (mode == kModeOpt && P.k_begin > P.traj_k0 && buf.status[b] != kOk) return;
+  double* ftT = buf.task_ft + t;  // entry c of this task: ftT[c * nt]
+  for (int c = 0; c < 6 * L; ++c) ftT[static_cast<size_t>(c) * nt] = 0.0;
+
+  SimEnv e;
+  e.lane = 0;
+  e.N = N;
+  e.gs = S.gs;
+  const double* fkb = buf.fk + static_cast<size_t>(b) * (12 * L + 3 * N);
+  e.px = fkb + 12 * L;
+  e.py = fkb + 12 * L + N;
+  e.pz = fkb + 12 * L + 2 * N;
+  e.sample_link = H.sample_link;
+  e.L = L;
+  e.corr = buf.corr + t * buf.cap_corr;
+  e.slots = buf.slots + t * buf.slot_stride;
+  e.fric_order = buf.fric_order + t * buf.slot_stride;
+  e.cap_corr = buf.cap_corr;
+  e.slot_cap = buf.slot_stride;
+  e.O = &O;
+  e.alpha = S.alpha;
+  e.mu = S.mu;
+  e.dt = S.dt;
+  e.radius = S.radius;
+  if (mode == kModeOpt) {
+    const int k = P.k_begin;
+    e.radius = P.iters > 1 ? P.r0 * (1.0 - static_cast<double>(k) / static_cast<double>(P.iters - 1)) : 0.0;
+  }
+  e.point_grads = buf.point_grads ? buf.point_grads + t * N * 3 : nullptr;
+
+  const FwdRec* rec = buf.fwd + t;
+  int status = rec->status;
+  double residual = rec->residual;
+  if (status == kOk) {
+    // canonical_state (rigid.hpp:29-33) with xdot = v_m; predict (sim.hpp:74-83)
+    const double* vv = m < kMaxSims ? S.vel[m] : S.vel_dev + 3 * m;
+    const V3 v_m{vv[0], vv[1], vv[2]};
+    const V3 prev_x = O.com;
+    const Q4 prev_q{1.0, 0.0, 0.0, 0.0};
+    const V3 prev_thd{0.0, 0.0, 0.0};
+    const V3 pred_xdot = v_m + V3{0.0 * e.dt, 0.0 * e.dt, 0.0 * e.dt};
+    const V3 pred_x = prev_x + pred_xdot * e.dt;
+    const Q4 pred_q = qnormalized(qmul(quat_exp(prev_thd * e.dt), prev_q));
+    const V3 x{rec->x[0], rec->x[1], rec->x[2]};
+    const Q4 q{rec->q[0], rec->q[1], rec->q[2], rec->q[3]};
+    const bool touched = rec->touched != 0;
+    const int ncorr = rec->ncorr, nfric = rec->nfric;
+    // finalize_velocities (sim.hpp:276-287) and the residual (losses.hpp:47-57)
+    V3 xdot, thd;
+    Q4 qd{0.0, 0.0, 0.0, 0.0};
+    const double inv_dt = 1.0 / e.dt;
+    if (!touched) {
+      xdot = pred_xdot;
+      thd = prev_thd;
+    } else {
+      xdot = (x - prev_x) * inv_dt;
+      qd = qmul(q, qconj(prev_q));
+      thd = quat_log(qd) * inv_dt;
+    }
+    const double n1 = norm(xdot), n2 = norm(thd);
+    residual = n1 + n2;
+    if (touched) {  // untouched: constant loss, zero gradient
+      // ---- adjoint: residual -> finalize
+      const V3 a_xdot = n1 > 0.0 ? xdot / n1 : V3{0.0, 0.0, 0.0};
+      const V3 a_thd = n2 > 0.0 ? thd / n2 : V3{0.0, 0.0, 0.0};
+      Q4 aQ = qmul_adj_a(quat_log_adj(qd, a_thd * inv_dt), qconj(prev_q));
+      V3 aX = a_xdot * inv_dt;
+      // ---- friction, reverse (sim.hpp:188-196): the slot's a_lambda / a_n accumulate
+      for (int j = nfric - 1; j >= 0; --j) {
+        SlotRec& s = e.slots[e.fric_order[j]];
+        double a_lam = s.a_lam;
+        V3 a_n{s.a_n[0], s.a_n[1], s.a_n[2]};
+        friction_adj(e, prev_x, prev_q, s, aX, aQ, a_lam, a_n);
+        s.a_lam = a_lam;
+        s.a_n[0] = a_n.x; s.a_n[1] = a_n.y; s.a_n[2] = a_n.z;
+      }
+      // ---- sweeps, reverse: runs of frozen state between logged corrections
+      int k = ncorr - 1;
+      V3 xk = pred_x;
+      Q4 qk = pred_q;
+      auto load_state = [&](int kk) {
+        xk = pred_x;
+        qk = pred_q;
+        if (kk >= 0) {
+          const CorrRec& c = e.corr[kk];
+          xk = V3{c.x[0], c.x[1], c.x[2]};
+          qk = Q4{c.q[0], c.q[1], c.q[2], c.q[3]};
+        }
+      };
+      // theta-axpy coefficient G = Iw^T H, H . k == ([0,k] (x) q_k) . aQ
+      auto g_of = [&](Q4 qq, Q4 aq) {
+        const V3 Hh{-qq.x * aq.w + qq.w * aq.x - qq.z * aq.y + qq.y * aq.z,
+                    -qq.y * aq.w + qq.z * aq.x + qq.w * aq.y - qq.x * aq.z,
+                    -qq.z * aq.w - qq.y * aq.x + qq.x * aq.y + qq.w * aq.z};
+        return ftmul(e.O->Iw, Hh);
+      };
+      load_state(k);
+      M3 Rk = rotation_matrix(qk);
+      V3 G = g_of(qk, aQ);
+      int next_f = k >= 0 ? e.corr[k].f : -1;
+      M3 aR;
+      for (int r = 0; r < 9; ++r) aR.m[r] = 0.0;
+      LaneFt acc;
+      int i = N - 1;
+      for (int pos = S.gs * N - 1; pos >= 0; pos -= kLaneU) {
+        lane_leak_steps<kLaneU, true>(sdf, e, pos, i, max(next_f, pos - kLaneU), xk, Rk, G, aX, aR, acc, ftT, nt);
+        // this lane's logged corrections inside the window (divergent; rare)
+        while (next_f > pos - kLaneU) {
+          const int f = next_f;
+          // R node of the state after correction k (read by the run above it)
+          aQ = qadd(aQ, rotmat_adj(qk, aR));
+          const CorrRec& c = e.corr[k];
+          const SlotRec& sl = e.slots[c.slot];
+          load_state(k - 1);
+          bool ok = true;
+          const CorrLin o = correction_linear(e, c, xk, qk, aX, aQ, sl.a_lam,
+                                              sl.last_corr == k ? V3{sl.a_n[0], sl.a_n[1], sl.a_n[2]}
+                                                                : V3{0.0, 0.0, 0.0},
+                                              ok);
+          if (!ok) status = kReplayMismatch;
+          aX = o.aX;
+          aQ = o.aQ;
+          aR = o.aR;  // R node of the state before it (continued by the run below)
+          {
+            const int ip = f % N;
+            const V3 pp{e.px[ip], e.py[ip], e.pz[ip]};
+            double* d = ftT + static_cast<size_t>(6 * e.sample_link[ip]) * nt;
+            const V3 tq = cross(pp, o.a_rel);
+            d[0] += o.a_rel.x; d[nt] += o.a_rel.y; d[2 * nt] += o.a_rel.z;
+            d[3 * nt] += tq.x; d[4 * nt] += tq.y; d[5 * nt] += tq.z;
+            add_point_grad(e, ip, o.a_rel);
+          }
+          --k;
+          Rk = rotation_matrix(qk);
+          G = g_of(qk, aQ);
+          next_f = k >= 0 ? e.corr[k].f : -1;
+          // the window's positions below the correction, with the state before it
+          for (int p2 = f - 1; p2 > pos - kLaneU && p2 > next_f; --p2)
+            lane_leak_steps<1, false>(sdf, e, p2, p2 % N, next_f, xk, Rk, G, aX, aR, acc, ftT, nt);
+        }
+        i -= kLaneU;
+        if (i < 0) i += N;
+      }
+      acc.flush(ftT, nt);
+      if (S.discard) {  // this sim's logs are consumed
+        l2_discard(e.corr, static_cast<size_t>(ncorr) * sizeof(CorrRec), 0, 1);
+        l2_discard(e.slots, static_cast<size_t>(rec->nslot) * sizeof(SlotRec), 0, 1);
+      }
+    }
+  }
+  buf.task_res[t] = residual;
+  buf.task_stat[t] = status;
+  if (buf.sim_res) buf.sim_res[t] = residual;
+}
+
+// Per-candidate epilogue after lane_adj_kernel: one warp per candidate.
+// Shared memory per warp (doubles): ft_all [M][6L], sres [M], sflag [M] (ints
+// in M doubles), scratch [6L + kMaxDim], sg [96], sq [40].
+__host__ __device__ inline int lane_epi_doubles(int M, int L) { return M * 6 * L + 2 * M + 6 * L + kMaxDim + 96 + 40; }
+
+__global__ void __launch_bounds__(32 * kEpiWarps) lane_epi_kernel(KHand H, KSim S, KOpt P, KBuf buf, int mode) {
+  extern __shared__ __align__(16) unsigned char smem[];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int M = S.M, N = H.N, L = H.L, J = H.J, D = 6 + J, Qd = 7 + J;
+  const int b = static_cast<int>(blockIdx.x) * kEpiWarps + warp;
+  if (b >= buf.B) return;  // warp-uniform
+  if (mode == kModeOpt && P.k_begin > P.traj_k0 && buf.status[b] != kOk) return;
+  double* wb = reinterpret_cast<double*>(smem) + static_cast<size_t>(warp) * lane_epi_doubles(M, L);
+  double* ft_all = wb;
+  double* sres = ft_all + M * 6 * L;
+  int* sflag = reinterpret_cast<int*>(sres + M);
+  double* scratch = sres + 2 * M;
+  double* sg = scratch + 6 * L + kMaxDim;
+  double* sq = sg + 96;
+  const size_t nt = static_cast<size_t>(buf.B) * M, b0 = static_cast<size_t>(b) * M;
+  for (int x = lane; x < M * 6 * L; x += 32) {
+    const int mm = x / (6 * L), c = x - mm * 6 * L;
+    ft_all[x] = __ldcg(buf.task_ft + static_cast<size_t>(c) * nt + b0 + mm);
+  }
+  for (int x = lane; x < M; x += 32) {
+    sres[x] = __ldcg(buf.task_res + b0 + x);
+    sflag[x] = __ldcg(buf.task_stat + b0 + x);
+  }
+  if (lane < Qd) sq[lane] = buf.q[static_cast<size_t>(b) * Qd + lane];
+  double am = 0.0, av = 0.0, b1t = 1.0, b2t = 1.0;
+  if (mode == kModeOpt) {
+    if (lane < D) {
+      am = buf.adam_m[static_cast<size_t>(b) * D + lane];
+      av = buf.adam_v[static_cast<size_t>(b) * D + lane];
+    }
+    for (int kk = 0; kk < P.k_begin; ++kk) { b1t = b1t * P.beta1; b2t = b2t * P.beta2; }
+  }
+  __syncwarp();
+  const double* link = buf.fk + static_cast<size_t>(b) * (12 * L + 3 * N);
+  if (buf.sim_grads && mode != kModeEval) {  // debug: per-perturbation gradient via the FK adjoint
+    for (int mm = 0; mm < M; ++mm) {
+      for (int x = lane; x < 6 * L; x += 32) scratch[x] = ft_all[mm * 6 * L + x];
+      __syncwarp();
+      fk_adjoint(H, sq, link, scratch, sg, lane);
+      for (int x = lane; x < D; x += 32) buf.sim_grads[(b0 + mm) * D + x] = sg[x];
+      __syncwarp();
+    }
+  }
+  int cand_status = kOk;
+  const int k = mode == kModeOpt ? P.k_begin : 0;
+  candidate_epilogue(H, S, P, buf, mode, b, k, lane, sflag, sres, ft_all, link, scratch, sg, sq, am, av, b1t, b2t,
+                     cand_status);
+  __syncwarp();
+  if (mode == kModeOpt) {
+    if (lane < Qd) buf.q[static_cast<size_t>(b) * Qd + lane] = sq[lane];
+    if (lane < D) {
+      buf.adam_m[static_cast<size_t>(b) * D + lane] = am;
+      buf.adam_v[static_cast<size_t>(b) * D + lane] = av;
+    }
+  }
+  if (lane == 0) buf.status[b] = cand_status;
+  __syncwarp();
+  if (S.discard) l2_discard(link, sizeof(double) * (12 * L + 3 * N), lane, 32);  // FK record consumed
+}

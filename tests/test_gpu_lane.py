@@ -1,0 +1,108 @@
+"""The lane adjoint (csrc/dgx_lane_adj.cuh: one thread per (candidate, sim),
+the reverse sweep walked serially in the tape's order) against the compiled
+reference and against the CTA adjoint, forced through dgx_ctx_set_adjoint on
+batches above the SM count (the split path) for every SDF backend it serves.
+
+Bars: losses and per-sim residuals BIT-EXACT (the forward kernel is shared);
+gradients within GRAD_RTOL of the reference tape (sim.hpp:105-125,
+tape.cpp:27-114) and within LANE_VS_CTA_RTOL of the CTA adjoint (the same
+closed forms, summed in a different order); rows of identical configurations
+bit-identical wherever they sit in the batch.
+"""
+import numpy as np
+import pytest
+
+from test_gpu_configs import Setup
+from test_gpu_parity import GRAD_RTOL, relerr
+
+pytestmark = pytest.mark.gpu
+LANE_VS_CTA_RTOL = 1e-11
+TILE = 21  # 8 distinct rows x 21 = 168 candidates > 148 SMs: split execution
+
+
+def _object(name):
+    from paper_2306_08132_b200 import model
+    return {"sphere": lambda: model.sphere(0.025), "box": lambda: model.box((0.04, 0.06, 0.05)),
+            "boxgrid64": lambda: model.box_grid(res=64), "cylinder64": lambda: model.cylinder_grid(res=64),
+            "blob128": lambda: model.blob_grid(seed=3, res=128)}[name]()
+
+
+def _run(ctx, variant, fn):
+    ctx.set_adjoint(variant)
+    ctx.set_kernel_timing(True)
+    try:
+        out = fn()
+        kt = ctx.kernel_times()
+    finally:
+        ctx.set_kernel_timing(False)
+        ctx.set_adjoint("auto")
+    assert kt["adjoint"][1] >= 1 and kt["fused"][1] == 0, kt  # the split path ran
+    return out
+
+
+CASES = [("barrett3", "sphere", 0.01), ("barrett3", "box", 0.0), ("allegro16", "boxgrid64", 0.02),
+         ("allegro16", "cylinder64", 0.015), ("shadow22_dense", "blob128", 0.02)]
+
+
+@pytest.mark.parametrize("hand_name,obj_name,radius", CASES)
+def test_lane_adjoint_loss_gradient(ctx, oracle, hand_name, obj_name, radius):
+    from paper_2306_08132_b200 import api
+    s = Setup(ctx, oracle, hand_name, _object(obj_name), B=8, seed=91)
+    q = np.tile(s.q, (TILE, 1))
+    proto, params = api.StabilityProtocol.standard(), api.SimParams(dilation_radius=radius)
+    lg = lambda: api.loss_gradient(ctx, s.obj, s.hand, q, proto, params)  # noqa: E731
+    ll, gl, stl = _run(ctx, "lane", lg)
+    lc, gc, stc = _run(ctx, "cta", lg)
+    assert not np.any(stl) and not np.any(stc)
+    assert np.array_equal(ll, lc)
+    assert relerr(gl, gc) < LANE_VS_CTA_RTOL, relerr(gl, gc)
+    for t in range(1, TILE):  # position in the batch does not matter
+        assert np.array_equal(gl[8 * t:8 * t + 8], gl[:8])
+    p = oracle.default_params(dilation_radius=radius)
+    for b in range(8):
+        rl, ds, dr, dl = oracle.loss_gradient(s.ro, s.rh, s.q[b], p)
+        assert np.array_equal(ll[b], rl), (b, ll[b], rl)
+        assert relerr(gl[b, 0], ds) < GRAD_RTOL, (b, relerr(gl[b, 0], ds))
+        assert relerr(gl[b, 1], dr) < GRAD_RTOL
+        assert np.array_equal(gl[b, 2], dl)
+
+
+def test_lane_adjoint_per_sim_and_point_gradients(ctx, oracle):
+    """dgx_debug_sims through the lane adjoint: per-perturbation residuals,
+    gradients (sim_grads) and d residual / d p (point_grads) vs the tape."""
+    from paper_2306_08132_b200 import api
+    s = Setup(ctx, oracle, "allegro16", _object("boxgrid64"), B=8, seed=92)
+    q = np.tile(s.q, (TILE, 1))
+    proto, params = api.StabilityProtocol.standard(), api.SimParams(dilation_radius=0.02)
+    res, g, gp, st = _run(ctx, "lane", lambda: api.debug_sims(ctx, s.obj, s.hand, q, proto, params, point_grads=True))
+    assert not np.any(st)
+    p = oracle.default_params(dilation_radius=0.02)
+    for b in range(3):
+        for m in range(7):
+            rres, rg, rgp, _ = oracle.sim_record(s.ro, s.rh, s.q[b], m, p, points_grad=True)
+            assert res[b, m] == rres and res[b + 8, m] == rres
+            assert relerr(g[b, m], rg) < GRAD_RTOL, (b, m)
+            assert relerr(gp[b, m], rgp) < GRAD_RTOL, (b, m)
+
+
+@pytest.mark.parametrize("hand_name,obj_name", [("allegro16", "boxgrid64"), ("barrett3", "sphere")])
+def test_lane_adjoint_optimizer_teacher_forced(ctx, oracle, hand_name, obj_name):
+    """Two optimizer iterates (Adam state carried on the device) through the
+    lane adjoint; each iterate's rows vs the reference optimizer step from the
+    same state (losses bit-exact, gradients / q / Adam m within GRAD_RTOL)."""
+    from paper_2306_08132_b200 import api
+    s = Setup(ctx, oracle, hand_name, _object(obj_name), B=8, seed=93)
+    q = np.tile(s.q, (TILE, 1))
+    m = v = None
+    for k in (0, 1):
+        out = _run(ctx, "lane", lambda: api.optimize(
+            ctx, s.obj, s.hand, q, api.StabilityProtocol.standard(), api.SimParams(), api.LossWeights(),
+            api.OptConfig(iterations=500), k_begin=k, k_end=k + 1, adam_m=m, adam_v=v, record=True))
+        assert not np.any(out["status"])
+        r = oracle.optimize(s.ro, s.rh, q[:8], oracle.default_params(), iters=500, k_begin=k, k_end=k + 1,
+                            adam_m=None if m is None else m[:8], adam_v=None if v is None else v[:8], record=True)
+        assert np.array_equal(out["traj"][:8, :, :3], r["losses"])
+        assert relerr(out["traj"][:8, :, 3:], r["grads"]) < GRAD_RTOL
+        assert relerr(out["q"][:8], r["q"]) < GRAD_RTOL
+        assert relerr(out["m"][:8], r["m"]) < GRAD_RTOL
+        q, m, v = out["q"], out["m"], out["v"]

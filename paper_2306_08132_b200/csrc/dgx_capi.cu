@@ -322,7 +322,7 @@ SplitGrid prepare_split(dgx_ctx* c, Scratch& sc, const dgx_hand* h, const dgx_ob
   int av = adjoint_variant();
   if (av == 3 && c->adjoint != DGX_ADJOINT_AUTO) av = c->adjoint == DGX_ADJOINT_LANE ? 2 : 0;
   g.task = record && av == 1;
-  g.lane = record && N >= kLaneU &&
+  g.lane = record && N >= 32 &&  // (the lane adjoint stages 32-position blocks)
            (av == 2 || (av == 3 && static_cast<long long>(B) * M >=
                                        static_cast<long long>(kLaneMinWarpsPerSm) * 32 * c->num_sms));
   if (g.lane) {

@@ -2678,7 +2678,7 @@ static cudaError_t launch_lane_t(const KHand& H, const KObj& O, const Sdf& sdf, 
   if constexpr (kSplitCapable<Sdf>) {
     const long long nt = static_cast<long long>(buf.B) * S.M;
     const int grid = static_cast<int>((nt + kLaneAdjThreads - 1) / kLaneAdjThreads);
-    lane_adj_kernel<Sdf><<<grid, kLaneAdjThreads, 0, st>>>(H, O, sdf, S, P, buf, mode);
+    lane_adj_kernel<Sdf><<<grid, kLaneAdjThreads, lane_smem_bytes(S.M), st>>>(H, O, sdf, S, P, buf, mode);
     return cudaGetLastError();
   }
   return cudaErrorInvalidValue;

@@ -34,10 +34,19 @@
 
 constexpr int kLaneAdjThreads = 32;  // one warp per CTA: tasks spread over all SMs' schedulers
 constexpr int kEpiWarps = 4;
-#ifndef DGX_LANE_PREFETCH
-#define DGX_LANE_PREFETCH 16
+static_assert(kLaneAdjThreads == 32 && 32 % kLaneU == 0, "lane adjoint: one warp per CTA, windows tile 32-position blocks");
+// staged points: per buffer and candidate of the warp a row of x / y / z for
+// 32 positions; rows 98 doubles apart (196 words: the warp's <= 6 candidates
+// fall on distinct banks)
+constexpr int kLaneRowArr = 32, kLaneRow = 3 * kLaneRowArr + 2;
+__host__ __device__ inline int lane_cands_per_warp(int M) { return (31 / M + 2) < 32 ? (31 / M + 2) : 32; }
+__host__ __device__ inline int lane_smem_bytes(int M) { return 2 * lane_cands_per_warp(M) * kLaneRow * 8; }
+#ifndef DGX_LANE_CELL_NOL1
+#define DGX_LANE_CELL_NOL1 0
 #endif
-constexpr int kLanePrefetch = DGX_LANE_PREFETCH;  // points prefetched this many positions ahead
+// cell loads: 0 plain (L1 reuse between consecutive points: no_allocate measured
+// 35.9 vs 30.9 ms), 1 L1::no_allocate, 2 L1::evict_first
+constexpr int kLaneCellNoL1 = DGX_LANE_CELL_NOL1;
 
 // Geometry prefetch split: grids issue their cell loads for all U positions
 // before finishing any (grid_fetch / grid_finish); other backends classify in
@@ -50,7 +59,7 @@ struct GeoPre {
 template <>
 struct GeoPre<GridSdf> {
   GridFetch f;
-  __device__ __forceinline__ void fetch(const GridSdf& s, V3 r) { grid_fetch(s, r, f); }
+  __device__ __forceinline__ void fetch(const GridSdf& s, V3 r) { grid_fetch<kLaneCellNoL1>(s, r, f); }
   __device__ __forceinline__ FastEval finish(const GridSdf& s, V3 r, double radius) const {
     return grid_finish(s, r, f, radius);
   }
@@ -83,26 +92,19 @@ struct LaneFt {
 // The leak steps of U consecutive descending positions pos, pos-1, ... (point
 // indices i, i-1, ... wrapping at N) with the frozen state (xk, Rk); slot u
 // takes part iff pos - u > lim (above the lane's next correction). The points
-// kLanePrefetch positions further down are prefetched into L1 (they do not
-// depend on the state; lanes of one candidate share the lines).
-template <int U, bool Prefetch, class Sdf>
+// come from the warp's staged block (ps: this lane's candidate row, x / y / z
+// at ps[0 / kLaneRowArr / 2 kLaneRowArr + j], j = jb + u).
+template <int U, class Sdf>
 __device__ __forceinline__ void lane_leak_steps(const Sdf& sdf, const SimEnv& e, int pos, int i, int lim, V3 xk,
                                                 const M3& Rk, V3 G, V3& a, M3& aR, LaneFt& acc, double* ftT,
-                                                size_t nt) {
-  if (Prefetch && kLanePrefetch > 0) {
-    int ip = i - kLanePrefetch;
-    if (ip < 0) ip += e.N;
-    asm volatile("prefetch.global.L1 [%0];" ::"l"(e.px + ip));
-    asm volatile("prefetch.global.L1 [%0];" ::"l"(e.py + ip));
-    asm volatile("prefetch.global.L1 [%0];" ::"l"(e.pz + ip));
-  }
+                                                size_t nt, const double* ps, int jb) {
   V3 p[U], rel[U], rl[U];
   int ii[U];
   GeoPre<Sdf> pre[U];
 #pragma unroll
   for (int u = 0; u < U; ++u) {
     ii[u] = i - u < 0 ? i - u + e.N : i - u;
-    p[u] = V3{e.px[ii[u]], e.py[ii[u]], e.pz[ii[u]]};
+    p[u] = V3{ps[jb + u], ps[kLaneRowArr + jb + u], ps[2 * kLaneRowArr + jb + u]};
     rel[u] = p[u] - xk;
     rl[u] = ftmul_add(Rk, rel[u], e.O->com);
     pre[u].fetch(sdf, rl[u]);
@@ -152,15 +154,25 @@ __device__ __forceinline__ void lane_leak_steps(const Sdf& sdf, const SimEnv& e,
 template <class Sdf>
 __global__ void __launch_bounds__(kLaneAdjThreads) lane_adj_kernel(KHand H, const __grid_constant__ KObj O, Sdf sdf,
                                                                    KSim S, KOpt P, KBuf buf, int mode) {
+  extern __shared__ __align__(16) unsigned char smem[];
   const int M = S.M, N = H.N, L = H.L;
   const size_t nt = static_cast<size_t>(buf.B) * M;
-  const size_t t = static_cast<size_t>(blockIdx.x) * blockDim.x + threadIdx.x;
-  if (t >= nt) return;  // no warp-collective operations below
-  const int b = static_cast<int>(t / M), m = static_cast<int>(t % M);
+  const int lane = static_cast<int>(threadIdx.x);  // one warp per CTA
+  const size_t t0 = static_cast<size_t>(blockIdx.x) * kLaneAdjThreads;
+  const size_t t = t0 + lane;
+  // every lane stays to the end (the warp stages points together); lanes past
+  // the batch, of skipped candidates or of sims without an adjoint idle
+  const bool in = t < nt;
+  const size_t tc = in ? t : nt - 1;
+  const int b = static_cast<int>(tc / M), m = static_cast<int>(tc % M);
+  const int b_first = static_cast<int>(t0 / M);
+  const size_t t_last = t0 + kLaneAdjThreads - 1 < nt ? t0 + kLaneAdjThreads - 1 : nt - 1;
+  const int ncw = static_cast<int>(t_last / M) - b_first + 1;
   // a candidate that failed at an earlier iterate of this call stays there
-  if (mode == kModeOpt && P.k_begin > P.traj_k0 && buf.status[b] != kOk) return;
-  double* ftT = buf.task_ft + t;  // entry c of this task: ftT[c * nt]
-  for (int c = 0; c < 6 * L; ++c) ftT[static_cast<size_t>(c) * nt] = 0.0;
+  const bool skip = !in || (mode == kModeOpt && P.k_begin > P.traj_k0 && buf.status[b] != kOk);
+  double* ftT = buf.task_ft + tc;  // entry c of this task: ftT[c * nt]
+  if (!skip)
+    for (int c = 0; c < 6 * L; ++c) ftT[static_cast<size_t>(c) * nt] = 0.0;
 
   SimEnv e;
   e.lane = 0;
@@ -172,9 +184,9 @@ __global__ void __launch_bounds__(kLaneAdjThreads) lane_adj_kernel(KHand H, cons
   e.pz = fkb + 12 * L + 2 * N;
   e.sample_link = H.sample_link;
   e.L = L;
-  e.corr = buf.corr + t * buf.cap_corr;
-  e.slots = buf.slots + t * buf.slot_stride;
-  e.fric_order = buf.fric_order + t * buf.slot_stride;
+  e.corr = buf.corr + tc * buf.cap_corr;
+  e.slots = buf.slots + tc * buf.slot_stride;
+  e.fric_order = buf.fric_order + tc * buf.slot_stride;
   e.cap_corr = buf.cap_corr;
   e.slot_cap = buf.slot_stride;
   e.O = &O;
@@ -186,25 +198,29 @@ __global__ void __launch_bounds__(kLaneAdjThreads) lane_adj_kernel(KHand H, cons
     const int k = P.k_begin;
     e.radius = P.iters > 1 ? P.r0 * (1.0 - static_cast<double>(k) / static_cast<double>(P.iters - 1)) : 0.0;
   }
-  e.point_grads = buf.point_grads ? buf.point_grads + t * N * 3 : nullptr;
+  e.point_grads = buf.point_grads ? buf.point_grads + tc * N * 3 : nullptr;
 
-  const FwdRec* rec = buf.fwd + t;
+  const FwdRec* rec = buf.fwd + tc;
   int status = rec->status;
   double residual = rec->residual;
-  if (status == kOk) {
-    // canonical_state (rigid.hpp:29-33) with xdot = v_m; predict (sim.hpp:74-83)
-    const double* vv = m < kMaxSims ? S.vel[m] : S.vel_dev + 3 * m;
-    const V3 v_m{vv[0], vv[1], vv[2]};
-    const V3 prev_x = O.com;
-    const Q4 prev_q{1.0, 0.0, 0.0, 0.0};
-    const V3 prev_thd{0.0, 0.0, 0.0};
-    const V3 pred_xdot = v_m + V3{0.0 * e.dt, 0.0 * e.dt, 0.0 * e.dt};
-    const V3 pred_x = prev_x + pred_xdot * e.dt;
-    const Q4 pred_q = qnormalized(qmul(quat_exp(prev_thd * e.dt), prev_q));
+  // canonical_state (rigid.hpp:29-33) with xdot = v_m; predict (sim.hpp:74-83)
+  const double* vv = m < kMaxSims ? S.vel[m] : S.vel_dev + 3 * m;
+  const V3 v_m{vv[0], vv[1], vv[2]};
+  const V3 prev_x = O.com;
+  const Q4 prev_q{1.0, 0.0, 0.0, 0.0};
+  const V3 prev_thd{0.0, 0.0, 0.0};
+  const V3 pred_xdot = v_m + V3{0.0 * e.dt, 0.0 * e.dt, 0.0 * e.dt};
+  const V3 pred_x = prev_x + pred_xdot * e.dt;
+  const Q4 pred_q = qnormalized(qmul(quat_exp(prev_thd * e.dt), prev_q));
+  bool live = false;  // this lane walks the reverse sweep
+  V3 aX{0.0, 0.0, 0.0};
+  Q4 aQ{0.0, 0.0, 0.0, 0.0};
+  const int ncorr = rec->ncorr;
+  if (!skip && status == kOk) {
     const V3 x{rec->x[0], rec->x[1], rec->x[2]};
     const Q4 q{rec->q[0], rec->q[1], rec->q[2], rec->q[3]};
     const bool touched = rec->touched != 0;
-    const int ncorr = rec->ncorr, nfric = rec->nfric;
+    const int nfric = rec->nfric;
     // finalize_velocities (sim.hpp:276-287) and the residual (losses.hpp:47-57)
     V3 xdot, thd;
     Q4 qd{0.0, 0.0, 0.0, 0.0};
@@ -219,12 +235,13 @@ __global__ void __launch_bounds__(kLaneAdjThreads) lane_adj_kernel(KHand H, cons
     }
     const double n1 = norm(xdot), n2 = norm(thd);
     residual = n1 + n2;
-    if (touched) {  // untouched: constant loss, zero gradient
+    live = touched;  // untouched: constant loss, zero gradient
+    if (live) {
       // ---- adjoint: residual -> finalize
       const V3 a_xdot = n1 > 0.0 ? xdot / n1 : V3{0.0, 0.0, 0.0};
       const V3 a_thd = n2 > 0.0 ? thd / n2 : V3{0.0, 0.0, 0.0};
-      Q4 aQ = qmul_adj_a(quat_log_adj(qd, a_thd * inv_dt), qconj(prev_q));
-      V3 aX = a_xdot * inv_dt;
+      aQ = qmul_adj_a(quat_log_adj(qd, a_thd * inv_dt), qconj(prev_q));
+      aX = a_xdot * inv_dt;
       // ---- friction, reverse (sim.hpp:188-196): the slot's a_lambda / a_n accumulate
       for (int j = nfric - 1; j >= 0; --j) {
         SlotRec& s = e.slots[e.fric_order[j]];
@@ -234,36 +251,76 @@ __global__ void __launch_bounds__(kLaneAdjThreads) lane_adj_kernel(KHand H, cons
         s.a_lam = a_lam;
         s.a_n[0] = a_n.x; s.a_n[1] = a_n.y; s.a_n[2] = a_n.z;
       }
-      // ---- sweeps, reverse: runs of frozen state between logged corrections
-      int k = ncorr - 1;
-      V3 xk = pred_x;
-      Q4 qk = pred_q;
-      auto load_state = [&](int kk) {
-        xk = pred_x;
-        qk = pred_q;
-        if (kk >= 0) {
-          const CorrRec& c = e.corr[kk];
-          xk = V3{c.x[0], c.x[1], c.x[2]};
-          qk = Q4{c.q[0], c.q[1], c.q[2], c.q[3]};
-        }
-      };
-      // theta-axpy coefficient G = Iw^T H, H . k == ([0,k] (x) q_k) . aQ
-      auto g_of = [&](Q4 qq, Q4 aq) {
-        const V3 Hh{-qq.x * aq.w + qq.w * aq.x - qq.z * aq.y + qq.y * aq.z,
-                    -qq.y * aq.w + qq.z * aq.x + qq.w * aq.y - qq.x * aq.z,
-                    -qq.z * aq.w - qq.y * aq.x + qq.x * aq.y + qq.w * aq.z};
-        return ftmul(e.O->Iw, Hh);
-      };
-      load_state(k);
-      M3 Rk = rotation_matrix(qk);
-      V3 G = g_of(qk, aQ);
-      int next_f = k >= 0 ? e.corr[k].f : -1;
-      M3 aR;
-      for (int r = 0; r < 9; ++r) aR.m[r] = 0.0;
-      LaneFt acc;
-      int i = N - 1;
-      for (int pos = S.gs * N - 1; pos >= 0; pos -= kLaneU) {
-        lane_leak_steps<kLaneU, true>(sdf, e, pos, i, max(next_f, pos - kLaneU), xk, Rk, G, aX, aR, acc, ftT, nt);
+    }
+  }
+  // ---- sweeps, reverse: runs of frozen state between logged corrections.
+  // The warp walks positions gs N - 1 .. 0 in lockstep; the points of each
+  // block of 32 positions are staged in shared memory for the warp's
+  // candidates (cp.async, double-buffered: the next block is in flight while
+  // this one is processed).
+  if (__any_sync(kFull, live)) {
+    double* sb = reinterpret_cast<double*>(smem);
+    const int rows = ncw * kLaneRow;  // doubles per buffer
+    const int top = S.gs * N - 1;
+    auto stage = [&](int blk_top, int bi) {  // positions blk_top - 31 .. blk_top into buffer bi
+      const int itop = blk_top % N;
+      for (int x = lane; x < ncw * 3 * 32; x += 32) {
+        const int c = x / 96, r = x - 96 * c, arr = r >> 5, j = r & 31;
+        if (blk_top - j < 0) continue;
+        int ij = itop - j;
+        if (ij < 0) ij += N;
+        const double* src = buf.fk + static_cast<size_t>(b_first + c) * (12 * L + 3 * N) + 12 * L +
+                            static_cast<size_t>(arr) * N + ij;
+        const double* dst = sb + bi * rows + c * kLaneRow + arr * kLaneRowArr + j;
+        const unsigned sa = static_cast<unsigned>(__cvta_generic_to_shared(dst));
+        asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(sa), "l"(src) : "memory");
+      }
+      asm volatile("cp.async.commit_group;" ::: "memory");
+    };
+    int k = ncorr - 1;
+    V3 xk = pred_x;
+    Q4 qk = pred_q;
+    auto load_state = [&](int kk) {
+      xk = pred_x;
+      qk = pred_q;
+      if (kk >= 0) {
+        const CorrRec& c = e.corr[kk];
+        xk = V3{c.x[0], c.x[1], c.x[2]};
+        qk = Q4{c.q[0], c.q[1], c.q[2], c.q[3]};
+      }
+    };
+    // theta-axpy coefficient G = Iw^T H, H . k == ([0,k] (x) q_k) . aQ
+    auto g_of = [&](Q4 qq, Q4 aq) {
+      const V3 Hh{-qq.x * aq.w + qq.w * aq.x - qq.z * aq.y + qq.y * aq.z,
+                  -qq.y * aq.w + qq.z * aq.x + qq.w * aq.y - qq.x * aq.z,
+                  -qq.z * aq.w - qq.y * aq.x + qq.x * aq.y + qq.w * aq.z};
+      return ftmul(e.O->Iw, Hh);
+    };
+    if (live) load_state(k);
+    M3 Rk = rotation_matrix(qk);
+    V3 G = g_of(qk, aQ);
+    int next_f = live && k >= 0 ? e.corr[k].f : -1;
+    M3 aR;
+    for (int r = 0; r < 9; ++r) aR.m[r] = 0.0;
+    LaneFt acc;
+    int i = N - 1;
+    stage(top, 0);
+    int blk = 0, blk_top = top;
+    const double* ps = sb;
+    for (int pos = top; pos >= 0; pos -= kLaneU) {
+      if (((top - pos) & 31) == 0) {  // next block: stage the one after it, wait for this one
+        __syncwarp();  // every lane is done with the buffer about to be refilled
+        if (pos - 32 >= 0) stage(pos - 32, (blk + 1) & 1);
+        else asm volatile("cp.async.commit_group;" ::: "memory");
+        asm volatile("cp.async.wait_group 1;" ::: "memory");
+        __syncwarp();
+        ps = sb + (blk & 1) * rows + (b - b_first) * kLaneRow;
+        blk_top = pos;
+        ++blk;
+      }
+      if (live) {
+        lane_leak_steps<kLaneU>(sdf, e, pos, i, max(next_f, pos - kLaneU), xk, Rk, G, aX, aR, acc, ftT, nt, ps,
+                                blk_top - pos);
         // this lane's logged corrections inside the window (divergent; rare)
         while (next_f > pos - kLaneU) {
           const int f = next_f;
@@ -296,11 +353,14 @@ __global__ void __launch_bounds__(kLaneAdjThreads) lane_adj_kernel(KHand H, cons
           next_f = k >= 0 ? e.corr[k].f : -1;
           // the window's positions below the correction, with the state before it
           for (int p2 = f - 1; p2 > pos - kLaneU && p2 > next_f; --p2)
-            lane_leak_steps<1, false>(sdf, e, p2, p2 % N, next_f, xk, Rk, G, aX, aR, acc, ftT, nt);
+            lane_leak_steps<1>(sdf, e, p2, p2 % N, next_f, xk, Rk, G, aX, aR, acc, ftT, nt, ps, blk_top - p2);
         }
-        i -= kLaneU;
-        if (i < 0) i += N;
       }
+      i -= kLaneU;
+      if (i < 0) i += N;
+    }
+    asm volatile("cp.async.wait_all;" ::: "memory");
+    if (live) {
       acc.flush(ftT, nt);
       if (S.discard) {  // this sim's logs are consumed
         l2_discard(e.corr, static_cast<size_t>(ncorr) * sizeof(CorrRec), 0, 1);
@@ -308,6 +368,7 @@ __global__ void __launch_bounds__(kLaneAdjThreads) lane_adj_kernel(KHand H, cons
       }
     }
   }
+  if (skip) return;
   buf.task_res[t] = residual;
   buf.task_stat[t] = status;
   if (buf.sim_res) buf.sim_res[t] = residual;

@@ -10,6 +10,7 @@
 #include <cstdlib>
 #include <stdexcept>
 #include <string>
+#include <limits>
 #include <vector>
 
 #include "../../include/dgx.h"
@@ -120,6 +121,7 @@ struct dgx_object {
   int kind;
   SdfSet sdf{};
   DevBuf vals;  // grid values, or the mesh block (nodes, faces, tri, vx, vn, MeshGeom)
+  DevBuf bmin;  // grids: block lower bounds of the forward pre-filter (GridSdf::bmin)
   KObj k;
   // mesh objects: device vertices + count (table-contact samples of the drop)
   const double* mesh_vx = nullptr;
@@ -853,6 +855,37 @@ int dgx_object_upload(dgx_ctx* c, const dgx_object_desc* d, dgx_object** out) {
                              static_cast<const float*>(o->vals.p), dcells, pairs, static_cast<float>(d->origin[0]),
                              static_cast<float>(d->origin[1]), static_cast<float>(d->origin[2]),
                              static_cast<float>(d->spacing), static_cast<float>(d->inv_spacing)};
+        // block lower bounds for the forward pre-filter (GridSdf::bmin): blocks of
+        // 2^bs cells per axis, each the min over its nodes widened by one node
+        // ~16 blocks along the largest axis (measured: 64^3 with 4-cell blocks
+        // forward 1.61 -> 1.40 ms, 128^3 with 8-cell blocks 20.3 -> 17.4 ms per
+        // 4096-candidate step; 8-cell blocks on 64^3 gain nothing)
+        const int nmax = std::max(nx, std::max(ny, nz)) - 1;
+        int bs = std::max(1, static_cast<int>(std::lround(std::log2(nmax / 16.0))));
+        if (const char* ev = std::getenv("DGX_GRID_BLOCK")) bs = std::atoi(ev);  // 0: off (A/B)
+        if (bs > 0) {
+          const int bnx = ((nx - 2) >> bs) + 1, bny = ((ny - 2) >> bs) + 1, bnz = ((nz - 2) >> bs) + 1;
+          std::vector<float> bm(static_cast<size_t>(bnx) * bny * bnz);
+          for (int bk = 0; bk < bnz; ++bk)
+            for (int bj = 0; bj < bny; ++bj)
+              for (int bi = 0; bi < bnx; ++bi) {
+                float mn = std::numeric_limits<float>::infinity();
+                const int i0 = std::max(0, (bi << bs) - 1), i1 = std::min(nx - 1, ((bi + 1) << bs) + 1);
+                const int j0 = std::max(0, (bj << bs) - 1), j1 = std::min(ny - 1, ((bj + 1) << bs) + 1);
+                const int k0 = std::max(0, (bk << bs) - 1), k1 = std::min(nz - 1, ((bk + 1) << bs) + 1);
+                for (int k = k0; k <= k1; ++k)
+                  for (int j = j0; j <= j1; ++j)
+                    for (int i = i0; i <= i1; ++i) mn = std::min(mn, at(i, j, k));
+                bm[(static_cast<size_t>(bk) * bny + bj) * bnx + bi] = mn;
+              }
+          o->bmin.ensure(bm.size() * sizeof(float));
+          cuda_check(cudaMemcpy(o->bmin.p, bm.data(), bm.size() * sizeof(float), cudaMemcpyHostToDevice),
+                     "grid block bounds upload");
+          o->sdf.grd.bmin = static_cast<const float*>(o->bmin.p);
+          o->sdf.grd.bshift = bs;
+          o->sdf.grd.bnx = bnx;
+          o->sdf.grd.bny = bny;
+        }
       } else if (d->kind == DGX_SDF_MESH) {
         // MeshSdf(TriMesh, alpha_phong) (sdf.cpp:17-20): validate, BVH, upload
         if (!(d->alpha_phong >= 0.0 && d->alpha_phong <= 1.0))
@@ -912,6 +945,7 @@ int dgx_object_upload(dgx_ctx* c, const dgx_object_desc* d, dgx_object** out) {
       o->k.Iw = mul(mul(Rp, o->k.inertia_body_inv), transposed(Rp));
     } catch (...) {
       o->vals.release();
+      o->bmin.release();
       delete o;
       throw;
     }
@@ -924,6 +958,7 @@ int dgx_object_free(dgx_object* o) {
     if (!o) return;
     cudaSetDevice(o->ctx->device);
     o->vals.release();
+    o->bmin.release();
     delete o;
   });
 }

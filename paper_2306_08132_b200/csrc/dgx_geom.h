@@ -274,6 +274,14 @@ struct GridSdf {
   int pairs;
   // FP32 copies of origin / h / 1/h for the forward's FP32 pre-filter
   float ofx, ofy, ofz, hf, inv_hf;
+  // device only (may be null): per block of 2^bshift cells per axis, the
+  // minimum node value over the block's nodes widened by one node on every
+  // side (bmin[(bk*bny + bj)*bnx + bi]): a lower bound of the interpolated
+  // (and, outside the box, extended) value anywhere in the block, even when a
+  // rounded cell index is off by one. The forward's pre-filter decides far
+  // points from it without the cell lookup.
+  const float* bmin = nullptr;
+  int bshift = 0, bnx = 0, bny = 0;
 
   DGX_GHD double at(int i, int j, int k) const {
 #if defined(__CUDA_ARCH__)

@@ -47,6 +47,9 @@ __host__ __device__ inline int lane_smem_bytes(int M) { return 2 * lane_cands_pe
 // cell loads: 0 plain (L1 reuse between consecutive points: no_allocate measured
 // 35.9 vs 30.9 ms), 1 L1::no_allocate, 2 L1::evict_first
 constexpr int kLaneCellNoL1 = DGX_LANE_CELL_NOL1;
+#ifndef DGX_LANE_PTS_EVICT_FIRST
+#define DGX_LANE_PTS_EVICT_FIRST 1
+#endif
 
 // Geometry prefetch split: grids issue their cell loads for all U positions
 // before finishing any (grid_fetch / grid_finish); other backends classify in
@@ -260,6 +263,10 @@ __global__ void __launch_bounds__(kLaneAdjThreads) lane_adj_kernel(KHand H, cons
   // this one is processed).
   if (__any_sync(kFull, live)) {
     double* sb = reinterpret_cast<double*>(smem);
+#if DGX_LANE_PTS_EVICT_FIRST
+    unsigned long long pol;
+    asm("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
+#endif
     const int rows = ncw * kLaneRow;  // doubles per buffer
     const int top = S.gs * N - 1;
     auto stage = [&](int blk_top, int bi) {  // positions blk_top - 31 .. blk_top into buffer bi
@@ -273,7 +280,14 @@ __global__ void __launch_bounds__(kLaneAdjThreads) lane_adj_kernel(KHand H, cons
                             static_cast<size_t>(arr) * N + ij;
         const double* dst = sb + bi * rows + c * kLaneRow + arr * kLaneRowArr + j;
         const unsigned sa = static_cast<unsigned>(__cvta_generic_to_shared(dst));
+#if DGX_LANE_PTS_EVICT_FIRST
+        // each sweep streams every candidate's points once (~0.4 GB at config 3):
+        // evict-first in L2 so they do not displace the grid cells
+        asm volatile("cp.async.ca.shared.global.L2::cache_hint [%0], [%1], 8, %2;" ::"r"(sa), "l"(src), "l"(pol)
+                     : "memory");
+#else
         asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(sa), "l"(src) : "memory");
+#endif
       }
       asm volatile("cp.async.commit_group;" ::: "memory");
     };

@@ -1636,6 +1636,13 @@ struct CtasPerSm<MeshSdf> {
 // of this instance). Config 2: 2 CTAs/SM 101k cand-iter/s, 3 CTAs/SM (80
 // registers, 1 KB of spills) 96k, fused 86k.
 constexpr int kFwdCtasPerSm = 2;
+// the forward's SDF parameter stays a by-value copy (measured: as a
+// __grid_constant__ parameter the config-3 forward ran 17.5 -> 18.0 ms); the
+// other structs and the other kernels' parameters are __grid_constant__ (no
+// local copies: config-3 lane adjoint 29.1 -> 28.2 ms)
+#ifndef DGX_FWD_SDF_GC
+#define DGX_FWD_SDF_GC
+#endif
 
 // The CTA's next candidate after b. Candidates differ in cost (contacts,
 // corrections), so a CTA that finishes early takes the next unclaimed one
@@ -1994,8 +2001,10 @@ __device__ __forceinline__ void kernel_body(const KHand& H, const KObj& O, const
 
 // fused / adjoint instances: the register budget follows CTAs per SM
 template <class Sdf, int Occ = CtasPerSm<Sdf>::value, int Phase = kPhaseFused, bool Multi = false>
-__global__ void __launch_bounds__(224, Occ) fused_kernel(KHand H, const __grid_constant__ KObj O, Sdf sdf, KSim S,
-                                                         KOpt P, KBuf buf, int mode) {
+__global__ void __launch_bounds__(224, Occ) fused_kernel(const __grid_constant__ KHand H, const __grid_constant__ KObj O,
+                                                         const __grid_constant__ Sdf sdf, const __grid_constant__ KSim S,
+                                                         const __grid_constant__ KOpt P, const __grid_constant__ KBuf buf,
+                                                         int mode) {
   kernel_body<Sdf, Phase, false, Multi>(H, O, sdf, S, P, buf, mode);
 }
 
@@ -2004,8 +2013,10 @@ __global__ void __launch_bounds__(224, Occ) fused_kernel(KHand H, const __grid_c
 // sub-partitions allow 4096 / 32 = 128 registers per thread; __maxnreg__(144)
 // leaves one CTA per SM (90k vs 101k cand-iter/s)
 template <class Sdf, bool PtsG = false>
-__global__ void __launch_bounds__(224, kFwdCtasPerSm) fwd_kernel(KHand H, const __grid_constant__ KObj O, Sdf sdf,
-                                                                 KSim S, KOpt P, KBuf buf, int mode) {
+__global__ void __launch_bounds__(224, kFwdCtasPerSm) fwd_kernel(const __grid_constant__ KHand H, const __grid_constant__ KObj O,
+                                                                 DGX_FWD_SDF_GC Sdf sdf, const __grid_constant__ KSim S,
+                                                                 const __grid_constant__ KOpt P, const __grid_constant__ KBuf buf,
+                                                                 int mode) {
   kernel_body<Sdf, kPhaseFwd, PtsG>(H, O, sdf, S, P, buf, mode);
 }
 
@@ -2202,8 +2213,9 @@ __device__ __forceinline__ void adj_task_body(const KHand& H, const KObj& O, con
 }
 
 template <class Sdf, int MinBlocks>
-__global__ void __launch_bounds__(32 * kTaskWarps, MinBlocks) adj_task_kernel(KHand H, const __grid_constant__ KObj O,
-                                                                              Sdf sdf, KSim S, KOpt P, KBuf buf,
+__global__ void __launch_bounds__(32 * kTaskWarps, MinBlocks) adj_task_kernel(const __grid_constant__ KHand H, const __grid_constant__ KObj O,
+                                                                              const __grid_constant__ Sdf sdf, const __grid_constant__ KSim S,
+                                                                              const __grid_constant__ KOpt P, const __grid_constant__ KBuf buf,
                                                                               int mode) {
   adj_task_body<Sdf>(H, O, sdf, S, P, buf, mode);
 }
@@ -2249,7 +2261,7 @@ __global__ void __launch_bounds__(256) forward_kernel(KHand H, const double* q, 
 constexpr int kMaxThresholds = 16;
 
 template <class Sdf>
-__global__ void __launch_bounds__(256) contacts_kernel(KHand H, Sdf sdf, int B, const double* __restrict__ q,
+__global__ void __launch_bounds__(256) contacts_kernel(const __grid_constant__ KHand H, const __grid_constant__ Sdf sdf, int B, const double* __restrict__ q,
                                                        const double* __restrict__ area, int T,
                                                        const double* __restrict__ thr, int cap,
                                                        double* __restrict__ ca, int* __restrict__ cnt,
@@ -2379,8 +2391,8 @@ __device__ __forceinline__ void seg_flush12(double (&v)[12], int key, double* ft
 }
 
 template <class Sdf>
-__global__ void __launch_bounds__(32 * kEnergyWarps) energy_kernel(KHand H, const __grid_constant__ KObj O, Sdf sdf,
-                                                                  KSim S, int B, const double* __restrict__ q,
+__global__ void __launch_bounds__(32 * kEnergyWarps) energy_kernel(const __grid_constant__ KHand H, const __grid_constant__ KObj O,
+                                                                  const __grid_constant__ Sdf sdf, const __grid_constant__ KSim S, int B, const double* __restrict__ q,
                                                                   const int* __restrict__ status,
                                                                   double* __restrict__ e_out,
                                                                   double* __restrict__ g_out,

@@ -155,8 +155,10 @@ __device__ __forceinline__ void lane_leak_steps(const Sdf& sdf, const SimEnv& e,
 }
 
 template <class Sdf>
-__global__ void __launch_bounds__(kLaneAdjThreads) lane_adj_kernel(KHand H, const __grid_constant__ KObj O, Sdf sdf,
-                                                                   KSim S, KOpt P, KBuf buf, int mode) {
+__global__ void __launch_bounds__(kLaneAdjThreads) lane_adj_kernel(const __grid_constant__ KHand H, const __grid_constant__ KObj O,
+                                                                   const __grid_constant__ Sdf sdf, const __grid_constant__ KSim S,
+                                                                   const __grid_constant__ KOpt P, const __grid_constant__ KBuf buf,
+                                                                   int mode) {
   extern __shared__ __align__(16) unsigned char smem[];
   const int M = S.M, N = H.N, L = H.L;
   const size_t nt = static_cast<size_t>(buf.B) * M;
@@ -393,7 +395,8 @@ __global__ void __launch_bounds__(kLaneAdjThreads) lane_adj_kernel(KHand H, cons
 // in M doubles), scratch [6L + kMaxDim], sg [96], sq [40].
 __host__ __device__ inline int lane_epi_doubles(int M, int L) { return M * 6 * L + 2 * M + 6 * L + kMaxDim + 96 + 40; }
 
-__global__ void __launch_bounds__(32 * kEpiWarps) lane_epi_kernel(KHand H, KSim S, KOpt P, KBuf buf, int mode) {
+__global__ void __launch_bounds__(32 * kEpiWarps) lane_epi_kernel(const __grid_constant__ KHand H, const __grid_constant__ KSim S,
+                                                                  const __grid_constant__ KOpt P, const __grid_constant__ KBuf buf, int mode) {
   extern __shared__ __align__(16) unsigned char smem[];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int M = S.M, N = H.N, L = H.L, J = H.J, D = 6 + J, Qd = 7 + J;

@@ -83,6 +83,7 @@ struct LaneFt {
     T = V3{0.0, 0.0, 0.0};
   }
   __device__ __forceinline__ void add(double* ftT, size_t nt, int l, V3 ap, V3 p) {
+    DGX_ASSERT(l >= 0 && l < 32);
     if (l != link) {
       flush(ftT, nt);
       link = l;
@@ -107,6 +108,7 @@ __device__ __forceinline__ void lane_leak_steps(const Sdf& sdf, const SimEnv& e,
 #pragma unroll
   for (int u = 0; u < U; ++u) {
     ii[u] = i - u < 0 ? i - u + e.N : i - u;
+    DGX_ASSERT(jb + u >= 0 && jb + u < kLaneRowArr && ii[u] >= 0 && ii[u] < e.N);
     p[u] = V3{ps[jb + u], ps[kLaneRowArr + jb + u], ps[2 * kLaneRowArr + jb + u]};
     rel[u] = p[u] - xk;
     rl[u] = ftmul_add(Rk, rel[u], e.O->com);
@@ -248,7 +250,9 @@ __global__ void __launch_bounds__(kLaneAdjThreads) lane_adj_kernel(const __grid_
       aQ = qmul_adj_a(quat_log_adj(qd, a_thd * inv_dt), qconj(prev_q));
       aX = a_xdot * inv_dt;
       // ---- friction, reverse (sim.hpp:188-196): the slot's a_lambda / a_n accumulate
+      DGX_ASSERT(nfric >= 0 && nfric <= e.slot_cap && ncorr >= 0 && ncorr <= e.cap_corr);
       for (int j = nfric - 1; j >= 0; --j) {
+        DGX_ASSERT(e.fric_order[j] >= 0 && e.fric_order[j] < e.slot_cap);
         SlotRec& s = e.slots[e.fric_order[j]];
         double a_lam = s.a_lam;
         V3 a_n{s.a_n[0], s.a_n[1], s.a_n[2]};
@@ -280,6 +284,7 @@ __global__ void __launch_bounds__(kLaneAdjThreads) lane_adj_kernel(const __grid_
         if (ij < 0) ij += N;
         const double* src = buf.fk + static_cast<size_t>(b_first + c) * (12 * L + 3 * N) + 12 * L +
                             static_cast<size_t>(arr) * N + ij;
+        DGX_ASSERT(c < lane_cands_per_warp(M) && ij >= 0 && ij < N && b_first + c < buf.B);
         const double* dst = sb + bi * rows + c * kLaneRow + arr * kLaneRowArr + j;
         const unsigned sa = static_cast<unsigned>(__cvta_generic_to_shared(dst));
 #if DGX_LANE_PTS_EVICT_FIRST
@@ -342,7 +347,9 @@ __global__ void __launch_bounds__(kLaneAdjThreads) lane_adj_kernel(const __grid_
           const int f = next_f;
           // R node of the state after correction k (read by the run above it)
           aQ = qadd(aQ, rotmat_adj(qk, aR));
+          DGX_ASSERT(k >= 0 && k < e.cap_corr && f >= 0 && f <= pos);
           const CorrRec& c = e.corr[k];
+          DGX_ASSERT(c.slot >= 0 && c.slot < e.slot_cap);
           const SlotRec& sl = e.slots[c.slot];
           load_state(k - 1);
           bool ok = true;

@@ -1,7 +1,7 @@
 """Small grasp-search workloads for compute-sanitizer (memcheck / racecheck):
 
   split  160 candidates (> #SMs): split forward + CTA adjoint (and, with
-         DGX_ADJ_TASK=1, the warp-task adjoint), allegro16 on the 64^3 box grid,
+         DGX_ADJ_TASK=1, the warp-task adjoint), then the lane adjoint, allegro16 on the 64^3 box grid,
          loss_gradient + a 2-iterate optimize; plus the global-points forward
          (shadow22_dense, N = 4093) at 150 candidates
   fused  16 candidates: fused kernel (sphere, grid, mesh), a T = 2 protocol,
@@ -37,6 +37,11 @@ def run(hand_name, od, B, protocol=proto, weights=w, k=2):
 if which == "split":
     run("allegro16", model.box_grid(res=64), 160)
     run("shadow22_dense", model.blob_grid(seed=3, res=64), 150, k=1)
+    ctx.set_adjoint("lane")  # the lane adjoint (dgx_lane_adj.cuh) on the same workloads
+    run("allegro16", model.box_grid(res=64), 160)
+    run("shadow22_dense", model.blob_grid(seed=3, res=64), 150, k=1)
+    run("barrett3", model.sphere(0.025), 150, k=1)
+    ctx.set_adjoint("auto")
 else:
     run("barrett3", model.sphere(0.025), 16)
     run("allegro16", model.box_grid(res=32), 16)

@@ -317,15 +317,17 @@ int task_seg() {
   return seg;
 }
 
+// concurrent: how many such launches run at once on side streams
+// (dgx_optimize_multi); the lane adjoint's parallelism is their summed tasks
 SplitGrid prepare_split(dgx_ctx* c, Scratch& sc, const dgx_hand* h, const dgx_object* o, KSim& S, int B,
-                        bool record, KBuf& buf) {
+                        bool record, KBuf& buf, int concurrent) {
   const int M = S.M, N = h->N, L = h->L;
   SplitGrid g{};
   int av = adjoint_variant();
   if (av == 3 && c->adjoint != DGX_ADJOINT_AUTO) av = c->adjoint == DGX_ADJOINT_LANE ? 2 : 0;
   g.task = record && av == 1;
   g.lane = record && N >= 32 &&  // (the lane adjoint stages 32-position blocks)
-           (av == 2 || (av == 3 && static_cast<long long>(B) * M >=
+           (av == 2 || (av == 3 && static_cast<long long>(B) * M * std::max(1, concurrent) >=
                                        static_cast<long long>(kLaneMinWarpsPerSm) * 32 * c->num_sms));
   if (g.lane) {
     g.smem_a = 0;
@@ -460,7 +462,7 @@ void bind_claim(Scratch& sc, KBuf& buf, int, cudaStream_t st) {
 // Every launch for B candidates whose per-candidate arrays start at buf's
 // pointers, on stream st with scratch sc.
 void launch_range(dgx_ctx* c, Scratch& sc, const dgx_hand* h, const dgx_object* o, KSim S, KOpt P, KBuf buf,
-                  int B, int mode, cudaStream_t st) {
+                  int B, int mode, cudaStream_t st, int concurrent = 1) {
   const int M = S.M, D = 6 + h->J, Qd = 7 + h->J, N = h->N;
   if (mode == kModeOpt) {
     P.traj_k0 = P.k_begin;
@@ -512,7 +514,7 @@ void launch_range(dgx_ctx* c, Scratch& sc, const dgx_hand* h, const dgx_object* 
     return;
   }
   const bool record = mode != kModeEval;
-  const SplitGrid g = prepare_split(c, sc, h, o, S, B, record, buf);
+  const SplitGrid g = prepare_split(c, sc, h, o, S, B, record, buf, concurrent);
   const int k0 = mode == kModeOpt ? P.k_begin : 0, k1 = mode == kModeOpt ? P.k_end : 1;
   for (int b0 = 0; b0 < B; b0 += g.chunk) {
     const int nb = std::min(g.chunk, B - b0);
@@ -1227,7 +1229,12 @@ int dgx_optimize_multi(dgx_ctx* c, const dgx_hand* h, int32_t n_obj, const dgx_o
       cuda_check(cudaMemsetAsync(dt, 0, sizeof(double) * B * steps * (3 + D), c->stream), "cudaMemsetAsync");
     int32_t* ds = st.out(status, static_cast<size_t>(B));
     // fork onto the side streams (object i -> stream i % P), each with its own scratch
-    const int P_streams = std::min<int>(n_obj, 4);
+    int n_live = 0;
+    for (int i = 0; i < n_obj; ++i) n_live += counts[i] > 0 ? 1 : 0;
+    int max_streams = 4;
+    if (const char* ev = std::getenv("DGX_STREAMS")) max_streams = std::max(1, std::atoi(ev));  // A/B
+    const int P_streams = std::max(1, std::min<int>(n_obj, max_streams));
+    const int concurrent = std::max(1, std::min(n_live, P_streams));
     while (static_cast<int>(c->subs.size()) < P_streams) {
       SubStream sub;
       cuda_check(cudaStreamCreateWithFlags(&sub.stream, cudaStreamNonBlocking), "cudaStreamCreate");
@@ -1248,7 +1255,7 @@ int dgx_optimize_multi(dgx_ctx* c, const dgx_hand* h, int32_t n_obj, const dgx_o
       buf.adam_v = dv + off * D;
       buf.traj = dt ? dt + off * steps * (3 + D) : nullptr;
       buf.status = ds + off;
-      launch_range(c, sub.scratch, h, objs[i], S, P, buf, Bi, kModeOpt, sub.stream);
+      launch_range(c, sub.scratch, h, objs[i], S, P, buf, Bi, kModeOpt, sub.stream, concurrent);
       off += Bi;
     }
     for (int k = 0; k < P_streams; ++k) {

@@ -33,6 +33,12 @@
 #include <climits>
 #include <cstdint>
 
+// global-points forward: prefetch the next chunk's points into L1 (A/B knob;
+// measured slower: config-3 forward 17.5 -> 18.5 ms)
+#ifndef DGX_FWD_PREFETCH
+#define DGX_FWD_PREFETCH 0
+#endif
+
 #ifdef DGX_PROFILE_REGIONS
 namespace dgx {
 __device__ unsigned long long g_prof[48];
@@ -114,6 +120,7 @@ struct SimEnv {
   int fold;               // warp-task adjoint: fold the identical final sweeps
   int discard;            // KSim::discard
   int slot_cap;           // contact-slot / friction-order entries of this sim's logs
+  int pts_global;         // px / py / pz point into global memory (global-points forward)
 };
 
 // Forward classification of grids through the FP32 pre-filter (see
@@ -940,6 +947,18 @@ __device__ double run_sim(const Sdf& sdf, SimEnv& e, V3 v_m, bool record, bool m
       }
   #endif
       int cls[2];
+  #if DGX_FWD_PREFETCH
+      if (e.pts_global) {  // the next chunk's points (global-points forward) into L1 while this one runs
+        const int np = pos + 64 < N ? pos + 64 : 0;
+  #pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          const int i = min(np + 32 * h + lane, N - 1);
+          asm volatile("prefetch.global.L1 [%0];" ::"l"(e.px + i));
+          asm volatile("prefetch.global.L1 [%0];" ::"l"(e.py + i));
+          asm volatile("prefetch.global.L1 [%0];" ::"l"(e.pz + i));
+        }
+      }
+  #endif
   #pragma unroll
       for (int h = 0; h < 2; ++h) {
         const int i = pos + 32 * h + lane;
@@ -1835,6 +1854,7 @@ __device__ __forceinline__ void kernel_body(const KHand& H, const KObj& O, const
   e.mu = S.mu;
   e.dt = S.dt;
   e.point_grads = nullptr;
+  e.pts_global = PtsG ? 1 : 0;
   e.fold = S.fold;
   e.discard = S.discard;
   e.mcache = buf.mesh_cache ? buf.mesh_cache + wslot * static_cast<size_t>(S.gs) * N * S.steps : nullptr;
@@ -2079,6 +2099,7 @@ __device__ __forceinline__ void adj_task_body(const KHand& H, const KObj& O, con
   e.mcache = nullptr;
   e.mcert = nullptr;
   e.mcf = nullptr;
+  e.pts_global = 1;
   e.fold = S.fold;
   e.discard = S.discard;
   const int k = mode == kModeOpt ? P.k_begin : 0;

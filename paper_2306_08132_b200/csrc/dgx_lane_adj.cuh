@@ -206,6 +206,7 @@ __global__ void __launch_bounds__(kLaneAdjThreads) lane_adj_kernel(const __grid_
     e.radius = P.iters > 1 ? P.r0 * (1.0 - static_cast<double>(k) / static_cast<double>(P.iters - 1)) : 0.0;
   }
   e.point_grads = buf.point_grads ? buf.point_grads + tc * N * 3 : nullptr;
+  e.pts_global = 1;
 
   const FwdRec* rec = buf.fwd + tc;
   int status = rec->status;

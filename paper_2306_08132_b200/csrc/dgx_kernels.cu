@@ -866,6 +866,11 @@ __device__ __forceinline__ void correction_matrices(const SimEnv& e, int k_lo, i
 // the forward returns the state after the step, the adjoint takes the adjoint
 // of that state and returns the adjoints of pred and of prev's pose (friction's
 // "before" point and finalize read prev, sim.hpp:250, 284-285).
+__device__ __forceinline__ void put3(double* d, V3 v) { d[0] = v.x; d[1] = v.y; d[2] = v.z; }
+__device__ __forceinline__ void put4(double* d, Q4 v) { d[0] = v.w; d[1] = v.x; d[2] = v.y; d[3] = v.z; }
+__device__ __forceinline__ V3 get3(const double* d) { return V3{d[0], d[1], d[2]}; }
+__device__ __forceinline__ Q4 get4(const double* d) { return Q4{d[0], d[1], d[2], d[3]}; }
+
 struct StepCtx {
   V3 prev_x, prev_xd, prev_w, pred_x, pred_xd, pred_w;
   Q4 prev_q, pred_q;
@@ -990,7 +995,10 @@ __device__ double run_sim(const Sdf& sdf, SimEnv& e, V3 v_m, bool record, bool m
         const int i = pos + 32 * h + lane;
         bool act = false;
         if ((h ? cls[1] : cls[0]) <= 0) {
-          eval_point(sdf, e, i, x, R, record, pe);
+          // grids: R is rebuilt from q here (the same values) instead of being held
+          // in registers across the pre-filter loop, which reads only the FP32 pose
+          if constexpr (kF32Prefilter<Sdf>) eval_point(sdf, e, i, x, rotation_matrix(q), record, pe);
+          else eval_point(sdf, e, i, x, R, record, pe);
           act = record ? (pe.rho_d < 0.0) : !(pe.rho_d >= 0.0);
         }
         mask = __ballot_sync(kFull, act);
@@ -1022,8 +1030,8 @@ __device__ double run_sim(const Sdf& sdf, SimEnv& e, V3 v_m, bool record, bool m
       if (co.applied) {
         x = co.x;
         q = co.q;
-        R = rotation_matrix(q);
-        if constexpr (kF32Prefilter<Sdf>) Pf = pose_f32(x, R, e.O->com);
+        if constexpr (kF32Prefilter<Sdf>) Pf = pose_f32(x, rotation_matrix(q), e.O->com);
+        else R = rotation_matrix(q);
         touched = true;
         f_last = sweep * N + ij;
         singular_since = 0;
@@ -1402,10 +1410,6 @@ __device__ double run_sim(const Sdf& sdf, SimEnv& e, V3 v_m, bool record, bool m
 }
 
 
-__device__ __forceinline__ void put3(double* d, V3 v) { d[0] = v.x; d[1] = v.y; d[2] = v.z; }
-__device__ __forceinline__ void put4(double* d, Q4 v) { d[0] = v.w; d[1] = v.x; d[2] = v.y; d[3] = v.z; }
-__device__ __forceinline__ V3 get3(const double* d) { return V3{d[0], d[1], d[2]}; }
-__device__ __forceinline__ Q4 get4(const double* d) { return Q4{d[0], d[1], d[2], d[3]}; }
 
 // perturbation_residual with StabilityProtocol::steps = T > 1 (losses.hpp:47-57):
 // T steps of predict + solve (sim.hpp:310-316) from the canonical state, the

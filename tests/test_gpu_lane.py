@@ -106,3 +106,27 @@ def test_lane_adjoint_optimizer_teacher_forced(ctx, oracle, hand_name, obj_name)
         assert relerr(out["q"][:8], r["q"]) < GRAD_RTOL
         assert relerr(out["m"][:8], r["m"]) < GRAD_RTOL
         q, m, v = out["q"], out["m"], out["v"]
+
+
+def test_lane_adjoint_correction_log_overflow_is_per_candidate():
+    """A correction-log capacity of 70 through the lane adjoint: candidates that
+    overflow report status 3, the others equal a default-capacity run
+    bit-for-bit (the same lane path); statuses equal the CTA adjoint's."""
+    from paper_2306_08132_b200 import api, init, model
+    small, big = api.Context(0, correction_capacity=70), api.Context(0)
+    hd = model.HandDesc.asset("allegro16")
+    od = model.box_grid(res=32)
+    q = init.approach_init(od, hd, 400, seed=9)
+    proto, params = api.StabilityProtocol.standard(), api.SimParams(dilation_radius=0.01)
+    res = {}
+    for name, c in (("small", small), ("big", big)):
+        hand, obj = api.Hand(c, hd), api.GraspObject(c, od)
+        for variant in ("lane", "cta"):
+            res[name, variant] = _run(c, variant, lambda: api.loss_gradient(c, obj, hand, q, proto, params))
+    ls, gs, ss = res["small", "lane"]
+    lb, gb, sb = res["big", "lane"]
+    assert not np.any(sb)
+    assert set(np.unique(ss).tolist()) <= {0, 3} and 0 < np.count_nonzero(ss == 3) < 400
+    assert np.array_equal(ss, res["small", "cta"][2])
+    ok = ss == 0
+    assert np.array_equal(ls[ok], lb[ok]) and np.array_equal(gs[ok], gb[ok])

@@ -258,3 +258,33 @@ def test_correction_log_overflow_is_per_candidate(B):
     assert 0 < np.count_nonzero(ss == 3) < B  # both kinds present
     ok = ss == 0
     assert np.array_equal(ls[ok], lb[ok]) and np.array_equal(gs[ok], gb[ok])
+
+
+@pytest.mark.parametrize("hand_name,grid", [("allegro16", "box64"), ("shadow22_dense", "blob128")])
+def test_grid_block_bounds_keep_decisions(monkeypatch, hand_name, grid):
+    """The forward pre-filter's block lower bounds (GridSdf::bmin, DESIGN.md
+    3.10) only skip cell lookups of points they prove inactive: the same grid
+    uploaded without them (DGX_GRID_BLOCK=0) gives bit-identical losses,
+    gradients, statuses and SolveStats through the split path."""
+    from paper_2306_08132_b200 import api, init, model
+    c = api.Context(0)
+    hd = model.HandDesc.asset(hand_name)
+    od = model.box_grid(res=64) if grid == "box64" else model.blob_grid(seed=3, res=128)
+    hand = api.Hand(c, hd)
+    with_b = api.GraspObject(c, od)
+    monkeypatch.setenv("DGX_GRID_BLOCK", "0")
+    without = api.GraspObject(c, od)
+    monkeypatch.delenv("DGX_GRID_BLOCK")
+    q = init.approach_init(od, hd, 200, seed=12)
+    q[:, :3] -= 0.3 * (q[:, :3] - od.com)
+    proto = api.StabilityProtocol.standard()
+    for radius in (0.0, 0.015):
+        params = api.SimParams(dilation_radius=radius)
+        a = api.loss_gradient(c, with_b, hand, q, proto, params)
+        b = api.loss_gradient(c, without, hand, q, proto, params)
+        for x, y in zip(a, b):
+            assert np.array_equal(x, y, equal_nan=True)
+        ea = api.evaluate_losses(c, with_b, hand, q, proto, params)
+        eb = api.evaluate_losses(c, without, hand, q, proto, params)
+        for x, y in zip(ea, eb):
+            assert np.array_equal(x, y, equal_nan=True)

@@ -47,6 +47,9 @@ __host__ __device__ inline int lane_smem_bytes(int M) { return 2 * lane_cands_pe
 // cell loads: 0 plain (L1 reuse between consecutive points: no_allocate measured
 // 35.9 vs 30.9 ms), 1 L1::no_allocate, 2 L1::evict_first
 constexpr int kLaneCellNoL1 = DGX_LANE_CELL_NOL1;
+#ifndef DGX_LANE_UNIFORM_FINISH
+#define DGX_LANE_UNIFORM_FINISH 1
+#endif
 #ifndef DGX_LANE_PTS_EVICT_FIRST
 #define DGX_LANE_PTS_EVICT_FIRST 1
 #endif
@@ -64,7 +67,11 @@ struct GeoPre<GridSdf> {
   GridFetch f;
   __device__ __forceinline__ void fetch(const GridSdf& s, V3 r) { grid_fetch<kLaneCellNoL1>(s, r, f); }
   __device__ __forceinline__ FastEval finish(const GridSdf& s, V3 r, double radius) const {
+#if DGX_LANE_UNIFORM_FINISH
+    return grid_finish_uniform(s, r, f, radius);
+#else
     return grid_finish(s, r, f, radius);
+#endif
   }
 };
 

@@ -326,7 +326,7 @@ SplitGrid prepare_split(dgx_ctx* c, Scratch& sc, const dgx_hand* h, const dgx_ob
   int av = adjoint_variant();
   if (av == 3 && c->adjoint != DGX_ADJOINT_AUTO) av = c->adjoint == DGX_ADJOINT_LANE ? 2 : 0;
   g.task = record && av == 1;
-  g.lane = record && N >= 32 &&  // (the lane adjoint stages 32-position blocks)
+  g.lane = record && N >= 64 &&  // (the lane adjoint stages blocks of <= 64 positions)
            (av == 2 || (av == 3 && static_cast<long long>(B) * M * std::max(1, concurrent) >=
                                        static_cast<long long>(kLaneMinWarpsPerSm) * 32 * c->num_sms));
   if (g.lane) {

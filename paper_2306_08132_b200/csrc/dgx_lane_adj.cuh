@@ -34,11 +34,16 @@
 
 constexpr int kLaneAdjThreads = 32;  // one warp per CTA: tasks spread over all SMs' schedulers
 constexpr int kEpiWarps = 4;
-static_assert(kLaneAdjThreads == 32 && 32 % kLaneU == 0, "lane adjoint: one warp per CTA, windows tile 32-position blocks");
+// staged block of positions (a multiple of kLaneU: windows never straddle blocks)
+#ifndef DGX_LANE_BLK
+#define DGX_LANE_BLK 32
+#endif
+constexpr int kLaneBlk = DGX_LANE_BLK;
+static_assert(kLaneAdjThreads == 32 && kLaneBlk % kLaneU == 0, "lane adjoint: one warp per CTA, windows tile the blocks");
 // staged points: per buffer and candidate of the warp a row of x / y / z for
 // 32 positions; rows 98 doubles apart (196 words: the warp's <= 6 candidates
 // fall on distinct banks)
-constexpr int kLaneRowArr = 32, kLaneRow = 3 * kLaneRowArr + 2;
+constexpr int kLaneRowArr = kLaneBlk, kLaneRow = 3 * kLaneRowArr + 2;
 __host__ __device__ inline int lane_cands_per_warp(int M) { return (31 / M + 2) < 32 ? (31 / M + 2) : 32; }
 __host__ __device__ inline int lane_smem_bytes(int M) { return 2 * lane_cands_per_warp(M) * kLaneRow * 8; }
 #ifndef DGX_LANE_CELL_NOL1
@@ -283,10 +288,10 @@ __global__ void __launch_bounds__(kLaneAdjThreads) lane_adj_kernel(const __grid_
 #endif
     const int rows = ncw * kLaneRow;  // doubles per buffer
     const int top = S.gs * N - 1;
-    auto stage = [&](int blk_top, int bi) {  // positions blk_top - 31 .. blk_top into buffer bi
+    auto stage = [&](int blk_top, int bi) {  // positions blk_top - kLaneBlk + 1 .. blk_top into buffer bi
       const int itop = blk_top % N;
-      for (int x = lane; x < ncw * 3 * 32; x += 32) {
-        const int c = x / 96, r = x - 96 * c, arr = r >> 5, j = r & 31;
+      for (int x = lane; x < ncw * 3 * kLaneBlk; x += 32) {
+        const int c = x / (3 * kLaneBlk), r = x - 3 * kLaneBlk * c, arr = r / kLaneBlk, j = r - arr * kLaneBlk;
         if (blk_top - j < 0) continue;
         int ij = itop - j;
         if (ij < 0) ij += N;
@@ -334,12 +339,13 @@ __global__ void __launch_bounds__(kLaneAdjThreads) lane_adj_kernel(const __grid_
     LaneFt acc;
     int i = N - 1;
     stage(top, 0);
-    int blk = 0, blk_top = top;
+    int blk = 0, blk_top = top, blk_next = top;
     const double* ps = sb;
     for (int pos = top; pos >= 0; pos -= kLaneU) {
-      if (((top - pos) & 31) == 0) {  // next block: stage the one after it, wait for this one
+      if (pos == blk_next) {  // next block: stage the one after it, wait for this one
+        blk_next = pos - kLaneBlk;
         __syncwarp();  // every lane is done with the buffer about to be refilled
-        if (pos - 32 >= 0) stage(pos - 32, (blk + 1) & 1);
+        if (pos - kLaneBlk >= 0) stage(pos - kLaneBlk, (blk + 1) & 1);
         else asm volatile("cp.async.commit_group;" ::: "memory");
         asm volatile("cp.async.wait_group 1;" ::: "memory");
         __syncwarp();
@@ -351,7 +357,7 @@ __global__ void __launch_bounds__(kLaneAdjThreads) lane_adj_kernel(const __grid_
         lane_leak_steps<kLaneU>(sdf, e, pos, i, max(next_f, pos - kLaneU), xk, Rk, G, aX, aR, acc, ftT, nt, ps,
                                 blk_top - pos);
         // this lane's logged corrections inside the window (divergent; rare)
-        while (next_f > pos - kLaneU) {
+        while (next_f >= 0 && next_f > pos - kLaneU) {  // (next_f = -1: no more corrections)
           const int f = next_f;
           // R node of the state after correction k (read by the run above it)
           aQ = qadd(aQ, rotmat_adj(qk, aR));

@@ -130,3 +130,24 @@ def test_lane_adjoint_correction_log_overflow_is_per_candidate():
     assert np.array_equal(ss, res["small", "cta"][2])
     ok = ss == 0
     assert np.array_equal(ls[ok], lb[ok]) and np.array_equal(gs[ok], gb[ok])
+
+
+@pytest.mark.parametrize("gs", [1, 3])
+def test_lane_adjoint_odd_sweep_count(ctx, oracle, gs):
+    """gs * N even or odd: the reverse walk's last window may reach below
+    position 0 (barrett3, N = 1999: gs = 1 / 3 give an even top position);
+    sims without further corrections must not read the log there."""
+    from paper_2306_08132_b200 import api
+    s = Setup(ctx, oracle, "barrett3", _object("boxgrid64"), B=8, seed=94)
+    q = np.tile(s.q, (TILE, 1))
+    proto = api.StabilityProtocol.standard()
+    params = api.SimParams(dilation_radius=0.015, gs_iters=gs)
+    ll, gl, stl = _run(ctx, "lane", lambda: api.loss_gradient(ctx, s.obj, s.hand, q, proto, params))
+    lc, gc, stc = _run(ctx, "cta", lambda: api.loss_gradient(ctx, s.obj, s.hand, q, proto, params))
+    assert not np.any(stl) and np.array_equal(ll, lc)
+    assert relerr(gl, gc) < LANE_VS_CTA_RTOL
+    p = oracle.default_params(dilation_radius=0.015, gs_iters=gs)
+    for b in range(4):
+        rl, ds, dr, dl = oracle.loss_gradient(s.ro, s.rh, s.q[b], p)
+        assert np.array_equal(ll[b], rl)
+        assert relerr(gl[b, 0], ds) < GRAD_RTOL

@@ -2715,6 +2715,13 @@ static cudaError_t launch_lane_t(const KHand& H, const KObj& O, const Sdf& sdf, 
   if constexpr (kSplitCapable<Sdf>) {
     const long long nt = static_cast<long long>(buf.B) * S.M;
     const int grid = static_cast<int>((nt + kLaneAdjThreads - 1) / kLaneAdjThreads);
+    static bool configured = false;  // small M: up to 32 candidates' staged points per warp (> 48 KB)
+    if (!configured) {
+      const cudaError_t e =
+          cudaFuncSetAttribute(lane_adj_kernel<Sdf>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+      if (e != cudaSuccess) return e;
+      configured = true;
+    }
     lane_adj_kernel<Sdf><<<grid, kLaneAdjThreads, lane_smem_bytes(S.M), st>>>(H, O, sdf, S, P, buf, mode);
     return cudaGetLastError();
   }

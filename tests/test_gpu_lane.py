@@ -151,3 +151,50 @@ def test_lane_adjoint_odd_sweep_count(ctx, oracle, gs):
         rl, ds, dr, dl = oracle.loss_gradient(s.ro, s.rh, s.q[b], p)
         assert np.array_equal(ll[b], rl)
         assert relerr(gl[b, 0], ds) < GRAD_RTOL
+
+
+@pytest.mark.parametrize("nvel", [1, 9])
+def test_lane_adjoint_protocol_sizes(ctx, oracle, nvel):
+    """Any number of perturbation velocities through the lane adjoint (M = 1:
+    32 candidates per warp; M = 9: velocities beyond KSim's inline 8 come from
+    the device copy), vs the CTA adjoint and the reference."""
+    from paper_2306_08132_b200 import api
+    s = Setup(ctx, oracle, "allegro16", _object("boxgrid64"), B=8, seed=95)
+    q = np.tile(s.q, (TILE, 1))
+    base = api.StabilityProtocol.standard().velocities
+    vel = [tuple(v) for v in base] + [(0.3, 0.3, 0.0), (0.0, 0.2, -0.4)]
+    proto = api.StabilityProtocol(vel[:nvel])
+    params = api.SimParams(dilation_radius=0.015)
+    ll, gl, stl = _run(ctx, "lane", lambda: api.loss_gradient(ctx, s.obj, s.hand, q, proto, params))
+    lc, gc, stc = _run(ctx, "cta", lambda: api.loss_gradient(ctx, s.obj, s.hand, q, proto, params))
+    assert not np.any(stl) and np.array_equal(ll, lc)
+    assert relerr(gl, gc) < LANE_VS_CTA_RTOL
+    for t in range(1, TILE):
+        assert np.array_equal(gl[8 * t:8 * t + 8], gl[:8])
+
+
+def test_lane_adjoint_nonfinite_rows_and_energy(ctx, oracle):
+    """A NaN base position (free flight, gradient 0) and a NaN joint (status 1)
+    in a lane-adjoint batch leave the other rows bit-identical; an optimizer
+    iterate with the grasp-energy terms on agrees with the CTA adjoint."""
+    from paper_2306_08132_b200 import api
+    s = Setup(ctx, oracle, "allegro16", _object("boxgrid64"), B=8, seed=96)
+    q = np.tile(s.q, (TILE, 1))
+    proto, params = api.StabilityProtocol.standard(), api.SimParams(dilation_radius=0.01)
+    bad = q.copy()
+    bad[0, 0] = np.nan
+    bad[1, 9] = np.nan
+    lb, gb, sb = _run(ctx, "lane", lambda: api.loss_gradient(ctx, s.obj, s.hand, bad, proto, params))
+    lo, go, so = _run(ctx, "lane", lambda: api.loss_gradient(ctx, s.obj, s.hand, q, proto, params))
+    assert sb[0] == 0 and sb[1] == 1 and not np.any(sb[2:]) and not np.any(so)
+    assert np.array_equal(lb[2:], lo[2:]) and np.array_equal(gb[2:], go[2:])
+    assert np.array_equal(gb[0, 0], np.zeros_like(gb[0, 0]))
+    w = api.LossWeights(force_closure=0.3, penetration=2.0, contact_threshold=0.004)
+    opt = api.OptConfig(iterations=500)
+    ol = _run(ctx, "lane", lambda: api.optimize(ctx, s.obj, s.hand, q, proto, api.SimParams(), w, opt,
+                                                 k_begin=2, k_end=3, record=True))
+    oc = _run(ctx, "cta", lambda: api.optimize(ctx, s.obj, s.hand, q, proto, api.SimParams(), w, opt,
+                                                k_begin=2, k_end=3, record=True))
+    assert not np.any(ol["status"]) and np.array_equal(ol["traj"][:, :, :3], oc["traj"][:, :, :3])
+    assert relerr(ol["traj"][:, :, 3:], oc["traj"][:, :, 3:]) < LANE_VS_CTA_RTOL
+    assert relerr(ol["q"], oc["q"]) < LANE_VS_CTA_RTOL

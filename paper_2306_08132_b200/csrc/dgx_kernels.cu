@@ -2740,14 +2740,17 @@ cudaError_t launch_lane_adj(const KHand& H, const KObj& O, const SdfSet& sdf, co
 
 cudaError_t launch_lane_epi(const KHand& H, const KSim& S, const KOpt& P, const KBuf& buf, int mode, cudaStream_t st) {
   static bool configured = false;
-  const int smem = 8 * kEpiWarps * lane_epi_doubles(S.M, H.L);
+  // kEpiWarps candidates per CTA, fewer when many sims' link sums would not fit
+  const int per_warp = 8 * lane_epi_doubles(S.M, H.L);
+  const int warps = std::max(1, std::min(kEpiWarps, (227 * 1024) / per_warp));
+  const int smem = warps * per_warp;
   if (!configured) {
     cudaError_t e = cudaFuncSetAttribute(lane_epi_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
     if (e != cudaSuccess) return e;
     configured = true;
   }
   if (smem > 227 * 1024) return cudaErrorInvalidValue;
-  lane_epi_kernel<<<(buf.B + kEpiWarps - 1) / kEpiWarps, 32 * kEpiWarps, smem, st>>>(H, S, P, buf, mode);
+  lane_epi_kernel<<<(buf.B + warps - 1) / warps, 32 * warps, smem, st>>>(H, S, P, buf, mode);
   return cudaGetLastError();
 }
 

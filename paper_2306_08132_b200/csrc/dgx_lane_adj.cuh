@@ -421,7 +421,7 @@ __global__ void __launch_bounds__(32 * kEpiWarps) lane_epi_kernel(const __grid_c
   extern __shared__ __align__(16) unsigned char smem[];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int M = S.M, N = H.N, L = H.L, J = H.J, D = 6 + J, Qd = 7 + J;
-  const int b = static_cast<int>(blockIdx.x) * kEpiWarps + warp;
+  const int b = static_cast<int>(blockIdx.x) * static_cast<int>(blockDim.x >> 5) + warp;
   if (b >= buf.B) return;  // warp-uniform
   if (mode == kModeOpt && P.k_begin > P.traj_k0 && buf.status[b] != kOk) return;
   double* wb = reinterpret_cast<double*>(smem) + static_cast<size_t>(warp) * lane_epi_doubles(M, L);

@@ -153,16 +153,19 @@ def test_lane_adjoint_odd_sweep_count(ctx, oracle, gs):
         assert relerr(gl[b, 0], ds) < GRAD_RTOL
 
 
-@pytest.mark.parametrize("nvel", [1, 9])
+@pytest.mark.parametrize("nvel", [1, 9, 48])
 def test_lane_adjoint_protocol_sizes(ctx, oracle, nvel):
     """Any number of perturbation velocities through the lane adjoint (M = 1:
     32 candidates per warp; M = 9: velocities beyond KSim's inline 8 come from
-    the device copy), vs the CTA adjoint and the reference."""
+    the device copy; M = 48: the epilogue's per-sim link sums need fewer
+    candidates per CTA), vs the CTA adjoint."""
     from paper_2306_08132_b200 import api
     s = Setup(ctx, oracle, "allegro16", _object("boxgrid64"), B=8, seed=95)
     q = np.tile(s.q, (TILE, 1))
     base = api.StabilityProtocol.standard().velocities
     vel = [tuple(v) for v in base] + [(0.3, 0.3, 0.0), (0.0, 0.2, -0.4)]
+    rng = np.random.default_rng(7)
+    vel += [tuple(0.5 * d / np.linalg.norm(d)) for d in rng.normal(size=(48, 3))]
     proto = api.StabilityProtocol(vel[:nvel])
     params = api.SimParams(dilation_radius=0.015)
     ll, gl, stl = _run(ctx, "lane", lambda: api.loss_gradient(ctx, s.obj, s.hand, q, proto, params))

@@ -34,6 +34,11 @@
 
 constexpr int kLaneAdjThreads = 32;  // one warp per CTA: tasks spread over all SMs' schedulers
 constexpr int kEpiWarps = 4;
+// min resident 1-warp CTAs per SM the register budget is sized for (1: up to
+// 255 registers; A/B knob)
+#ifndef DGX_LANE_MINB
+#define DGX_LANE_MINB 1
+#endif
 // staged block of positions (a multiple of kLaneU: windows never straddle blocks)
 #ifndef DGX_LANE_BLK
 #define DGX_LANE_BLK 32
@@ -169,7 +174,7 @@ __device__ __forceinline__ void lane_leak_steps(const Sdf& sdf, const SimEnv& e,
 }
 
 template <class Sdf>
-__global__ void __launch_bounds__(kLaneAdjThreads) lane_adj_kernel(const __grid_constant__ KHand H, const __grid_constant__ KObj O,
+__global__ void __launch_bounds__(kLaneAdjThreads, DGX_LANE_MINB) lane_adj_kernel(const __grid_constant__ KHand H, const __grid_constant__ KObj O,
                                                                    const __grid_constant__ Sdf sdf, const __grid_constant__ KSim S,
                                                                    const __grid_constant__ KOpt P, const __grid_constant__ KBuf buf,
                                                                    int mode) {

@@ -33,6 +33,12 @@
 #include <climits>
 #include <cstdint>
 
+// 32-position groups the forward classifies per iteration (A/B knob)
+#ifndef DGX_FWD_HALVES
+#define DGX_FWD_HALVES 2
+#endif
+static constexpr int kFwdHalves = DGX_FWD_HALVES;
+
 // global-points forward: prefetch the next chunk's points into L1 (A/B knob;
 // measured slower: config-3 forward 17.5 -> 18.5 ms)
 #ifndef DGX_FWD_PREFETCH
@@ -951,12 +957,13 @@ __device__ double run_sim(const Sdf& sdf, SimEnv& e, V3 v_m, bool record, bool m
         if (sweep * N + pos - f_last - 1 >= N && singular_since == 0) { fwd_end = sweep * N + pos; break; }
       }
   #endif
-      int cls[2];
+      constexpr int kH = kFwdHalves;  // 32-position groups classified per iteration
+      int cls[kH];
   #if DGX_FWD_PREFETCH
       if (e.pts_global) {  // the next chunk's points (global-points forward) into L1 while this one runs
-        const int np = pos + 64 < N ? pos + 64 : 0;
+        const int np = pos + 32 * kH < N ? pos + 32 * kH : 0;
   #pragma unroll
-        for (int h = 0; h < 2; ++h) {
+        for (int h = 0; h < kH; ++h) {
           const int i = min(np + 32 * h + lane, N - 1);
           asm volatile("prefetch.global.L1 [%0];" ::"l"(e.px + i));
           asm volatile("prefetch.global.L1 [%0];" ::"l"(e.py + i));
@@ -965,7 +972,7 @@ __device__ double run_sim(const Sdf& sdf, SimEnv& e, V3 v_m, bool record, bool m
       }
   #endif
   #pragma unroll
-      for (int h = 0; h < 2; ++h) {
+      for (int h = 0; h < kH; ++h) {
         const int i = pos + 32 * h + lane;
         const int ic = i < N ? i : N - 1;
         if constexpr (kF32Prefilter<Sdf>) {
@@ -977,12 +984,16 @@ __device__ double run_sim(const Sdf& sdf, SimEnv& e, V3 v_m, bool record, bool m
           cls[h] = i < N ? classify_fwd(sdf, e, sweep * N + i, rl).cls : 1;
         }
       }
-      const unsigned cand0 = __ballot_sync(kFull, cls[0] <= 0);
-      const unsigned cand1 = __ballot_sync(kFull, cls[1] <= 0);
+      unsigned cand[kH];
+      unsigned any = 0u;
+  #pragma unroll
+      for (int h = 0; h < kH; ++h) {
+        cand[h] = __ballot_sync(kFull, cls[h] <= 0);
+        any |= cand[h];
+      }
       PROF_CNT(16, 1);
-      PROF_CNT(17, __popc(cand0) + __popc(cand1));
-      if ((cand0 | cand1) == 0u) {
-        pos += 64;
+      if (any == 0u) {
+        pos += 32 * kH;
         if (pos >= N) { pos = 0; ++sweep; }
         continue;
       }
@@ -990,11 +1001,16 @@ __device__ double run_sim(const Sdf& sdf, SimEnv& e, V3 v_m, bool record, bool m
       int hsel = -1;
       unsigned mask = 0u;
   #pragma unroll 1
-      for (int h = 0; h < 2; ++h) {
-        if ((h ? cand1 : cand0) == 0u) continue;
+      for (int h = 0; h < kH; ++h) {
+        unsigned ch = cand[0];
+        int clh = cls[0];
+  #pragma unroll
+        for (int hh = 1; hh < kH; ++hh)
+          if (h == hh) { ch = cand[hh]; clh = cls[hh]; }
+        if (ch == 0u) continue;
         const int i = pos + 32 * h + lane;
         bool act = false;
-        if ((h ? cls[1] : cls[0]) <= 0) {
+        if (clh <= 0) {
           // grids: R is rebuilt from q here (the same values) instead of being held
           // in registers across the pre-filter loop, which reads only the FP32 pose
           if constexpr (kF32Prefilter<Sdf>) eval_point(sdf, e, i, x, rotation_matrix(q), record, pe);
@@ -1008,7 +1024,7 @@ __device__ double run_sim(const Sdf& sdf, SimEnv& e, V3 v_m, bool record, bool m
         }
       }
       if (hsel < 0) {
-        pos += 64;
+        pos += 32 * kH;
         if (pos >= N) { pos = 0; ++sweep; }
         continue;
       }

@@ -1674,7 +1674,18 @@ struct CtasPerSm<MeshSdf> {
 // Split-execution forward kernel: 2 CTAs per SM (the adjoint is compiled out
 // of this instance). Config 2: 2 CTAs/SM 101k cand-iter/s, 3 CTAs/SM (80
 // registers, 1 KB of spills) 96k, fused 86k.
-constexpr int kFwdCtasPerSm = 2;
+#ifndef DGX_FWD_CTAS
+#define DGX_FWD_CTAS 2
+#endif
+constexpr int kFwdCtasPerSm = DGX_FWD_CTAS;
+// the global-points forward (large hands: 24 KB of shared memory per CTA) at 3
+// CTAs per SM: config 3 17.2 -> 16.8 ms per step despite 80 registers and
+// 1 KB of spills; with the points in shared memory 3 CTAs lose (config 2
+// 1.40 -> 1.86 ms, config 4 2.48 -> 3.03 ms)
+#ifndef DGX_FWD_CTAS_PTSG
+#define DGX_FWD_CTAS_PTSG 3
+#endif
+constexpr int kFwdCtasPerSmPtsG = DGX_FWD_CTAS_PTSG;
 // the forward's SDF parameter stays a by-value copy (measured: as a
 // __grid_constant__ parameter the config-3 forward ran 17.5 -> 18.0 ms); the
 // other structs and the other kernels' parameters are __grid_constant__ (no
@@ -2053,7 +2064,7 @@ __global__ void __launch_bounds__(224, Occ) fused_kernel(const __grid_constant__
 // sub-partitions allow 4096 / 32 = 128 registers per thread; __maxnreg__(144)
 // leaves one CTA per SM (90k vs 101k cand-iter/s)
 template <class Sdf, bool PtsG = false>
-__global__ void __launch_bounds__(224, kFwdCtasPerSm) fwd_kernel(const __grid_constant__ KHand H, const __grid_constant__ KObj O,
+__global__ void __launch_bounds__(224, PtsG ? kFwdCtasPerSmPtsG : kFwdCtasPerSm) fwd_kernel(const __grid_constant__ KHand H, const __grid_constant__ KObj O,
                                                                  DGX_FWD_SDF_GC Sdf sdf, const __grid_constant__ KSim S,
                                                                  const __grid_constant__ KOpt P, const __grid_constant__ KBuf buf,
                                                                  int mode) {

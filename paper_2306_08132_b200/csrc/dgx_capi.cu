@@ -479,6 +479,7 @@ void launch_range(dgx_ctx* c, Scratch& sc, const dgx_hand* h, const dgx_object* 
   const bool split = use_split(o) && B > c->num_sms && !(mode == kModeOpt && P.k_end == P.k_begin) &&
                      S.steps == 1;  // multi-step protocols run the fused kernel
   S.pts_global = SmemLayout(N, h->L, M, 0).total > kSplitMaxFwdSmem ? 1 : 0;
+  if (const char* ev = std::getenv("DGX_PTS_GLOBAL")) S.pts_global = std::atoi(ev) != 0;  // A/B
   // grasp-energy terms (optimizer only): their weighted gradient depends on
   // the iterate's q, so it is computed per iterate right before the
   // iterate's grasp-search launch and added before Adam (KBuf::egrad)

@@ -1678,12 +1678,12 @@ struct CtasPerSm<MeshSdf> {
 #define DGX_FWD_CTAS 2
 #endif
 constexpr int kFwdCtasPerSm = DGX_FWD_CTAS;
-// the global-points forward (large hands: 24 KB of shared memory per CTA) at 3
-// CTAs per SM: config 3 17.2 -> 16.8 ms per step despite 80 registers and
-// 1 KB of spills; with the points in shared memory 3 CTAs lose (config 2
-// 1.40 -> 1.86 ms, config 4 2.48 -> 3.03 ms)
+// the global-points forward (large hands: 24 KB of shared memory per CTA) at 4
+// CTAs per SM: config 3 forward 2 / 3 / 4 / 5 CTAs 17.2 / 16.8 / 15.6 / 16.5 ms
+// per step (4: 72 registers, 1.1 KB of spills); with the points in shared
+// memory 3 CTAs lose (config 2 1.40 -> 1.86 ms, config 4 2.48 -> 3.03 ms)
 #ifndef DGX_FWD_CTAS_PTSG
-#define DGX_FWD_CTAS_PTSG 3
+#define DGX_FWD_CTAS_PTSG 4
 #endif
 constexpr int kFwdCtasPerSmPtsG = DGX_FWD_CTAS_PTSG;
 // the forward's SDF parameter stays a by-value copy (measured: as a

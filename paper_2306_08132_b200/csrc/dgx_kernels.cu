@@ -33,9 +33,11 @@
 #include <climits>
 #include <cstdint>
 
-// 32-position groups the forward classifies per iteration (A/B knob)
+// 32-position groups the forward classifies per iteration (A/B knob; measured
+// forward ms per step, config 3 / config 2 / config 4: 1 group 15.12 / 1.35 /
+// 2.46, 2 groups 15.62 / 1.40 / 2.49, 3-4 groups slower)
 #ifndef DGX_FWD_HALVES
-#define DGX_FWD_HALVES 2
+#define DGX_FWD_HALVES 1
 #endif
 static constexpr int kFwdHalves = DGX_FWD_HALVES;
 
@@ -957,7 +959,9 @@ __device__ double run_sim(const Sdf& sdf, SimEnv& e, V3 v_m, bool record, bool m
         if (sweep * N + pos - f_last - 1 >= N && singular_since == 0) { fwd_end = sweep * N + pos; break; }
       }
   #endif
-      constexpr int kH = kFwdHalves;  // 32-position groups classified per iteration
+      // 32-position groups classified per iteration: the split forward kFwdHalves, the fused kernel 2
+      // (config 1, fused: 69.3k with 2 groups, 66.8k with 1)
+      constexpr int kH = Phase == kPhaseFwd ? kFwdHalves : 2;
       int cls[kH];
   #if DGX_FWD_PREFETCH
       if (e.pts_global) {  // the next chunk's points (global-points forward) into L1 while this one runs

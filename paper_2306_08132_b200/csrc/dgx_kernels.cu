@@ -1682,12 +1682,14 @@ struct CtasPerSm<MeshSdf> {
 #define DGX_FWD_CTAS 2
 #endif
 constexpr int kFwdCtasPerSm = DGX_FWD_CTAS;
-// the global-points forward (large hands: 24 KB of shared memory per CTA) at 4
-// CTAs per SM: config 3 forward 2 / 3 / 4 / 5 CTAs 17.2 / 16.8 / 15.6 / 16.5 ms
-// per step (4: 72 registers, 1.1 KB of spills); with the points in shared
-// memory 3 CTAs lose (config 2 1.40 -> 1.86 ms, config 4 2.48 -> 3.03 ms)
+// the global-points forward (large hands: 24 KB of shared memory per CTA) at 5
+// CTAs per SM: config 3 forward with one 32-position group per iteration
+// 4 / 5 / 6 / 7 CTAs 15.26 / 14.73 / 19.7 / 30.0 ms per step (5: 56 registers,
+// 1.3 KB of spills; with two groups 2 / 3 / 4 / 5 CTAs 17.2 / 16.8 / 15.6 /
+// 16.5 ms); with the points in shared memory 3 CTAs lose (config 2 1.40 ->
+// 1.86 ms, config 4 2.48 -> 3.03 ms)
 #ifndef DGX_FWD_CTAS_PTSG
-#define DGX_FWD_CTAS_PTSG 4
+#define DGX_FWD_CTAS_PTSG 5
 #endif
 constexpr int kFwdCtasPerSmPtsG = DGX_FWD_CTAS_PTSG;
 // the forward's SDF parameter stays a by-value copy (measured: as a

@@ -36,6 +36,13 @@
 // 32-position groups the forward classifies per iteration (A/B knob; measured
 // forward ms per step, config 3 / config 2 / config 4: 1 group 15.12 / 1.35 /
 // 2.46, 2 groups 15.62 / 1.40 / 2.49, 3-4 groups slower)
+// out-of-line rare forward paths (A/B knobs)
+#ifndef DGX_CORR_INLINE
+#define DGX_CORR_INLINE __device__ __forceinline__
+#endif
+#ifndef DGX_FRIC_INLINE
+#define DGX_FRIC_INLINE __device__ __forceinline__
+#endif
 #ifndef DGX_FWD_HALVES
 #define DGX_FWD_HALVES 1
 #endif
@@ -296,7 +303,7 @@ struct SimStats {
 
 // ContactSolver::apply_friction (sim.hpp:247-274) on values; returns whether
 // the state changed. Friction-ratio stat as sim.hpp:266-272.
-__device__ __forceinline__ bool friction_fwd(const SimEnv& e, V3 prev_x, Q4 prev_q, V3& x, Q4& q, V3 rb, V3 n,
+DGX_FRIC_INLINE bool friction_fwd(const SimEnv& e, V3 prev_x, Q4 prev_q, V3& x, Q4& q, V3 rb, V3 n,
                                              double lambda_n, SimStats& st, Q4& E, double& sin_half) {
   V3 before = prev_x + rotate(prev_q, rb);
   V3 arm = rotate(q, rb);
@@ -677,7 +684,7 @@ struct CorrOut {
 // active point of the window; logs the correction (state after it) and the
 // contact slot. Called by all lanes of the warp (identical values); lane 0
 // writes the logs.
-__device__ __forceinline__ CorrOut apply_correction(const SimEnv& e, const CorrIn in) {
+DGX_CORR_INLINE CorrOut apply_correction(const SimEnv& e, const CorrIn in) {
   CorrOut out;
   out.x = in.x;
   out.q = in.q;

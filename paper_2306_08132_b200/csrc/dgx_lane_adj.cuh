@@ -12,13 +12,14 @@
 // reference tape's order (tape.cpp:27-114): per position, the leak geometry of
 // the frozen state (sim.hpp:105-125; the same leak_geo / leak_coef as the CTA
 // adjoint), then adj_x <- adj_x - s n and the point adjoint folded into the
-// per-link force / torque sums. No staging, no map composition, no scan and no
-// shuffles. The 32 lanes of a warp are 32 (candidate, sim) tasks walking the
+// per-link force / torque sums. No map composition, no scan and no shuffles.
+// The 32 lanes of a warp are 32 (candidate, sim) tasks walking the
 // SAME position sequence (sweep * N + i, descending) in lockstep, so the point
 // index, its link and the link-change flushes are warp-uniform; only a lane's
 // logged corrections (its run boundaries) diverge. U positions are processed
 // per step: their geometry is independent (issued together: ILP), the
-// recurrence then applies them in order.
+// recurrence then applies them in order. The warp's candidates' points are
+// staged per block of positions in shared memory (cp.async, double-buffered).
 //
 // Logged corrections and frictions are reversed with the same closed forms as
 // the CTA adjoint (correction_linear, friction_adj; dgx_adjoint.cuh), one
@@ -46,8 +47,8 @@ constexpr int kEpiWarps = 4;
 constexpr int kLaneBlk = DGX_LANE_BLK;
 static_assert(kLaneAdjThreads == 32 && kLaneBlk % kLaneU == 0, "lane adjoint: one warp per CTA, windows tile the blocks");
 // staged points: per buffer and candidate of the warp a row of x / y / z for
-// 32 positions; rows 98 doubles apart (196 words: the warp's <= 6 candidates
-// fall on distinct banks)
+// kLaneBlk positions; rows 3 kLaneBlk + 2 doubles apart (with 32: 196 words,
+// so the warp's <= 6 candidates (M = 7) fall on distinct banks)
 constexpr int kLaneRowArr = kLaneBlk, kLaneRow = 3 * kLaneRowArr + 2;
 __host__ __device__ inline int lane_cands_per_warp(int M) { return (31 / M + 2) < 32 ? (31 / M + 2) : 32; }
 __host__ __device__ inline int lane_smem_bytes(int M) { return 2 * lane_cands_per_warp(M) * kLaneRow * 8; }
@@ -57,9 +58,11 @@ __host__ __device__ inline int lane_smem_bytes(int M) { return 2 * lane_cands_pe
 // cell loads: 0 plain (L1 reuse between consecutive points: no_allocate measured
 // 35.9 vs 30.9 ms), 1 L1::no_allocate, 2 L1::evict_first
 constexpr int kLaneCellNoL1 = DGX_LANE_CELL_NOL1;
+// grids: grid_finish_uniform (one normalisation, branch-free outside handling)
 #ifndef DGX_LANE_UNIFORM_FINISH
 #define DGX_LANE_UNIFORM_FINISH 1
 #endif
+// point staging copies with an L2 evict-first policy
 #ifndef DGX_LANE_PTS_EVICT_FIRST
 #define DGX_LANE_PTS_EVICT_FIRST 1
 #endif

@@ -107,8 +107,7 @@ struct FwdRec {
   double x[3];
   double q[4];
   double residual;
-  int ncorr, nslot, nfric, touched, status;
-  int fwd_end;  // first position the forward's quiet-window exit left unclassified (gs N: none)
+  int ncorr, nslot, nfric, touched, status, pad;
 };
 
 // Per (warp slot, step) record of a multi-step perturbation sim

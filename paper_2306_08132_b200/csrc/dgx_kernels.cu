@@ -920,7 +920,6 @@ __device__ double run_sim(const Sdf& sdf, SimEnv& e, V3 v_m, bool record, bool m
   Q4 q = pred_q;
   bool touched = false;
   int ncorr = 0, nslot = 0, nfric = 0;
-  int fwd_end = e.gs * N;  // forward: quiet-window exit position (recorded for the lane adjoint)
   const int nwords = (N + 31) / 32;
   if constexpr (Phase == kPhaseAdj || Phase == kPhaseAdjTask) {
     x = V3{rec->x[0], rec->x[1], rec->x[2]};
@@ -960,10 +959,10 @@ __device__ double run_sim(const Sdf& sdf, SimEnv& e, V3 v_m, bool record, bool m
     int f_last = -1, singular_since = 0;
     while (sweep < e.gs) {
   #if defined(DGX_QUIET) || defined(DGX_QUIET_FWD)  // exact
-      if (sweep * N + pos - f_last - 1 >= N && singular_since == 0) { fwd_end = sweep * N + pos; break; }
+      if (sweep * N + pos - f_last - 1 >= N && singular_since == 0) break;
   #else
       if constexpr (kQuietExit) {
-        if (sweep * N + pos - f_last - 1 >= N && singular_since == 0) { fwd_end = sweep * N + pos; break; }
+        if (sweep * N + pos - f_last - 1 >= N && singular_since == 0) break;
       }
   #endif
       // 32-position groups classified per iteration: the split forward kFwdHalves, the fused kernel 2
@@ -1164,7 +1163,6 @@ __device__ double run_sim(const Sdf& sdf, SimEnv& e, V3 v_m, bool record, bool m
       rec->ncorr = ncorr;
       rec->nslot = nslot;
       rec->nfric = nfric;
-      rec->fwd_end = fwd_end;
     }
     return residual;
   }

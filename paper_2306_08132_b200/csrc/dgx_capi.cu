@@ -280,7 +280,6 @@ struct SplitGrid {
   int chunk, grid_f, grid_a, smem_f, smem_a;
   bool task;  // adjoint as warp tasks (adj_task_kernel) instead of one CTA per candidate
   bool lane;  // adjoint with one thread per (candidate, sim) + the epilogue kernel (the default)
-  bool pc;    // lane adjoint as the producer / consumer pipeline (experimental)
 };
 
 // Split adjoint variant. Default (auto): the lane adjoint
@@ -300,7 +299,6 @@ int adjoint_variant() {  // 0 cta, 1 task, 2 lane, 3 auto
     if (std::strcmp(ev, "cta") == 0) return 0;
     if (std::strcmp(ev, "task") == 0) return 1;
     if (std::strcmp(ev, "lane") == 0) return 2;
-    if (std::strcmp(ev, "pc") == 0) return 4;  // experimental producer / consumer lane adjoint
     return 3;
   }();
   return v;
@@ -328,9 +326,8 @@ SplitGrid prepare_split(dgx_ctx* c, Scratch& sc, const dgx_hand* h, const dgx_ob
   int av = adjoint_variant();
   if (av == 3 && c->adjoint != DGX_ADJOINT_AUTO) av = c->adjoint == DGX_ADJOINT_LANE ? 2 : 0;
   g.task = record && av == 1;
-  g.pc = record && N >= 64 && av == 4;
   g.lane = record && N >= 64 &&  // (the lane adjoint stages blocks of <= 64 positions)
-           (av == 2 || av == 4 || (av == 3 && static_cast<long long>(B) * M * std::max(1, concurrent) >=
+           (av == 2 || (av == 3 && static_cast<long long>(B) * M * std::max(1, concurrent) >=
                                        static_cast<long long>(kLaneMinWarpsPerSm) * 32 * c->num_sms));
   if (g.lane) {
     g.smem_a = 0;
@@ -555,8 +552,7 @@ void launch_range(dgx_ctx* c, Scratch& sc, const dgx_hand* h, const dgx_object* 
       bind_claim(sc, cb, nb, st);
       if (g.lane) {
         counted_launch(c, kPhaseAdj, st, "lane adjoint kernels", [&] {
-          cudaError_t e = g.pc ? launch_pc_adj(h->k, o->k, o->sdf, S, Pk, cb, mode, st)
-                               : launch_lane_adj(h->k, o->k, o->sdf, S, Pk, cb, mode, st);
+          cudaError_t e = launch_lane_adj(h->k, o->k, o->sdf, S, Pk, cb, mode, st);
           if (e != cudaSuccess) return e;
           ++c->launches;  // + the epilogue kernel
           return launch_lane_epi(h->k, S, Pk, cb, mode, st);

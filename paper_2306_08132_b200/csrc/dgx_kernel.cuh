@@ -281,8 +281,6 @@ cudaError_t adj_task_occupancy(int kind, int smem, int* per_sm);
 // the per-candidate epilogue kernel (one warp per candidate)
 cudaError_t launch_lane_adj(const KHand& H, const KObj& O, const SdfSet& sdf, const KSim& S, const KOpt& P,
                             const KBuf& buf, int mode, cudaStream_t st);
-cudaError_t launch_pc_adj(const KHand& H, const KObj& O, const SdfSet& sdf, const KSim& S, const KOpt& P,
-                          const KBuf& buf, int mode, cudaStream_t st);  // experimental (DGX_ADJ=pc)
 cudaError_t launch_lane_epi(const KHand& H, const KSim& S, const KOpt& P, const KBuf& buf, int mode, cudaStream_t st);
 inline bool split_capable(int kind) { return kind != kSdfMesh; }
 // out[n, 8] = rho - radius, grad (3), proxy (3), sign per point (MeshSdf::dilated,

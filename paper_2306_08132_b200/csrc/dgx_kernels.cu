@@ -2284,7 +2284,6 @@ __global__ void __launch_bounds__(32 * kTaskWarps, MinBlocks) adj_task_kernel(co
 }
 
 #include "dgx_lane_adj.cuh"
-#include "dgx_pc_adj.cuh"
 }  // namespace dgx
 
 // ---------------------------------------------------------------------------
@@ -2765,28 +2764,6 @@ static cudaError_t launch_lane_t(const KHand& H, const KObj& O, const Sdf& sdf, 
     return cudaGetLastError();
   }
   return cudaErrorInvalidValue;
-}
-
-template <class Sdf>
-static cudaError_t launch_pc_t(const KHand& H, const KObj& O, const Sdf& sdf, const KSim& S, const KOpt& P,
-                               const KBuf& buf, int mode, cudaStream_t st) {
-  if constexpr (kSplitCapable<Sdf>) {
-    const long long nt = static_cast<long long>(buf.B) * S.M;
-    const int grid = static_cast<int>((nt + 31) / 32);
-    pc_adj_kernel<Sdf><<<grid, 32 * (kPcProd + 1), pc_smem_bytes(), st>>>(H, O, sdf, S, P, buf, mode);
-    return cudaGetLastError();
-  }
-  return cudaErrorInvalidValue;
-}
-
-cudaError_t launch_pc_adj(const KHand& H, const KObj& O, const SdfSet& sdf, const KSim& S, const KOpt& P,
-                          const KBuf& buf, int mode, cudaStream_t st) {
-  switch (sdf.kind) {
-    case kSdfSphere: return launch_pc_t(H, O, sdf.sph, S, P, buf, mode, st);
-    case kSdfBox: return launch_pc_t(H, O, sdf.box, S, P, buf, mode, st);
-    case kSdfGrid: return launch_pc_t(H, O, sdf.grd, S, P, buf, mode, st);
-    default: return cudaErrorInvalidValue;
-  }
 }
 
 cudaError_t launch_lane_adj(const KHand& H, const KObj& O, const SdfSet& sdf, const KSim& S, const KOpt& P,

@@ -63,6 +63,9 @@ constexpr int kLaneCellNoL1 = DGX_LANE_CELL_NOL1;
 #define DGX_LANE_UNIFORM_FINISH 1
 #endif
 // point staging copies with an L2 evict-first policy
+#ifndef DGX_LANE_PTS_FK
+#define DGX_LANE_PTS_FK 0
+#endif
 #ifndef DGX_LANE_PTS_EVICT_FIRST
 #define DGX_LANE_PTS_EVICT_FIRST 1
 #endif
@@ -113,23 +116,57 @@ struct LaneFt {
   }
 };
 
+// Where a position's world point comes from: the warp's staged block
+// (StagedPts) or, with DGX_LANE_PTS_FK, rebuilt from the hand's sample and the
+// candidate's link transform (FkPts: p = R_l s + t_l, the forward's own FK
+// expression, so the same bits; s and the link are warp-uniform, the link
+// transform is reloaded only when the walk changes link).
+struct StagedPts {
+  const double* ps;  // this lane's candidate row of the current block
+  int top;           // position of the row's entry 0
+  __device__ __forceinline__ V3 get(int pos, int) const {
+    const int j = top - pos;
+    DGX_ASSERT(j >= 0 && j < kLaneRowArr);
+    return V3{ps[j], ps[kLaneRowArr + j], ps[2 * kLaneRowArr + j]};
+  }
+};
+struct FkPts {
+  const double* samples;
+  const int* sample_link;
+  const double* links;  // the candidate's link transforms [L][12] (R row-major, t)
+  int cl = -1;
+  M3 R;
+  V3 tr;
+  __device__ __forceinline__ V3 get(int, int i) {
+    const int l = sample_link[i];
+    if (l != cl) {
+#pragma unroll
+      for (int m = 0; m < 9; ++m) R.m[m] = links[12 * l + m];
+      tr = V3{links[12 * l + 9], links[12 * l + 10], links[12 * l + 11]};
+      cl = l;
+    }
+    const V3 sp{samples[3 * i], samples[3 * i + 1], samples[3 * i + 2]};
+    return mul(R, sp) + tr;
+  }
+};
+
 // The leak steps of U consecutive descending positions pos, pos-1, ... (point
 // indices i, i-1, ... wrapping at N) with the frozen state (xk, Rk); slot u
 // takes part iff pos - u > lim (above the lane's next correction). The points
 // come from the warp's staged block (ps: this lane's candidate row, x / y / z
 // at ps[0 / kLaneRowArr / 2 kLaneRowArr + j], j = jb + u).
-template <int U, class Sdf>
+template <int U, class Sdf, class Pts>
 __device__ __forceinline__ void lane_leak_steps(const Sdf& sdf, const SimEnv& e, int pos, int i, int lim, V3 xk,
                                                 const M3& Rk, V3 G, V3& a, M3& aR, LaneFt& acc, double* ftT,
-                                                size_t nt, const double* ps, int jb) {
+                                                size_t nt, Pts& pts) {
   V3 p[U], rel[U], rl[U];
   int ii[U];
   GeoPre<Sdf> pre[U];
 #pragma unroll
   for (int u = 0; u < U; ++u) {
     ii[u] = i - u < 0 ? i - u + e.N : i - u;
-    DGX_ASSERT(jb + u >= 0 && jb + u < kLaneRowArr && ii[u] >= 0 && ii[u] < e.N);
-    p[u] = V3{ps[jb + u], ps[kLaneRowArr + jb + u], ps[2 * kLaneRowArr + jb + u]};
+    DGX_ASSERT(ii[u] >= 0 && ii[u] < e.N);
+    p[u] = pts.get(pos - u, ii[u]);
     rel[u] = p[u] - xk;
     rl[u] = ftmul_add(Rk, rel[u], e.O->com);
     pre[u].fetch(sdf, rl[u]);
@@ -346,11 +383,17 @@ __global__ void __launch_bounds__(kLaneAdjThreads, DGX_LANE_MINB) lane_adj_kerne
     for (int r = 0; r < 9; ++r) aR.m[r] = 0.0;
     LaneFt acc;
     int i = N - 1;
+#if DGX_LANE_PTS_FK
+    FkPts fkp{H.samples, H.sample_link, fkb};
+    (void)sb;
+    (void)rows;
+#else
     stage(top, 0);
+#endif
     int blk = 0, blk_top = top, blk_next = top;
     const double* ps = sb;
     for (int pos = top; pos >= 0; pos -= kLaneU) {
-      if (pos == blk_next) {  // next block: stage the one after it, wait for this one
+      if (!DGX_LANE_PTS_FK && pos == blk_next) {  // next block: stage the one after it, wait for this one
         blk_next = pos - kLaneBlk;
         __syncwarp();  // every lane is done with the buffer about to be refilled
         if (pos - kLaneBlk >= 0) stage(pos - kLaneBlk, (blk + 1) & 1);
@@ -362,8 +405,12 @@ __global__ void __launch_bounds__(kLaneAdjThreads, DGX_LANE_MINB) lane_adj_kerne
         ++blk;
       }
       if (live) {
-        lane_leak_steps<kLaneU>(sdf, e, pos, i, max(next_f, pos - kLaneU), xk, Rk, G, aX, aR, acc, ftT, nt, ps,
-                                blk_top - pos);
+#if DGX_LANE_PTS_FK
+        lane_leak_steps<kLaneU>(sdf, e, pos, i, max(next_f, pos - kLaneU), xk, Rk, G, aX, aR, acc, ftT, nt, fkp);
+#else
+        StagedPts sp{ps, blk_top};
+        lane_leak_steps<kLaneU>(sdf, e, pos, i, max(next_f, pos - kLaneU), xk, Rk, G, aX, aR, acc, ftT, nt, sp);
+#endif
         // this lane's logged corrections inside the window (divergent; rare)
         while (next_f >= 0 && next_f > pos - kLaneU) {  // (next_f = -1: no more corrections)
           const int f = next_f;
@@ -398,13 +445,19 @@ __global__ void __launch_bounds__(kLaneAdjThreads, DGX_LANE_MINB) lane_adj_kerne
           next_f = k >= 0 ? e.corr[k].f : -1;
           // the window's positions below the correction, with the state before it
           for (int p2 = f - 1; p2 > pos - kLaneU && p2 > next_f; --p2)
-            lane_leak_steps<1>(sdf, e, p2, p2 % N, next_f, xk, Rk, G, aX, aR, acc, ftT, nt, ps, blk_top - p2);
+#if DGX_LANE_PTS_FK
+            lane_leak_steps<1>(sdf, e, p2, p2 % N, next_f, xk, Rk, G, aX, aR, acc, ftT, nt, fkp);
+#else
+            lane_leak_steps<1>(sdf, e, p2, p2 % N, next_f, xk, Rk, G, aX, aR, acc, ftT, nt, sp);
+#endif
         }
       }
       i -= kLaneU;
       if (i < 0) i += N;
     }
+#if !DGX_LANE_PTS_FK
     asm volatile("cp.async.wait_all;" ::: "memory");
+#endif
     if (live) {
       acc.flush(ftT, nt);
       if (S.discard) {  // this sim's logs are consumed

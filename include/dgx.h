@@ -181,7 +181,7 @@ int64_t dgx_ctx_launch_count(const dgx_ctx* ctx);
 int dgx_ctx_set_kernel_timing(dgx_ctx* ctx, int enable);
 /* Split-execution adjoint kernel (measurement / testing; no reference
  * counterpart). DGX_ADJOINT_AUTO (default): the lane adjoint (one thread per
- * (candidate, sim)) when the batch gives it >= 4 warps per SM, else the CTA
+ * (candidate, sim)) when the batch gives it >= 3 warps per SM, else the CTA
  * adjoint (one CTA per candidate, bit-identical to the fused kernel).
  * Gradients of the two agree to rounding. The DGX_ADJ
  * environment variable (lane | cta | task) overrides AUTO. */

@@ -286,11 +286,12 @@ struct SplitGrid {
 // (lane_adj_kernel, one thread per (candidate, sim), dgx_lane_adj.cuh) when the
 // batch gives it at least kLaneMinWarpsPerSm warps per SM, else the CTA-per-
 // candidate adjoint (bit-identical to the fused kernel). The lane adjoint's
-// parallelism is its task count: config 3 (4096 x 7 tasks, 6 warps / SM)
-// 30.9 vs 52.3 ms per step; 2048 x 7 tasks (3 warps / SM) 31.8 vs 26.1 ms per
-// 2048 (U = 4 build). DGX_ADJ=lane|cta|task forces one (A/B measurements);
-// DGX_ADJ_TASK=1 is the warp-task adjoint (kept for A/B, never faster).
-constexpr int kLaneMinWarpsPerSm = 4;
+// parallelism is its task count. Config-3 workload, whole step cand-iter/s
+// lane vs CTA (tools/adjoint_crossover.sh): 1024 candidates (1.5 warps / SM)
+// 35.6k vs 57.8k, 2048 (3 warps / SM) 64.5k vs 60.5k, 3072 80.4k vs 57.7k,
+// 4096 (6 warps / SM) 97.7k vs 55.8k. DGX_ADJ=lane|cta|task forces one (A/B
+// measurements); DGX_ADJ_TASK=1 is the warp-task adjoint (never faster).
+constexpr int kLaneMinWarpsPerSm = 3;
 int adjoint_variant() {  // 0 cta, 1 task, 2 lane, 3 auto
   static const int v = [] {
     const char* ev = std::getenv("DGX_ADJ");

@@ -63,6 +63,9 @@ constexpr int kLaneCellNoL1 = DGX_LANE_CELL_NOL1;
 #define DGX_LANE_UNIFORM_FINISH 1
 #endif
 // point staging copies with an L2 evict-first policy
+#ifndef DGX_LANE_RAW_GEO
+#define DGX_LANE_RAW_GEO 1
+#endif
 #ifndef DGX_LANE_PTS_FK
 #define DGX_LANE_PTS_FK 0
 #endif
@@ -77,6 +80,10 @@ template <class Sdf>
 struct GeoPre {
   __device__ __forceinline__ void fetch(const Sdf&, V3) {}
   __device__ __forceinline__ FastEval finish(const Sdf& s, V3 r, double radius) const { return classify(s, r, radius); }
+  __device__ __forceinline__ RawEval finish_raw(const Sdf& s, V3 r, double radius) const {
+    const FastEval fe = classify(s, r, radius);
+    return RawEval{fe.cls, fe.g, fdot(fe.g, fe.g)};
+  }
 };
 template <>
 struct GeoPre<GridSdf> {
@@ -88,6 +95,9 @@ struct GeoPre<GridSdf> {
 #else
     return grid_finish(s, r, f, radius);
 #endif
+  }
+  __device__ __forceinline__ RawEval finish_raw(const GridSdf& s, V3 r, double radius) const {
+    return grid_finish_raw(s, r, f, radius);
   }
 };
 
@@ -176,6 +186,38 @@ __device__ __forceinline__ void lane_leak_steps(const Sdf& sdf, const SimEnv& e,
   bool on[U];
 #pragma unroll
   for (int u = 0; u < U; ++u) {
+#if DGX_LANE_RAW_GEO
+    // the leak coefficients from the unnormalised direction v (|v|^2 = v2):
+    // w = inv_mass + aa.Iw aa with aa = rel x n, n = R v / |v|, so
+    // v2 w = inv_mass v2 + av.Iw av with av = rel x R v; the normalisation
+    // (rsqrt) runs beside that chain instead of in front of it
+    const RawEval fr = pre[u].finish_raw(sdf, rl[u], e.radius);
+    double sg = 1.0;
+    V3 v = fr.v;
+    double v2 = fr.v2;
+    on[u] = pos - u > lim && fr.cls > 0;
+    if (pos - u > lim && fr.cls == 0) {  // near the decision boundary: the exact (bit-exact) query decides
+      PointEval pe;
+      eval_point(sdf, e, ii[u], xk, Rk, true, pe);
+      on[u] = !(pe.rho_d < 0.0);
+      if (on[u]) {
+        v = pe.q.grad;
+        v2 = fdot(v, v);
+        sg = pe.fb ? static_cast<double>(pe.q.sign) : 1.0;
+      }
+    }
+    const V3 nv = fmul(Rk, v);
+    const V3 av = fcross(rel[u], nv);
+    const V3 Iav = fmul(e.O->Iw, av);
+    const double den = fma(e.O->inv_mass, v2, fdot(av, Iav));  // v2 w
+    on[u] = on[u] && den >= 1e-12 * v2;
+    const double inv = rsqrt_pos(v2);
+    const double lpc = v2 * rcp_fast(den);  // 1 / w
+    n[u] = nv * inv;
+    g[u] = v * inv;
+    c1[u] = e.alpha * e.O->inv_mass * lpc * sg;
+    c0[u] = 0.5 * e.alpha * lpc * (fdot(av, G) * inv) * sg;
+#else
     FastEval fe = pre[u].finish(sdf, rl[u], e.radius);
     double sg = 1.0;
     g[u] = fe.g;
@@ -199,6 +241,7 @@ __device__ __forceinline__ void lane_leak_steps(const Sdf& sdf, const SimEnv& e,
     const double lpc = rcp_fast(w);
     c1[u] = e.alpha * e.O->inv_mass * lpc * sg;
     c0[u] = 0.5 * e.alpha * lpc * fdot(aa, G) * sg;
+  #endif
   }
 #pragma unroll
   for (int u = 0; u < U; ++u) {

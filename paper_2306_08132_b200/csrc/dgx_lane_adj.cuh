@@ -63,6 +63,10 @@ constexpr int kLaneCellNoL1 = DGX_LANE_CELL_NOL1;
 #define DGX_LANE_UNIFORM_FINISH 1
 #endif
 // point staging copies with an L2 evict-first policy
+// the R-node adjoint accumulated in the world frame (sum rel (x) n s), mapped back at corrections
+#ifndef DGX_LANE_ARW
+#define DGX_LANE_ARW 1
+#endif
 #ifndef DGX_LANE_RAW_GEO
 #define DGX_LANE_RAW_GEO 1
 #endif
@@ -182,7 +186,10 @@ __device__ __forceinline__ void lane_leak_steps(const Sdf& sdf, const SimEnv& e,
     pre[u].fetch(sdf, rl[u]);
   }
   double c1[U], c0[U];
-  V3 n[U], g[U];
+  V3 n[U];
+#if !(DGX_LANE_ARW && DGX_LANE_RAW_GEO)
+  V3 g[U];  // the local-frame gradient (the emission's R-node term in the local frame)
+#endif
   bool on[U];
 #pragma unroll
   for (int u = 0; u < U; ++u) {
@@ -214,7 +221,9 @@ __device__ __forceinline__ void lane_leak_steps(const Sdf& sdf, const SimEnv& e,
     const double inv = rsqrt_pos(v2);
     const double lpc = v2 * rcp_fast(den);  // 1 / w
     n[u] = nv * inv;
+#if !DGX_LANE_ARW
     g[u] = v * inv;
+#endif
     c1[u] = e.alpha * e.O->inv_mass * lpc * sg;
     c0[u] = 0.5 * e.alpha * lpc * (fdot(av, G) * inv) * sg;
 #else
@@ -249,7 +258,11 @@ __device__ __forceinline__ void lane_leak_steps(const Sdf& sdf, const SimEnv& e,
       const double s = fma(c1[u], fdot(n[u], a), c0[u]);
       a = fma3(-s, n[u], a);
       const V3 a_rel = n[u] * s;
+#if DGX_LANE_ARW
+      outer_acc(aR, rel[u], a_rel);  // world frame: the R node's adjoint is aR R (g = R^T n)
+#else
       outer_acc(aR, rel[u], g[u] * s);
+#endif
       acc.add(ftT, nt, e.sample_link[ii[u]], a_rel, p[u]);
       add_point_grad(e, ii[u], a_rel);
     }
@@ -458,7 +471,17 @@ __global__ void __launch_bounds__(kLaneAdjThreads, DGX_LANE_MINB) lane_adj_kerne
         while (next_f >= 0 && next_f > pos - kLaneU) {  // (next_f = -1: no more corrections)
           const int f = next_f;
           // R node of the state after correction k (read by the run above it)
+#if DGX_LANE_ARW
+          {
+            M3 aRk;  // aR R_k
+            for (int r = 0; r < 3; ++r)
+              for (int cc = 0; cc < 3; ++cc)
+                aRk.m[3 * r + cc] = fma(aR.m[3 * r + 2], Rk.m[6 + cc], fma(aR.m[3 * r + 1], Rk.m[3 + cc], aR.m[3 * r] * Rk.m[cc]));
+            aQ = qadd(aQ, rotmat_adj(qk, aRk));
+          }
+#else
           aQ = qadd(aQ, rotmat_adj(qk, aR));
+#endif
           DGX_ASSERT(k >= 0 && k < e.cap_corr && f >= 0 && f <= pos);
           const CorrRec& c = e.corr[k];
           DGX_ASSERT(c.slot >= 0 && c.slot < e.slot_cap);
@@ -472,7 +495,17 @@ __global__ void __launch_bounds__(kLaneAdjThreads, DGX_LANE_MINB) lane_adj_kerne
           if (!ok) status = kReplayMismatch;
           aX = o.aX;
           aQ = o.aQ;
+#if DGX_LANE_ARW
+          {  // the R node of the state before it, as the world-frame accumulator o.aR R_{k-1}^T
+            const M3 Rb = rotation_matrix(qk);
+            for (int r = 0; r < 3; ++r)
+              for (int cc = 0; cc < 3; ++cc)
+                aR.m[3 * r + cc] = fma(o.aR.m[3 * r + 2], Rb.m[3 * cc + 2],
+                                       fma(o.aR.m[3 * r + 1], Rb.m[3 * cc + 1], o.aR.m[3 * r] * Rb.m[3 * cc]));
+          }
+#else
           aR = o.aR;  // R node of the state before it (continued by the run below)
+#endif
           {
             const int ip = f % N;
             const V3 pp{e.px[ip], e.py[ip], e.pz[ip]};

@@ -67,6 +67,9 @@ constexpr int kLaneCellNoL1 = DGX_LANE_CELL_NOL1;
 #ifndef DGX_LANE_ARW
 #define DGX_LANE_ARW 1
 #endif
+#ifndef DGX_LANE_FMA_U
+#define DGX_LANE_FMA_U 1
+#endif
 #ifndef DGX_LANE_RAW_GEO
 #define DGX_LANE_RAW_GEO 1
 #endif
@@ -92,7 +95,7 @@ struct GeoPre {
 template <>
 struct GeoPre<GridSdf> {
   GridFetch f;
-  __device__ __forceinline__ void fetch(const GridSdf& s, V3 r) { grid_fetch<kLaneCellNoL1>(s, r, f); }
+  __device__ __forceinline__ void fetch(const GridSdf& s, V3 r) { grid_fetch<kLaneCellNoL1, DGX_LANE_FMA_U != 0>(s, r, f); }
   __device__ __forceinline__ FastEval finish(const GridSdf& s, V3 r, double radius) const {
 #if DGX_LANE_UNIFORM_FINISH
     return grid_finish_uniform(s, r, f, radius);
